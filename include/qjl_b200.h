@@ -1,0 +1,162 @@
+/*
+ * qjl_b200.h -- C ABI of the B200-native (sm_100a) QJL decode-time key path.
+ *
+ * Plain C: raw device pointers, sizes, and a cudaStream_t passed as void*.
+ * Every entry point returns an int status (0 = OK, < 0 = error; see
+ * qjl_status_string / qjl_last_error).  The library allocates no persistent
+ * device memory: caches, sketches, outputs and workspaces are owned by the
+ * caller (PyTorch tensors in the Python host layer).  Calls are stream
+ * ordered; readers pass the prefix length `n`, which gives the reference's
+ * "consistent prefix" semantics (kvcache.py:189-196).
+ *
+ * Reference interfaces replaced (paths relative to /root/reference):
+ *   qjl_detect_outliers  <- detect_outliers            pkg/src/qjl/kvcache.py:104-123
+ *   qjl_build_sketch     <- KeyCacheState.create/__init__ sketch split
+ *                                                       pkg/src/qjl/kvcache.py:198-267
+ *   qjl_quantize_keys    <- KeyCacheState.append -> quantize_key (x2 sides)
+ *                                                       pkg/src/qjl/kvcache.py:293-306,
+ *                                                       pkg/src/qjl/estimator.py:110-124
+ *   qjl_sketch_query     <- sketch_query               pkg/src/qjl/estimator.py:127-132
+ *   qjl_scores           <- KeyCacheState.estimate_logits -> _side_logits ->
+ *                           packed_sign_dot_batch       pkg/src/qjl/kvcache.py:311-329,
+ *                                                       pkg/src/qjl/estimator.py:149-170
+ *   qjl_softmax_f64      <- softmax / estimate_scores  pkg/src/qjl/kvcache.py:38-44, :331-337
+ *   qjl_decode           <- quantized_decode (scores + softmax + weights @ values)
+ *                                                       pkg/src/qjl/attention.py:56-71
+ *   qjl_quantize_values  <- quantize_value             pkg/src/qjl/kvcache.py:140-161
+ *
+ * Data layout in HBM (unit = one (batch, kv-head) pair; all arrays unit-major):
+ *   key cache   bits_in  u8  [units][capacity][m_in/8]   LSB-first sign bits; byte-
+ *                                                         identical to the reference's
+ *                                                         LE u64 words when m % 64 == 0
+ *               bits_out u8  [units][capacity][m_out/8]
+ *               norm_in  f16 [units][capacity]           ||k_inlier||_2
+ *               norm_out f16 [units][capacity]           ||k_outlier||_2
+ *   value cache layout P2 (fast path): 2-bit codes, group 32, fp16 zero/scale
+ *               codes u8  [units][capacity][d/4]  in MMA fragment order
+ *               zero  f16 [units][capacity][d/32], scale f16 [units][capacity][d/32]
+ *   value cache layout U8 (reference-format path): 1 byte per code, any bits 1..8,
+ *               any group dividing d, fp32 zero/scale per (token, group).
+ *   sketch      s_full [units or 1][m_in+m_out][d]: rows 0..m_in-1 hold S_in at the
+ *               inlier columns (zeros at outlier columns), rows m_in.. hold S_out at
+ *               the outlier columns -- one zero-padded K=d GEMM per unit.
+ */
+#ifndef QJL_B200_H
+#define QJL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QJL_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define QJL_API __attribute__((visibility("default")))
+#else
+#define QJL_API
+#endif
+
+enum {
+  QJL_OK = 0,
+  QJL_ERR_ARG = -1,          /* shape / parameter error  -> Python ValueError   */
+  QJL_ERR_UNSUPPORTED = -2,  /* valid but unsupported configuration             */
+  QJL_ERR_CUDA = -3,         /* CUDA runtime / launch error -> RuntimeError     */
+  QJL_ERR_WORKSPACE = -4,    /* workspace too small                             */
+  QJL_ERR_EMPTY = -5         /* empty cache (kvcache.py:324-325)                */
+};
+
+enum { QJL_F32 = 0, QJL_F16 = 1, QJL_BF16 = 2, QJL_F64 = 3 };
+enum { QJL_VLAYOUT_U8 = 0, QJL_VLAYOUT_P2 = 1 };
+
+typedef struct qjl_key_cache {
+  uint8_t* bits_in;
+  uint8_t* bits_out;   /* NULL when m_out == 0 */
+  uint16_t* norm_in;
+  uint16_t* norm_out;  /* NULL when m_out == 0 */
+  int64_t capacity;
+  int32_t units, d, m_in, m_out;
+} qjl_key_cache_t;
+
+typedef struct qjl_value_cache {
+  void* codes;
+  void* zero;
+  void* scale;
+  int64_t capacity;
+  int32_t units, d, bits, group, layout;
+} qjl_value_cache_t;
+
+typedef struct qjl_sketch {
+  const void* s_full;   /* [units or 1][m_in + m_out][d] */
+  int32_t dtype;        /* QJL_F64 / QJL_F32 / QJL_BF16 / QJL_F16 */
+  int32_t pad_;
+  int64_t unit_stride;  /* elements between consecutive units; 0 = shared */
+} qjl_sketch_t;
+
+QJL_API int qjl_abi_version(void);
+QJL_API const char* qjl_status_string(int status);
+/* Detail message of the last failing call on this host thread. */
+QJL_API const char* qjl_last_error(void);
+/* SM count / compute capability of the current device. */
+QJL_API int qjl_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* Outlier profile per unit: top-h channels by mean |k| over n0 prompt rows,
+ * fp64 accumulation, ties -> lower index, channels sorted ascending.
+ * keys: [units][n0][d] (rows contiguous, unit stride in elements).
+ * channels: int32 [units][h]; magnitudes: f64 [units][d] (may be NULL). */
+QJL_API int qjl_detect_outliers(const void* keys, int dtype, int units, int64_t n0, int d,
+                        int64_t unit_stride, int h, int32_t* channels,
+                        double* magnitudes, void* stream);
+
+/* Build per-unit zero-padded sketches from device fp64 S_in [m_in][d-h] and
+ * S_out [m_out][h] (either may be NULL when its side is empty) and channels
+ * [units][h].  Output s_full [units][m_in+m_out][d] in `dtype` (RN rounding). */
+QJL_API int qjl_build_sketch(const double* s_in, const double* s_out, int m_in, int m_out,
+                     int d, int h, const int32_t* channels, int units, int dtype,
+                     void* s_full, void* stream);
+
+/* K1: append n keys per unit at rows [row_offset, row_offset + n).
+ * keys: [units][n][d] with `key_unit_stride` elements between units.
+ * channels: [units][h] outlier channels (for the norm split), may be NULL if h == 0. */
+QJL_API int qjl_quantize_keys(const void* keys, int dtype, int64_t n, int64_t key_unit_stride,
+                      const qjl_sketch_t* sketch, const int32_t* channels, int h,
+                      const qjl_key_cache_t* cache, int64_t row_offset, void* stream);
+
+/* S_full @ q per unit and query head: q [units][G][d] -> sq f32 [units][G][m_in+m_out]. */
+QJL_API int qjl_sketch_query(const void* q, int q_dtype, int units, int G, int d,
+                     const qjl_sketch_t* sketch, int m_total, float* sq, void* stream);
+
+/* K2: logits [units][G][n] (f32) of G query heads per unit over the first n keys. */
+QJL_API size_t qjl_scores_workspace(int units, int G, int m_total);
+QJL_API int qjl_scores(const qjl_key_cache_t* cache, int64_t n, const void* q, int q_dtype, int G,
+               const qjl_sketch_t* sketch, float* logits, void* workspace,
+               size_t workspace_bytes, void* stream);
+
+/* packed_sign_dot_batch: out f64 [G][n] = 2 * sum_{set bits of row i} values[g] - sum(values[g])
+ * for n packed rows of m bits (row_bytes apart, m % 32 == 0), values f64 [G][m]. */
+QJL_API int qjl_sign_dot_batch(const uint8_t* bits, int64_t n, int m, int64_t row_bytes,
+                               const double* values, int G, double* out, void* stream);
+
+/* Row softmax in fp64 of logits * inv_temperature: [rows][n] -> weights f64. */
+QJL_API int qjl_softmax_f64(const float* logits, int64_t rows, int64_t n, double inv_temperature,
+                    double* weights, void* stream);
+
+/* K2+K3 fused decode: out [units][G][d] f32 = softmax(logits * inv_temperature) @ V.
+ * lse (optional, may be NULL): [units][G] f32 log-sum-exp of the scaled logits. */
+QJL_API size_t qjl_decode_workspace(const qjl_key_cache_t* cache, const qjl_value_cache_t* values,
+                            int64_t n, int G);
+QJL_API int qjl_decode(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int64_t n,
+               const void* q, int q_dtype, int G, const qjl_sketch_t* sketch,
+               float inv_temperature, float* out, float* lse, void* workspace,
+               size_t workspace_bytes, void* stream);
+
+/* Value quantizer: v [units][n][d] -> value cache rows [row_offset, row_offset + n). */
+QJL_API int qjl_quantize_values(const void* v, int dtype, int64_t n, int64_t unit_stride,
+                        const qjl_value_cache_t* values, int64_t row_offset, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QJL_B200_H */

@@ -1,0 +1,303 @@
+// C ABI entry points (include/qjl_b200.h): argument validation mirroring the
+// reference's ValueError conditions, then stream-ordered launches.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace qjl {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  set_error("%s: CUDA error %d (%s)", what, (int)e, cudaGetErrorString(e));
+  return QJL_ERR_CUDA;
+}
+
+int device_sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cached[dev] = sms;
+  return sms;
+}
+
+static bool valid_dtype(int dt) { return dt == QJL_F32 || dt == QJL_F16 || dt == QJL_BF16 || dt == QJL_F64; }
+
+static int check_key_cache(const qjl_key_cache_t* kc) {
+  QJL_CHECK_ARG(kc != nullptr, "key cache descriptor is NULL");
+  QJL_CHECK_ARG(kc->units >= 1, "units must be >= 1 (got %d)", kc->units);
+  QJL_CHECK_ARG(kc->d >= 1 && kc->d <= 1024, "head dim d must be in [1, 1024] (got %d)", kc->d);
+  QJL_CHECK_ARG(kc->m_in >= 0 && kc->m_out >= 0 && kc->m_in + kc->m_out >= 1,
+                "sketch sizes must be non-negative with m_in + m_out >= 1");
+  if (kc->m_in % 32 || kc->m_out % 32) {
+    set_error("device path packs sketch bits in 32-bit words: m_in=%d, m_out=%d must be multiples of 32",
+              kc->m_in, kc->m_out);
+    return QJL_ERR_UNSUPPORTED;
+  }
+  if (kc->m_in + kc->m_out > 1024) {
+    set_error("m_in + m_out = %d exceeds 1024", kc->m_in + kc->m_out);
+    return QJL_ERR_UNSUPPORTED;
+  }
+  QJL_CHECK_ARG(kc->m_in == 0 || (kc->bits_in && kc->norm_in), "bits_in/norm_in must be set when m_in > 0");
+  QJL_CHECK_ARG(kc->m_out == 0 || (kc->bits_out && kc->norm_out), "bits_out/norm_out must be set when m_out > 0");
+  QJL_CHECK_ARG(kc->capacity >= 0, "capacity must be >= 0");
+  return QJL_OK;
+}
+
+static int check_value_cache(const qjl_value_cache_t* vc, int d, int units) {
+  QJL_CHECK_ARG(vc != nullptr, "value cache descriptor is NULL");
+  QJL_CHECK_ARG(vc->codes && vc->zero && vc->scale, "value cache pointers must be set");
+  QJL_CHECK_ARG(vc->d == d, "value dim %d != key dim %d", vc->d, d);
+  QJL_CHECK_ARG(vc->units == units, "value units %d != key units %d", vc->units, units);
+  QJL_CHECK_ARG(vc->bits >= 1 && vc->bits <= 8, "value bit width must be in [1, 8], got %d", vc->bits);
+  QJL_CHECK_ARG(vc->group >= 1 && d % vc->group == 0, "value group %d must divide d=%d", vc->group, d);
+  if (vc->layout == QJL_VLAYOUT_P2) {
+    if (!(d == 128 && vc->bits == 2 && vc->group == 32)) {
+      set_error("P2 value layout is 2-bit, group 32, d = 128 (got d=%d bits=%d group=%d)", d, vc->bits, vc->group);
+      return QJL_ERR_UNSUPPORTED;
+    }
+  } else {
+    QJL_CHECK_ARG(vc->layout == QJL_VLAYOUT_U8, "unknown value layout %d", vc->layout);
+  }
+  if (d > 128) {
+    set_error("decode supports head dim <= 128 (got %d)", d);
+    return QJL_ERR_UNSUPPORTED;
+  }
+  return QJL_OK;
+}
+
+static int check_sketch(const qjl_sketch_t* sk) {
+  QJL_CHECK_ARG(sk != nullptr && sk->s_full != nullptr, "sketch is NULL");
+  QJL_CHECK_ARG(valid_dtype(sk->dtype), "bad sketch dtype %d", sk->dtype);
+  QJL_CHECK_ARG(sk->unit_stride >= 0, "sketch unit stride must be >= 0");
+  return QJL_OK;
+}
+
+}  // namespace qjl
+
+using namespace qjl;
+
+#define QJL_TRY(expr)              \
+  do {                             \
+    int rc_ = (expr);              \
+    if (rc_ != QJL_OK) return rc_; \
+  } while (0)
+
+extern "C" {
+
+int qjl_abi_version(void) { return QJL_ABI_VERSION; }
+
+const char* qjl_status_string(int status) {
+  switch (status) {
+    case QJL_OK: return "ok";
+    case QJL_ERR_ARG: return "invalid argument";
+    case QJL_ERR_UNSUPPORTED: return "unsupported configuration";
+    case QJL_ERR_CUDA: return "CUDA error";
+    case QJL_ERR_WORKSPACE: return "workspace too small";
+    case QJL_ERR_EMPTY: return "cache is empty";
+  }
+  return "unknown status";
+}
+
+const char* qjl_last_error(void) { return g_err; }
+
+int qjl_device_info(int* sm_count, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+  if (sm_count) *sm_count = device_sm_count();
+  if (cc_major) cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (cc_minor) cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return QJL_OK;
+}
+
+int qjl_detect_outliers(const void* keys, int dtype, int units, int64_t n0, int d,
+                        int64_t unit_stride, int h, int32_t* channels, double* magnitudes,
+                        void* stream) {
+  QJL_CHECK_ARG(keys != nullptr, "keys is NULL");
+  QJL_CHECK_ARG(valid_dtype(dtype), "bad key dtype %d", dtype);
+  QJL_CHECK_ARG(units >= 1, "units must be >= 1");
+  QJL_CHECK_ARG(n0 >= 1, "prompt keys must be a non-empty n x d matrix");
+  QJL_CHECK_ARG(d >= 1 && d <= 1024, "d must be in [1, 1024]");
+  QJL_CHECK_ARG(h >= 0 && h <= d, "outlier count must be in [0, %d], got %d", d, h);
+  QJL_CHECK_ARG(h == 0 || channels != nullptr, "channels output is NULL");
+  QJL_CHECK_ARG(unit_stride >= n0 * d, "unit stride %lld < n0*d", (long long)unit_stride);
+  return launch_detect_outliers(keys, dtype, units, n0, d, unit_stride, h, channels, magnitudes,
+                                (cudaStream_t)stream);
+}
+
+int qjl_build_sketch(const double* s_in, const double* s_out, int m_in, int m_out, int d, int h,
+                     const int32_t* channels, int units, int dtype, void* s_full, void* stream) {
+  QJL_CHECK_ARG(s_full != nullptr, "s_full is NULL");
+  QJL_CHECK_ARG(valid_dtype(dtype), "bad sketch dtype %d", dtype);
+  QJL_CHECK_ARG(d >= 1 && d <= 1024 && h >= 0 && h <= d, "bad d/h");
+  QJL_CHECK_ARG(units >= 1, "units must be >= 1");
+  QJL_CHECK_ARG((s_in == nullptr) == (m_in == 0) && (m_in == 0) == (d - h == 0),
+                "inlier sketch must be present exactly when d - h > 0");
+  QJL_CHECK_ARG((s_out == nullptr) == (m_out == 0) && (m_out == 0) == (h == 0),
+                "outlier sketch must be present exactly when h > 0");
+  QJL_CHECK_ARG(h == 0 || channels != nullptr, "channels is NULL");
+  if (h > 0 && d - h > 0 && (int64_t)m_out * (d - h) < (int64_t)m_in * h) {
+    set_error("outlier bit rate below inlier bit rate: m_out/h = %d/%d < m_in/(d-h) = %d/%d", m_out, h,
+              m_in, d - h);
+    return QJL_ERR_ARG;  // kvcache.py:219-226
+  }
+  return launch_build_sketch(s_in, s_out, m_in, m_out, d, h, channels, units, dtype, s_full,
+                             (cudaStream_t)stream);
+}
+
+int qjl_quantize_keys(const void* keys, int dtype, int64_t n, int64_t key_unit_stride,
+                      const qjl_sketch_t* sketch, const int32_t* channels, int h,
+                      const qjl_key_cache_t* cache, int64_t row_offset, void* stream) {
+  QJL_TRY(check_key_cache(cache));
+  QJL_TRY(check_sketch(sketch));
+  QJL_CHECK_ARG(keys != nullptr, "keys is NULL");
+  QJL_CHECK_ARG(valid_dtype(dtype), "bad key dtype %d", dtype);
+  QJL_CHECK_ARG(n >= 0 && row_offset >= 0 && row_offset + n <= cache->capacity,
+                "rows [%lld, %lld) exceed capacity %lld", (long long)row_offset,
+                (long long)(row_offset + n), (long long)cache->capacity);
+  QJL_CHECK_ARG(h >= 0 && h <= cache->d && (h == 0 || channels), "bad outlier channels");
+  QJL_CHECK_ARG((h > 0) == (cache->m_out > 0), "outlier sketch must be present exactly when h > 0");
+  QJL_CHECK_ARG(key_unit_stride >= n * cache->d, "key unit stride too small");
+  if (n == 0) return QJL_OK;
+  int rc = launch_quantize_keys_tc(keys, dtype, n, key_unit_stride, *sketch, channels, h, *cache,
+                                   row_offset, (cudaStream_t)stream);
+  if (rc != QJL_ERR_UNSUPPORTED) return rc;
+  return launch_quantize_keys_simt(keys, dtype, n, key_unit_stride, *sketch, channels, h, *cache,
+                                   row_offset, (cudaStream_t)stream);
+}
+
+int qjl_sketch_query(const void* q, int q_dtype, int units, int G, int d, const qjl_sketch_t* sketch,
+                     int m_total, float* sq, void* stream) {
+  QJL_TRY(check_sketch(sketch));
+  QJL_CHECK_ARG(q && sq, "NULL pointer");
+  QJL_CHECK_ARG(valid_dtype(q_dtype), "bad query dtype %d", q_dtype);
+  QJL_CHECK_ARG(units >= 1 && G >= 1 && d >= 1 && d <= 1024 && m_total >= 1, "bad shape");
+  return launch_sketch_query(q, q_dtype, units, G, d, *sketch, m_total, m_total, sq, nullptr,
+                             (cudaStream_t)stream);
+}
+
+size_t qjl_scores_workspace(int units, int G, int m_total) {
+  return (size_t)units * G * (m_total + 2) * sizeof(float);
+}
+
+int qjl_scores(const qjl_key_cache_t* cache, int64_t n, const void* q, int q_dtype, int G,
+               const qjl_sketch_t* sketch, float* logits, void* workspace, size_t workspace_bytes,
+               void* stream) {
+  QJL_TRY(check_key_cache(cache));
+  QJL_TRY(check_sketch(sketch));
+  QJL_CHECK_ARG(q && logits, "NULL pointer");
+  QJL_CHECK_ARG(valid_dtype(q_dtype), "bad query dtype %d", q_dtype);
+  QJL_CHECK_ARG(G >= 1, "G must be >= 1");
+  if (n <= 0) {
+    set_error("cache is empty; append at least one key first");
+    return QJL_ERR_EMPTY;
+  }
+  QJL_CHECK_ARG(n <= cache->capacity, "n exceeds capacity");
+  const int m_total = cache->m_in + cache->m_out;
+  if (workspace_bytes < qjl_scores_workspace(cache->units, G, m_total) || !workspace) {
+    set_error("scores workspace needs %zu bytes", qjl_scores_workspace(cache->units, G, m_total));
+    return QJL_ERR_WORKSPACE;
+  }
+  float* sq = (float*)workspace;
+  float* sums = sq + (size_t)cache->units * G * m_total;
+  cudaStream_t st = (cudaStream_t)stream;
+  QJL_TRY(launch_sketch_query(q, q_dtype, cache->units, G, cache->d, *sketch, cache->m_in, m_total,
+                              sq, sums, st));
+  return launch_scores_simt(*cache, n, G, sq, sums, logits, st);
+}
+
+int qjl_sign_dot_batch(const uint8_t* bits, int64_t n, int m, int64_t row_bytes,
+                       const double* values, int G, double* out, void* stream) {
+  QJL_CHECK_ARG(bits && values && out, "NULL pointer");
+  QJL_CHECK_ARG(n >= 1 && G >= 1 && m >= 1, "bad shape");
+  if (m % 32 || row_bytes % 4 || row_bytes * 8 < m) {
+    set_error("sign_dot_batch needs m %% 32 == 0 and 4-byte aligned rows (m=%d, row_bytes=%lld)", m,
+              (long long)row_bytes);
+    return QJL_ERR_UNSUPPORTED;
+  }
+  if ((size_t)G * (m + 1) * 8 > 200 * 1024) {
+    set_error("sign_dot_batch: G*m too large");
+    return QJL_ERR_UNSUPPORTED;
+  }
+  return launch_sign_dot_batch(bits, n, m, row_bytes, values, G, out, (cudaStream_t)stream);
+}
+
+int qjl_softmax_f64(const float* logits, int64_t rows, int64_t n, double inv_temperature,
+                    double* weights, void* stream) {
+  QJL_CHECK_ARG(logits && weights, "NULL pointer");
+  QJL_CHECK_ARG(rows >= 1 && n >= 1, "bad shape");
+  QJL_CHECK_ARG(inv_temperature > 0, "temperature must be positive");
+  return launch_softmax_f64(logits, rows, n, inv_temperature, weights, (cudaStream_t)stream);
+}
+
+size_t qjl_decode_workspace(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int64_t n,
+                            int G) {
+  if (!cache || !values || n <= 0 || G <= 0) return 0;
+  const int m_total = cache->m_in + cache->m_out;
+  size_t a = decode_simt_workspace(cache->units, n, G, values->d, m_total);
+  if (decode_tc_supported(*cache, *values, G)) {
+    size_t b = decode_tc_workspace(*cache, *values, n, G);
+    return a > b ? a : b;
+  }
+  return a;
+}
+
+int qjl_decode(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int64_t n, const void* q,
+               int q_dtype, int G, const qjl_sketch_t* sketch, float inv_temperature, float* out,
+               float* lse, void* workspace, size_t workspace_bytes, void* stream) {
+  QJL_TRY(check_key_cache(cache));
+  QJL_TRY(check_value_cache(values, cache->d, cache->units));
+  QJL_TRY(check_sketch(sketch));
+  QJL_CHECK_ARG(q && out, "NULL pointer");
+  QJL_CHECK_ARG(valid_dtype(q_dtype), "bad query dtype %d", q_dtype);
+  QJL_CHECK_ARG(G >= 1, "G must be >= 1");
+  QJL_CHECK_ARG(inv_temperature > 0.f, "temperature must be positive");
+  if (n <= 0) {
+    set_error("cache is empty");
+    return QJL_ERR_EMPTY;
+  }
+  QJL_CHECK_ARG(n <= cache->capacity && n <= values->capacity, "n exceeds capacity");
+  const size_t need = qjl_decode_workspace(cache, values, n, G);
+  if (!workspace || workspace_bytes < need) {
+    set_error("decode workspace needs %zu bytes (got %zu)", need, workspace_bytes);
+    return QJL_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (decode_tc_supported(*cache, *values, G))
+    return launch_decode_tc(*cache, *values, n, q, q_dtype, G, *sketch, inv_temperature, out, lse,
+                            workspace, workspace_bytes, st);
+  const int m_total = cache->m_in + cache->m_out;
+  float* sq = (float*)workspace;
+  float* sums = sq + (size_t)cache->units * G * m_total;
+  float* part = sums + (size_t)cache->units * G * 2;
+  QJL_TRY(launch_sketch_query(q, q_dtype, cache->units, G, cache->d, *sketch, cache->m_in, m_total,
+                              sq, sums, st));
+  return launch_decode_simt(*cache, *values, n, G, sq, sums, inv_temperature, out, lse, part, st);
+}
+
+int qjl_quantize_values(const void* v, int dtype, int64_t n, int64_t unit_stride,
+                        const qjl_value_cache_t* values, int64_t row_offset, void* stream) {
+  QJL_CHECK_ARG(v != nullptr, "values is NULL");
+  QJL_CHECK_ARG(valid_dtype(dtype), "bad value dtype %d", dtype);
+  QJL_TRY(check_value_cache(values, values ? values->d : 0, values ? values->units : 0));
+  QJL_CHECK_ARG(n >= 0 && row_offset >= 0 && row_offset + n <= values->capacity,
+                "rows exceed value capacity");
+  QJL_CHECK_ARG(unit_stride >= n * values->d, "value unit stride too small");
+  if (n == 0) return QJL_OK;
+  return launch_quantize_values(v, dtype, n, unit_stride, *values, row_offset, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,386 @@
+// Prefill-side kernels: outlier profile, per-unit sketch build, generic (SIMT)
+// key quantizer, value quantizer.  The tcgen05 tensor-core key quantizer for
+// bf16/fp16 keys lives in k_quant_tc.cu; this file's quantizer handles every
+// dtype with fp64 accumulation (fp32 keys, odd shapes, single-key shims).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace qjl {
+
+// ---------------------------------------------------------------------------
+// detect_outliers (kvcache.py:104-123): mean |k| per channel in fp64, top-h by
+// (magnitude desc, index asc), emitted sorted ascending.  One CTA per unit:
+// deterministic summation order, no atomics.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(1024) k_detect_outliers(const T* __restrict__ keys, int64_t n0,
+                                                          int d, int64_t unit_stride, int h,
+                                                          int32_t* __restrict__ channels,
+                                                          double* __restrict__ magnitudes) {
+  extern __shared__ double sm_mag[];  // [rows_par][d] partials, then [d] means
+  const int u = blockIdx.x;
+  const T* K = keys + (int64_t)u * unit_stride;
+  const int rows_par = blockDim.x / d;  // blockDim.x is a multiple of d
+  const int c = threadIdx.x % d, rp = threadIdx.x / d;
+  double acc = 0.0;
+  if (rp < rows_par) {
+    for (int64_t r = rp; r < n0; r += rows_par) acc += fabs(to_f64(K[r * d + c]));
+    sm_mag[rp * d + c] = acc;
+  }
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < d)
+    for (int i = 0; i < rows_par; ++i) s += sm_mag[i * d + threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < d) sm_mag[threadIdx.x] = s / (double)n0;
+  __syncthreads();
+  __shared__ int sel[1024];
+  if (threadIdx.x < d) {
+    const double mc = sm_mag[threadIdx.x];
+    int rank = 0;
+    for (int j = 0; j < d; ++j) {
+      const double mj = sm_mag[j];
+      rank += (mj > mc) || (mj == mc && j < (int)threadIdx.x);
+    }
+    sel[threadIdx.x] = rank < h;
+    if (magnitudes) magnitudes[(int64_t)u * d + threadIdx.x] = mc;
+  }
+  __syncthreads();
+  if (threadIdx.x < d && sel[threadIdx.x]) {
+    int pos = 0;
+    for (int j = 0; j < (int)threadIdx.x; ++j) pos += sel[j];
+    channels[(int64_t)u * h + pos] = threadIdx.x;
+  }
+}
+
+int launch_detect_outliers(const void* keys, int dtype, int units, int64_t n0, int d,
+                           int64_t unit_stride, int h, int32_t* channels, double* mags,
+                           cudaStream_t st) {
+  const int rows_par = (1024 / d) > 0 ? 1024 / d : 1;
+  const int threads = rows_par * d;
+  const size_t smem = (size_t)rows_par * d * sizeof(double);
+  switch (dtype) {
+#define QJL_DET(DT)                                                                         \
+  case DT: {                                                                                \
+    auto kern = k_detect_outliers<Elem<DT>::T>;                                             \
+    if (smem > 48 * 1024)                                                                   \
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+    kern<<<units, threads, smem, st>>>((const Elem<DT>::T*)keys, n0, d, unit_stride, h,     \
+                                       channels, mags);                                     \
+    break;                                                                                  \
+  }
+    QJL_DET(QJL_F32)
+    QJL_DET(QJL_F16)
+    QJL_DET(QJL_BF16)
+    QJL_DET(QJL_F64)
+#undef QJL_DET
+    default: return QJL_ERR_ARG;
+  }
+  QJL_LAUNCH_CHECK("detect_outliers");
+  return QJL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Per-unit zero-padded sketch: rows [0, m_in) carry S_in at the
+// inlier columns in ascending order, rows [m_in, m_in+m_out) carry S_out at the
+// outlier columns; everything else is 0.  Rounded once to the operand dtype.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_build_sketch(const double* __restrict__ s_in, const double* __restrict__ s_out,
+                               int m_in, int m_out, int d, int h,
+                               const int32_t* __restrict__ channels, T* __restrict__ s_full) {
+  __shared__ int rank_in[1024];
+  __shared__ int rank_out[1024];
+  const int u = blockIdx.y;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    int ro = -1, below = 0;
+    for (int j = 0; j < h; ++j) {
+      const int ch = channels[(int64_t)u * h + j];
+      ro = (ch == c) ? j : ro;
+      below += ch < c;
+    }
+    rank_out[c] = ro;
+    rank_in[c] = ro >= 0 ? -1 : c - below;
+  }
+  __syncthreads();
+  const int m_total = m_in + m_out;
+  const int d_in = d - h;
+  T* out = s_full + (int64_t)u * m_total * d;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < m_total * d;
+       idx += gridDim.x * blockDim.x) {
+    const int r = idx / d, c = idx % d;
+    double v = 0.0;
+    if (r < m_in) {
+      if (rank_in[c] >= 0) v = s_in[(int64_t)r * d_in + rank_in[c]];
+    } else if (rank_out[c] >= 0) {
+      v = s_out[(int64_t)(r - m_in) * h + rank_out[c]];
+    }
+    out[idx] = from_f64<T>(v);
+  }
+}
+
+int launch_build_sketch(const double* s_in, const double* s_out, int m_in, int m_out, int d,
+                        int h, const int32_t* channels, int units, int dtype, void* s_full,
+                        cudaStream_t st) {
+  const int m_total = m_in + m_out;
+  dim3 grid((m_total * d + 255) / 256 < 64 ? (m_total * d + 255) / 256 : 64, units);
+  switch (dtype) {
+#define QJL_BS(DT)                                                                      \
+  case DT:                                                                              \
+    k_build_sketch<Elem<DT>::T><<<grid, 256, 0, st>>>(s_in, s_out, m_in, m_out, d, h,   \
+                                                      channels, (Elem<DT>::T*)s_full);  \
+    break;
+    QJL_BS(QJL_F32)
+    QJL_BS(QJL_F16)
+    QJL_BS(QJL_BF16)
+    QJL_BS(QJL_F64)
+#undef QJL_BS
+    default: return QJL_ERR_ARG;
+  }
+  QJL_LAUNCH_CHECK("build_sketch");
+  return QJL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Generic key quantizer (estimator.py:110-124 batched, kvcache.py:293-306):
+// projections in fp64 (exact products, fp64 sums), sign test `p >= 0` (ties and
+// -0.0 -> 1, NaN -> 0), bits packed with warp ballots: lane j of a warp owns
+// sketch row 32w+j, so the ballot word IS the LSB-first u32 of those 32 rows.
+// Norms ||k_in||, ||k_out|| in fp64, rounded once to fp16.
+// CTA = 256 threads, kTok tokens; S is staged through smem kCk columns at a time.
+// ---------------------------------------------------------------------------
+constexpr int kQTok = 16;
+constexpr int kQCk = 16;
+constexpr int kQThreads = 256;
+
+template <typename TK, typename TS, int RPT>
+__global__ void __launch_bounds__(kQThreads) k_quantize_keys_simt(
+    const TK* __restrict__ keys, int64_t n, int64_t key_unit_stride, const TS* __restrict__ s_full,
+    int64_t s_unit_stride, int d, int m_in, int m_out, const int32_t* __restrict__ channels, int h,
+    qjl_key_cache_t kc, int64_t row_offset) {
+  extern __shared__ double sm[];
+  const int m_total = m_in + m_out;
+  double* sk = sm;                         // [kQTok][d]
+  double* ss = sm + kQTok * d;             // [m_total][kQCk + 1]
+  __shared__ unsigned char is_out[1024];
+  const int u = blockIdx.y;
+  const int64_t t0 = (int64_t)blockIdx.x * kQTok;
+  const TK* K = keys + (int64_t)u * key_unit_stride;
+  const TS* S = s_full + (int64_t)u * s_unit_stride;
+
+  for (int c = threadIdx.x; c < d; c += blockDim.x) is_out[c] = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < h; j += blockDim.x) is_out[channels[(int64_t)u * h + j]] = 1;
+  for (int i = threadIdx.x; i < kQTok * d; i += blockDim.x) {
+    const int tt = i / d, c = i % d;
+    sk[i] = (t0 + tt < n) ? to_f64(K[(t0 + tt) * d + c]) : 0.0;
+  }
+
+  double acc[RPT][kQTok];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i)
+#pragma unroll
+    for (int t = 0; t < kQTok; ++t) acc[i][t] = 0.0;
+
+  for (int c0 = 0; c0 < d; c0 += kQCk) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < m_total * kQCk; i += blockDim.x) {
+      const int r = i / kQCk, cc = i % kQCk;
+      ss[r * (kQCk + 1) + cc] = (c0 + cc < d) ? to_f64(S[(int64_t)r * d + c0 + cc]) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int r = threadIdx.x + i * kQThreads;
+      if (r < m_total) {
+        for (int cc = 0; cc < kQCk && c0 + cc < d; ++cc) {
+          const double s = ss[r * (kQCk + 1) + cc];
+#pragma unroll
+          for (int t = 0; t < kQTok; ++t) acc[i][t] = fma(s, sk[t * d + c0 + cc], acc[i][t]);
+        }
+      }
+    }
+  }
+
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int r0 = (threadIdx.x & ~31) + i * kQThreads;  // warp-uniform first row
+    if (r0 >= m_total) continue;
+#pragma unroll
+    for (int t = 0; t < kQTok; ++t) {
+      const unsigned word = __ballot_sync(0xffffffffu, acc[i][t] >= 0.0);
+      const int64_t row = row_offset + t0 + t;
+      if (lane == 0 && t0 + t < n) {
+        if (r0 < m_in) {
+          reinterpret_cast<uint32_t*>(kc.bits_in + ((int64_t)u * kc.capacity + row) * (m_in / 8))[r0 / 32] = word;
+        } else {
+          reinterpret_cast<uint32_t*>(kc.bits_out + ((int64_t)u * kc.capacity + row) * (m_out / 8))[(r0 - m_in) / 32] = word;
+        }
+      }
+    }
+  }
+
+  // norms: one warp per token
+  const int warp = threadIdx.x >> 5;
+  for (int t = warp; t < kQTok; t += kQThreads / 32) {
+    if (t0 + t >= n) continue;
+    double s_in = 0.0, s_out = 0.0;
+    for (int c = lane; c < d; c += 32) {
+      const double v = sk[t * d + c];
+      if (is_out[c]) s_out = fma(v, v, s_out); else s_in = fma(v, v, s_in);
+    }
+    s_in = warp_sum_f64(s_in);
+    s_out = warp_sum_f64(s_out);
+    if (lane == 0) {
+      const int64_t row = (int64_t)u * kc.capacity + row_offset + t0 + t;
+      kc.norm_in[row] = f64_to_f16_bits(sqrt(s_in));
+      if (m_out > 0) kc.norm_out[row] = f64_to_f16_bits(sqrt(s_out));
+    }
+  }
+}
+
+template <typename TK, typename TS>
+static int launch_qk_simt_2(const void* keys, int64_t n, int64_t kus, const void* s, int64_t sus,
+                            int d, int m_in, int m_out, const int32_t* ch, int h,
+                            const qjl_key_cache_t& kc, int64_t row_offset, cudaStream_t st) {
+  const int m_total = m_in + m_out;
+  const int rpt = (m_total + kQThreads - 1) / kQThreads;
+  const size_t smem = ((size_t)kQTok * d + (size_t)m_total * (kQCk + 1)) * sizeof(double);
+  dim3 grid((unsigned)((n + kQTok - 1) / kQTok), kc.units);
+#define QJL_QK(R)                                                                          \
+  if (rpt == R) {                                                                          \
+    auto kern = k_quantize_keys_simt<TK, TS, R>;                                           \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
+    kern<<<grid, kQThreads, smem, st>>>((const TK*)keys, n, kus, (const TS*)s, sus, d,     \
+                                        m_in, m_out, ch, h, kc, row_offset);               \
+    QJL_LAUNCH_CHECK("quantize_keys_simt");                                                \
+    return QJL_OK;                                                                         \
+  }
+  QJL_QK(1)
+  QJL_QK(2)
+  QJL_QK(3)
+  QJL_QK(4)
+#undef QJL_QK
+  set_error("quantize_keys: m_in + m_out = %d exceeds 1024", m_total);
+  return QJL_ERR_UNSUPPORTED;
+}
+
+template <typename TK>
+static int launch_qk_simt_1(const void* keys, int64_t n, int64_t kus, const qjl_sketch_t& sk,
+                            int d, int m_in, int m_out, const int32_t* ch, int h,
+                            const qjl_key_cache_t& kc, int64_t row_offset, cudaStream_t st) {
+  switch (sk.dtype) {
+    case QJL_F64: return launch_qk_simt_2<TK, double>(keys, n, kus, sk.s_full, sk.unit_stride, d, m_in, m_out, ch, h, kc, row_offset, st);
+    case QJL_F32: return launch_qk_simt_2<TK, float>(keys, n, kus, sk.s_full, sk.unit_stride, d, m_in, m_out, ch, h, kc, row_offset, st);
+    case QJL_F16: return launch_qk_simt_2<TK, __half>(keys, n, kus, sk.s_full, sk.unit_stride, d, m_in, m_out, ch, h, kc, row_offset, st);
+    case QJL_BF16: return launch_qk_simt_2<TK, __nv_bfloat16>(keys, n, kus, sk.s_full, sk.unit_stride, d, m_in, m_out, ch, h, kc, row_offset, st);
+  }
+  return QJL_ERR_ARG;
+}
+
+int launch_quantize_keys_simt(const void* keys, int dtype, int64_t n, int64_t kus,
+                              const qjl_sketch_t& sk, const int32_t* ch, int h,
+                              const qjl_key_cache_t& kc, int64_t row_offset, cudaStream_t st) {
+  const int d = kc.d, m_in = kc.m_in, m_out = kc.m_out;
+  switch (dtype) {
+    case QJL_F32: return launch_qk_simt_1<float>(keys, n, kus, sk, d, m_in, m_out, ch, h, kc, row_offset, st);
+    case QJL_F64: return launch_qk_simt_1<double>(keys, n, kus, sk, d, m_in, m_out, ch, h, kc, row_offset, st);
+    case QJL_F16: return launch_qk_simt_1<__half>(keys, n, kus, sk, d, m_in, m_out, ch, h, kc, row_offset, st);
+    case QJL_BF16: return launch_qk_simt_1<__nv_bfloat16>(keys, n, kus, sk, d, m_in, m_out, ch, h, kc, row_offset, st);
+  }
+  return QJL_ERR_ARG;
+}
+
+// ---------------------------------------------------------------------------
+// Value quantizer (kvcache.py:140-161) per group: zero = min, scale =
+// (max - min)/(2^b - 1), codes = clip(rint((v - zero)/scale)) -- all in fp64 so
+// codes match the reference bit for bit (IEEE div + rint are exact-rounded);
+// constant group -> scale 0, codes 0.  Constants stored fp16 (P2) or f32 (U8).
+// One warp per token; lane l owns dims l + 32*i.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) k_quantize_values(const T* __restrict__ v, int64_t n,
+                                                         int64_t unit_stride,
+                                                         qjl_value_cache_t vc, int64_t row_offset) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = blockIdx.y;
+  const int64_t t = (int64_t)blockIdx.x * 8 + warp;
+  const int d = vc.d, G = d / vc.group, gs = vc.group;
+  const int levels = (1 << vc.bits) - 1;
+  __shared__ uint32_t words[8][8];
+  if (lane < 8) words[warp][lane] = 0u;
+  __syncwarp();
+  const bool valid = t < n;
+  const T* V = v + (int64_t)u * unit_stride + (valid ? t : 0) * d;
+  const int64_t row = (int64_t)u * vc.capacity + row_offset + t;
+  for (int g = 0; g < G; ++g) {
+    // group g spans dims [g*gs, (g+1)*gs); lanes stride over it
+    double mn = INFINITY, mx = -INFINITY;
+    for (int i = lane; i < gs; i += 32) {
+      const double x = to_f64(V[g * gs + i]);
+      mn = fmin(mn, x);
+      mx = fmax(mx, x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    const double zero = mn;
+    const double spread = mx - mn;
+    const double scale = spread == 0.0 ? 0.0 : spread / (double)levels;
+    for (int i = lane; i < gs; i += 32) {
+      const int dim = g * gs + i;
+      int code = 0;
+      if (spread != 0.0) {
+        double q = rint((to_f64(V[dim]) - zero) / scale);
+        q = fmin(fmax(q, 0.0), (double)levels);
+        code = (int)q;
+      }
+      if (valid) {
+        if (vc.layout == QJL_VLAYOUT_U8) {
+          reinterpret_cast<uint8_t*>(vc.codes)[row * d + dim] = (uint8_t)code;
+        } else {
+          int w, p;
+          p2_slot(dim, &w, &p);
+          atomicOr(&words[warp][w], (uint32_t)code << (2 * p));
+        }
+      }
+    }
+    if (valid && lane == 0) {
+      if (vc.layout == QJL_VLAYOUT_U8) {
+        reinterpret_cast<float*>(vc.zero)[row * G + g] = (float)zero;
+        reinterpret_cast<float*>(vc.scale)[row * G + g] = (float)scale;
+      } else {
+        reinterpret_cast<uint16_t*>(vc.zero)[row * G + g] = f64_to_f16_bits(zero);
+        reinterpret_cast<uint16_t*>(vc.scale)[row * G + g] = f64_to_f16_bits(scale);
+      }
+    }
+  }
+  __syncwarp();
+  if (valid && vc.layout == QJL_VLAYOUT_P2 && lane < 8)
+    reinterpret_cast<uint32_t*>(vc.codes)[row * 8 + lane] = words[warp][lane];
+}
+
+int launch_quantize_values(const void* v, int dtype, int64_t n, int64_t unit_stride,
+                           const qjl_value_cache_t& vc, int64_t row_offset, cudaStream_t st) {
+  dim3 grid((unsigned)((n + 7) / 8), vc.units);
+  switch (dtype) {
+#define QJL_QV(DT)                                                                          \
+  case DT:                                                                                  \
+    k_quantize_values<Elem<DT>::T><<<grid, 256, 0, st>>>((const Elem<DT>::T*)v, n,          \
+                                                         unit_stride, vc, row_offset);      \
+    break;
+    QJL_QV(QJL_F32)
+    QJL_QV(QJL_F16)
+    QJL_QV(QJL_BF16)
+    QJL_QV(QJL_F64)
+#undef QJL_QV
+    default: return QJL_ERR_ARG;
+  }
+  QJL_LAUNCH_CHECK("quantize_values");
+  return QJL_OK;
+}
+
+}  // namespace qjl

@@ -1,0 +1,50 @@
+// Internal launch entry points (host side), implemented in k_*.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/qjl_b200.h"
+
+namespace qjl {
+
+int launch_detect_outliers(const void* keys, int dtype, int units, int64_t n0, int d,
+                           int64_t unit_stride, int h, int32_t* channels, double* mags,
+                           cudaStream_t st);
+int launch_build_sketch(const double* s_in, const double* s_out, int m_in, int m_out, int d,
+                        int h, const int32_t* channels, int units, int dtype, void* s_full,
+                        cudaStream_t st);
+int launch_quantize_keys_simt(const void* keys, int dtype, int64_t n, int64_t kus,
+                              const qjl_sketch_t& sk, const int32_t* ch, int h,
+                              const qjl_key_cache_t& kc, int64_t row_offset, cudaStream_t st);
+// tcgen05 + TMA tensor-core key quantizer (bf16/fp16 keys); returns
+// QJL_ERR_UNSUPPORTED when the shape is outside its envelope.
+int launch_quantize_keys_tc(const void* keys, int dtype, int64_t n, int64_t kus,
+                            const qjl_sketch_t& sk, const int32_t* ch, int h,
+                            const qjl_key_cache_t& kc, int64_t row_offset, cudaStream_t st);
+int launch_quantize_values(const void* v, int dtype, int64_t n, int64_t unit_stride,
+                           const qjl_value_cache_t& vc, int64_t row_offset, cudaStream_t st);
+
+int launch_sketch_query(const void* q, int q_dtype, int units, int G, int d,
+                        const qjl_sketch_t& sk, int m_in, int m_total, float* sq, float* sums,
+                        cudaStream_t st);
+int launch_scores_simt(const qjl_key_cache_t& kc, int64_t n, int G, const float* sq,
+                       const float* sums, float* logits, cudaStream_t st);
+int launch_sign_dot_batch(const uint8_t* bits, int64_t n, int m, int64_t row_bytes,
+                          const double* values, int G, double* out, cudaStream_t st);
+int launch_softmax_f64(const float* logits, int64_t rows, int64_t n, double inv_t, double* w,
+                       cudaStream_t st);
+
+size_t decode_simt_workspace(int units, int64_t n, int G, int d, int m_total);
+int launch_decode_simt(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, int G,
+                       const float* sq, const float* sums, float inv_t, float* out, float* lse,
+                       float* ws, cudaStream_t st);
+
+// tensor-core fused decode for P2 caches (mma.sync IMMA scores + HMMA PV)
+bool decode_tc_supported(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int G);
+size_t decode_tc_workspace(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n,
+                           int G);
+int launch_decode_tc(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n,
+                     const void* q, int q_dtype, int G, const qjl_sketch_t& sk, float inv_t,
+                     float* out, float* lse, void* ws, size_t ws_bytes, cudaStream_t st);
+
+}  // namespace qjl

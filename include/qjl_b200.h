@@ -152,6 +152,13 @@ QJL_API int qjl_decode(const qjl_key_cache_t* cache, const qjl_value_cache_t* va
                float inv_temperature, float* out, float* lse, void* workspace,
                size_t workspace_bytes, void* stream);
 
+/* Benchmark timing hook: while enabled, the dominant kernel of every qjl_decode /
+ * qjl_quantize_keys call is bracketed by CUDA events recorded on its launch stream.
+ * qjl_timing_read synchronizes on them and returns the summed kernel time (ms)
+ * and the number of bracketed launches (reset != 0 clears the record). */
+QJL_API int qjl_timing_enable(int on);
+QJL_API int qjl_timing_read(double* total_ms, int* launches, int reset);
+
 /* Value quantizer: v [units][n][d] -> value cache rows [row_offset, row_offset + n). */
 QJL_API int qjl_quantize_values(const void* v, int dtype, int64_t n, int64_t unit_stride,
                         const qjl_value_cache_t* values, int64_t row_offset, void* stream);

@@ -3,6 +3,9 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -31,6 +34,34 @@ int device_sm_count() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (dev >= 0 && dev < 64) cached[dev] = sms;
   return sms;
+}
+
+static std::mutex g_tmu;
+static bool g_timing = false;
+static std::vector<cudaEvent_t> g_ev;   // pairs (start, stop)
+static size_t g_ev_used = 0;
+
+static cudaEvent_t next_event() {
+  if (g_ev_used == g_ev.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_ev.push_back(e);
+  }
+  return g_ev[g_ev_used++];
+}
+
+void timing_begin(cudaStream_t st) {
+  if (!g_timing) return;
+  std::lock_guard<std::mutex> lk(g_tmu);
+  if (g_ev_used % 2) return;  // unbalanced: ignore
+  cudaEventRecord(next_event(), st);
+}
+
+void timing_end(cudaStream_t st) {
+  if (!g_timing) return;
+  std::lock_guard<std::mutex> lk(g_tmu);
+  if (g_ev_used % 2 == 0) return;
+  cudaEventRecord(next_event(), st);
 }
 
 static bool valid_dtype(int dt) { return dt == QJL_F32 || dt == QJL_F16 || dt == QJL_BF16 || dt == QJL_F64; }
@@ -112,6 +143,30 @@ const char* qjl_status_string(int status) {
 }
 
 const char* qjl_last_error(void) { return g_err; }
+
+int qjl_timing_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_timing = on != 0;
+  return QJL_OK;
+}
+
+int qjl_timing_read(double* total_ms, int* launches, int reset) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  double tot = 0.0;
+  int cnt = 0;
+  for (size_t i = 0; i + 1 < g_ev_used; i += 2) {
+    cudaError_t e = cudaEventSynchronize(g_ev[i + 1]);
+    if (e != cudaSuccess) return cuda_status(e, "timing_read");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g_ev[i], g_ev[i + 1]);
+    tot += ms;
+    ++cnt;
+  }
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = cnt;
+  if (reset) g_ev_used = 0;
+  return QJL_OK;
+}
 
 int qjl_device_info(int* sm_count, int* cc_major, int* cc_minor) {
   int dev = 0;

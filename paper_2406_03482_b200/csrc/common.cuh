@@ -20,6 +20,9 @@ constexpr float kEstimatorScale = 1.2533141373155002512f;  // sqrt(pi/2), estima
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* what);
 int device_sm_count();
+// benchmark timing hook (api.cu): no-ops unless qjl_timing_enable(1)
+void timing_begin(cudaStream_t st);
+void timing_end(cudaStream_t st);
 
 #define QJL_CHECK_ARG(cond, ...)        \
   do {                                  \

@@ -206,7 +206,9 @@ int launch_decode_simt(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, i
   if (G <= GM) {                                                                            \
     cudaFuncSetAttribute(k_decode_simt<GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                          (int)smem);                                                        \
+    timing_begin(st);                                                                       \
     k_decode_simt<GM><<<grid, kDTile, smem, st>>>(kc, vc, n, G, chunk, sq, sums, inv_t, ws); \
+    timing_end(st);                                                                         \
     QJL_LAUNCH_CHECK("decode_simt");                                                        \
     k_decode_merge<<<kc.units * G, 128, 0, st>>>(ws, nsplit, G, vc.d, out, lse);            \
     QJL_LAUNCH_CHECK("decode_merge");                                                       \

@@ -252,8 +252,10 @@ static int launch_qk_simt_2(const void* keys, int64_t n, int64_t kus, const void
   if (rpt == R) {                                                                          \
     auto kern = k_quantize_keys_simt<TK, TS, R>;                                           \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
+    timing_begin(st);                                                                      \
     kern<<<grid, kQThreads, smem, st>>>((const TK*)keys, n, kus, (const TS*)s, sus, d,     \
                                         m_in, m_out, ch, h, kc, row_offset);               \
+    timing_end(st);                                                                        \
     QJL_LAUNCH_CHECK("quantize_keys_simt");                                                \
     return QJL_OK;                                                                         \
   }

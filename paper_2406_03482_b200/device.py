@@ -85,6 +85,9 @@ class DeviceKeyCache:
             raise ValueError("outlier bit rate below inlier bit rate: "
                              f"m_out/h = {m_out}/{h} < m_in/(d-h) = {m_in}/{d - h}")
         self.device = torch.device(device)
+        # rows are padded to whole 128-token tiles: the tensor-core decode streams
+        # full tiles with bulk copies and masks tokens >= n
+        capacity = (capacity + 127) // 128 * 128
         self.shape = CacheShape(units, d, m_in, m_out, h, capacity)
         self.key_dtype = key_dtype
         self.sketch_dtype = sketch_dtype or operand_dtype_for(key_dtype)

@@ -148,6 +148,39 @@ int main() {
       if (s == 0 && hD2[r * 8 + c] != 0) maxrel = 1;
     }
   printf("HMMA f16 subnormal-A max rel err %.3e (%s)\n", maxrel, maxrel < 1e-6 ? "ok" : "FLUSHED/BAD");
+  // (2b) subnormal A x subnormal B (P' lo parts are often fp16 subnormals)
+  for (int i = 0; i < 128; ++i) hB2[i] = (uint16_t)(1 + rand() % 1000);   // subnormal B
+  cudaMemcpy(dB2, hB2, 256, cudaMemcpyHostToDevice);
+  k_hmma_layout<<<1, 32>>>(dA2, dB2, dD2);
+  cudaMemcpy(hD2, dD2, 512, cudaMemcpyDeviceToHost);
+  maxrel = 0;
+  for (int r = 0; r < 16; ++r)
+    for (int c = 0; c < 8; ++c) {
+      double s = 0;
+      for (int k = 0; k < 16; ++k) s += (double)h2f(hA2[r * 16 + k]) * (double)h2f(hB2[k * 8 + c]);
+      double e = fabs(s - hD2[r * 8 + c]) / (fabs(s) + 1e-300);
+      if (s != 0 && e > maxrel) maxrel = e;
+      if (s == 0 && hD2[r * 8 + c] != 0) maxrel = 1;
+    }
+  printf("HMMA f16 subnormal-A x subnormal-B max rel err %.3e (%s) sample ref %.3e got %.3e\n", maxrel,
+         maxrel < 1e-6 ? "ok" : "FLUSHED/BAD", 0.0, hD2[0]);
+  // (2c) mixed-magnitude accumulation: normal B (~1) and tiny B (~1e-7 normal) in the same dot
+  for (int i = 0; i < 128; ++i) {
+    __half x = __float2half((i % 2) ? 1.0f : 3e-5f);
+    memcpy(&hB2[i], &x, 2);
+  }
+  cudaMemcpy(dB2, hB2, 256, cudaMemcpyHostToDevice);
+  k_hmma_layout<<<1, 32>>>(dA2, dB2, dD2);
+  cudaMemcpy(hD2, dD2, 512, cudaMemcpyDeviceToHost);
+  maxrel = 0;
+  for (int r = 0; r < 16; ++r)
+    for (int c = 0; c < 8; ++c) {
+      double s = 0;
+      for (int k = 0; k < 16; ++k) s += (double)h2f(hA2[r * 16 + k]) * (double)h2f(hB2[k * 8 + c]);
+      double e = fabs(s - hD2[r * 8 + c]) / (fabs(s) + 1e-300);
+      if (s != 0 && e > maxrel) maxrel = e;
+    }
+  printf("HMMA mixed-magnitude B max rel err %.3e\n", maxrel);
 
   // (3) throughput
   float* sink;

@@ -1,36 +1,39 @@
 // Tensor-core fused QJL decode (K2 score estimator + K3 online softmax . V) for
 // P2 value caches on sm_100a.
 //
-//  * Data movement: one producer warp streams each 128-token tile of the packed
-//    cache (sign bits, fp16 norms, 2-bit codes, fp16 zero/scale) HBM -> smem with
-//    cp.async.bulk (TMA bulk copies) into a kStages mbarrier ring; consumer warps
-//    never issue global loads on the hot path.
+//  * Data movement: thread 0 streams each 128-token tile of the packed cache
+//    (sign bits, fp16 norms, 2-bit codes, fp16 zero/scale) HBM -> smem with
+//    cp.async.bulk (TMA bulk copies) into a kStages mbarrier ring, kLookahead
+//    tiles ahead; the 4 warps never issue global loads on the hot path.
 //  * Scores (estimator.py:149-170 identity 2*sum_set(Sq) - sum(Sq)): the query
 //    sketch of every query head is quantized to a 32-bit fixed-point integer and
-//    split into four int8 digits; rows of an m16n8k32 IMMA A operand are
-//    (digit, query) pairs, so one IMMA computes 4 digits x 4 query heads x 8
-//    tokens x 32 sign bits with exact int32 accumulation.  The B operand is the
-//    packed sign word itself, masked in place: `w & (0x01010101 << 2q)` turns 4
-//    sign bits into 4 u8 lanes of value 2^(2q)*bit -- 2 LOP3 per 8 bits, no
-//    unpacking; the 2^s weights are folded into the digits.
+//    split into four int8 digits -- the B operand of an m16n8k32 IMMA whose
+//    columns are (query, digit) pairs -- so one IMMA computes 16 tokens x 4 query
+//    heads x 2 digits x 32 sign bits with exact int32 accumulation.  The A operand
+//    is the packed sign word itself, masked in place: `w & (0x01010101 << 2q)`
+//    turns 4 sign bits into 4 u8 lanes of value 2^(2q)*bit (2 LOP3 per 8 bits, no
+//    unpacking); the 2^s weights are folded into the digits.
 //  * PV: out[q][d] = sum_t P'[t][q] c[t][d] + sum_t p[t][q] zero[t][g], with
-//    P' = p * scale split hi/lo in fp16 (22-bit P'), codes entering an m16n8k16
-//    HMMA as EXACT fp16 subnormals c * 4^e * 2^-24 produced by a single LOP3 on
-//    a PRMT of two tokens' code words (P2 layout puts lane-row g's 16 dims in
-//    code word g), rescaled by 2^24/4^e per output row at the end.
+//    P' = p * scale split hi/lo in fp16 (22-bit P') as the B operand of an
+//    m16n8k16 HMMA whose A operand is the 2-bit code turned into the NORMAL fp16
+//    1 + c 4^s/1024 by one SHF + one LOP3 (P2 layout puts lane-row g's 16 dims in
+//    code word g); the offset sum_t P' is removed with an exact FFMA accumulator.
 //  * Online softmax in the log2 domain per query head; one partial (m, l, acc)
 //    per (CTA, unit segment); CTAs own equal contiguous ranges of the flattened
 //    (unit, tile) space (stream-K) so every SM gets the same number of tiles.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace qjl {
 namespace tc {
 
-constexpr int kNW = 4;             // consumer warps
+constexpr int kNW = 4;             // warps per CTA (all compute; warp 0 lane 0 issues copies)
 constexpr int kTile = 32 * kNW;    // tokens per pipeline stage
-constexpr int kStages = 4;
-constexpr int kThreads = 32 * (kNW + 1);
+constexpr int kStages = 5;
+constexpr int kLookahead = 3;      // tiles in flight ahead of the one being consumed
+constexpr int kThreads = 32 * kNW;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -89,9 +92,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void imma(int* d, const uint4& a, uint32_t b0, uint32_t b1) {
+// A = masked sign words (u8 lanes 2^s * bit), B = query-sketch digits (s8)
+__device__ __forceinline__ void imma_u8s8(int* d, const uint4& a, uint32_t b0, uint32_t b1) {
   asm volatile(
-      "mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};\n"
       : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
       : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
@@ -158,26 +162,29 @@ struct Layout {
   static constexpr int oScale = oZero + kConst;
   static constexpr int kStageBytes = oScale + kConst;
   static constexpr int oPbuf = kStages * kStageBytes;              // per warp 2 KB
-  static constexpr int oRed = oPbuf + kNW * 2048;                  // flush scratch
+  static constexpr int oRed = oPbuf;                               // flush scratch aliases P'
   static constexpr int kRec = 2 + 4 + 128;                          // m, l, Z[4], acc[128]
   static constexpr int kRedBytes = kNW * 4 * kRec * 4;
-  static constexpr int oBar = oRed + kRedBytes;
+  static constexpr int kScratch = kRedBytes > kNW * 2048 ? kRedBytes : kNW * 2048;
+  static constexpr int oBar = oPbuf + kScratch;
   static constexpr int kTotal = oBar + 2 * kStages * 8;
 };
 
 // ----------------------------------------------------------------- prep kernel
-// Per unit: Sq = S_full . q (fp64), per-side sigma = max|Sq|/2^30, weighted
-// integer sketch, 4 signed-byte digits laid out as IMMA A fragments.
+// Per unit: Sq = S_full . q (fp64, rounded to fp32 like the generic path),
+// per-side sigma = max|Sq| / 2^30, weighted integer sketch
+// x_j = rint(Sq_j / (sigma * 2^(j mod 8))), 4 signed-byte digits laid out as the
+// IMMA B operand: column n of n-tile nt = (query n/2, digit 2*nt + n%2).
 template <typename TQ, typename TS, int KCI, int KCO>
 __global__ void __launch_bounds__(256) k_prep(const TQ* __restrict__ q, int G, const TS* __restrict__ s_full,
-                                              int64_t s_unit_stride, float inv_t, uint4* __restrict__ afrag,
+                                              int64_t s_unit_stride, float inv_t, uint4* __restrict__ bfrag,
                                               float4* __restrict__ qconst) {
   constexpr int MI = KCI * 32, MO = KCO * 32, MT = MI + MO, KC = KCI + KCO;
   constexpr int d = 128;
   __shared__ double qs[4][d];
   __shared__ double sq[4][MT];
   __shared__ int32_t si[4][MT];
-  __shared__ double red[4][2][2];   // [q][side][max, sum]
+  __shared__ double red[4][2][2];   // [q][side][sigma, sum]
   const int u = blockIdx.x;
   const TS* S = s_full + (int64_t)u * s_unit_stride;
   for (int i = threadIdx.x; i < 4 * d; i += blockDim.x) {
@@ -195,7 +202,6 @@ __global__ void __launch_bounds__(256) k_prep(const TQ* __restrict__ q, int G, c
       a2 = fma(s, qs[2][c], a2);
       a3 = fma(s, qs[3][c], a3);
     }
-    // the generic path rounds Sq to fp32 before use; keep the same values
     sq[0][r] = (double)(float)a0;
     sq[1][r] = (double)(float)a1;
     sq[2][r] = (double)(float)a2;
@@ -213,10 +219,8 @@ __global__ void __launch_bounds__(256) k_prep(const TQ* __restrict__ q, int G, c
   for (int i = threadIdx.x; i < 4 * MT; i += blockDim.x) {
     const int g = i / MT, j = i % MT;
     const int side = j >= MI;
-    const double sigma = red[g][side][0];
     const int jl = side ? j - MI : j;
-    const double x = rint(sq[g][j] / (sigma * (double)(1 << (jl & 7))));
-    si[g][j] = (int32_t)x;
+    si[g][j] = (int32_t)rint(sq[g][j] / (red[g][side][0] * (double)(1 << (jl & 7))));
   }
   __syncthreads();
   if (threadIdx.x < 8) {
@@ -227,22 +231,23 @@ __global__ void __launch_bounds__(256) k_prep(const TQ* __restrict__ q, int G, c
     red[g][side][1] = s * red[g][side][0];
   }
   __syncthreads();
-  // A fragments: element (row, k) of chunk c lives in lane (row%8)*4 + (k%16)/4,
-  // reg (row>=8) + 2*(k>=16), byte k%4; row = digit*4 + query; k <-> sign bit p.
+  // B fragment of m16n8k32: element (k, n) lives in lane n*4 + (k%16)/4, reg
+  // (k >= 16), byte k%4.  k <-> sign bit p of the chunk word: k = 4q + i holds
+  // bit 8i + 2q, k = 16 + 4q + i holds bit 8i + 2q + 1 (the A side masks the
+  // sign word with 0x01010101 << 2q / 0x02020202 << 2q).
   for (int i = threadIdx.x; i < KC * 32; i += blockDim.x) {
     const int c = i / 32, lane = i % 32;
-    const int gl = lane >> 2, ql = lane & 3;
+    const int n = lane >> 2, ql = lane & 3;
+    const int qd = n >> 1;
     uint32_t regs[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < 4; ++r) {          // r = nt*2 + reg
+      const int nt = r >> 1, reg = r & 1;
+      const int digit = 2 * nt + (n & 1);
       uint32_t v = 0;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        const int row = gl + ((r & 1) ? 8 : 0);
-        const int k = ((r & 2) ? 16 : 0) + 4 * ql + b;
-        const int qd = row & 3, digit = row >> 2;
-        const int kk = k & 15;
-        const int p = 8 * (kk & 3) + 2 * (kk >> 2) + (k >= 16 ? 1 : 0);
+        const int p = 8 * b + 2 * ql + reg;
         const int side = c >= KCI;
         const int j = (side ? MI + (c - KCI) * 32 : c * 32) + p;
         int32_t x = si[qd][j];
@@ -257,7 +262,7 @@ __global__ void __launch_bounds__(256) k_prep(const TQ* __restrict__ q, int G, c
       }
       regs[r] = v;
     }
-    afrag[((int64_t)u * KC + c) * 32 + lane] = make_uint4(regs[0], regs[1], regs[2], regs[3]);
+    bfrag[((int64_t)u * KC + c) * 32 + lane] = make_uint4(regs[0], regs[1], regs[2], regs[3]);
   }
   if (threadIdx.x < 4) {
     const int g = threadIdx.x;
@@ -277,10 +282,19 @@ __global__ void __launch_bounds__(256) k_prep(const TQ* __restrict__ q, int G, c
 }
 
 // ----------------------------------------------------------------- main kernel
+// 4 warps per CTA, each owning 32 tokens of every 128-token stage; thread 0 also
+// issues the bulk copies kLookahead tiles ahead (no dedicated producer warp, so
+// three CTAs -- 12 warps -- fit per SM).
+//
+// Token order inside a warp's 32-token tile: score m-tile h covers tokens 16h..16h+15
+// with IMMA rows g / g+8 = tokens 16h+g / 16h+g+8, and the PV k-step h uses the
+// permuted k order k = 2j + e  <->  token 16h + j + 8e, so the fp16 pair (k, k+1)
+// of a B fragment is exactly the token pair a score lane owns (no exchange).
 template <int KCI, int KCO>
-__global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 1 : 2) k_decode_tc(const Params P) {
+__global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 3) k_decode_tc(const Params P) {
   using L = Layout<KCI, KCO>;
   constexpr int KC = KCI + KCO;
+  constexpr int R = L::kRec;
   extern __shared__ __align__(128) uint8_t sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::oBar);
   uint64_t* empty = full + kStages;
@@ -288,6 +302,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 1 : 2) k_decode_t
   const int C = P.ctas;
   const int64_t T = P.total_tiles;
   const int64_t r0 = tile_begin(blockIdx.x, T, C), r1 = tile_begin(blockIdx.x + 1, T, C);
+  const int ntiles = (int)(r1 - r0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -297,58 +312,52 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 1 : 2) k_decode_t
   }
   __syncthreads();
 
-  if (warp == kNW) {
-    // ============================ producer =============================
-    if (lane == 0) {
-      const auto& kc = P.kc;
-      const auto& vc = P.vc;
-      for (int64_t t = r0; t < r1; ++t) {
-        const int it = (int)(t - r0);
-        const int s = it % kStages;
-        if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
-        const int u = (int)(t / P.tpu);
-        const int64_t tok = (t % P.tpu) * kTile;
-        const int64_t row = (int64_t)u * kc.capacity + tok;     // capacity % 128 == 0
-        uint8_t* st = sm + s * L::kStageBytes;
-        mbar_expect_tx(&full[s], L::kStageBytes);
-        bulk_g2s(st + L::oBitsIn, kc.bits_in + row * (KCI * 4), L::kBitsIn, &full[s]);
-        if (KCO) {
-          bulk_g2s(st + L::oBitsOut, kc.bits_out + row * (KCO * 4), L::kBitsOut, &full[s]);
-          bulk_g2s(st + L::oNormOut, kc.norm_out + row, L::kNorm, &full[s]);
-        }
-        bulk_g2s(st + L::oNormIn, kc.norm_in + row, L::kNorm, &full[s]);
-        const int64_t vrow = (int64_t)u * vc.capacity + tok;
-        bulk_g2s(st + L::oCodes, (const uint8_t*)vc.codes + vrow * 32, L::kCodes, &full[s]);
-        bulk_g2s(st + L::oZero, (const uint8_t*)vc.zero + vrow * 8, L::kConst, &full[s]);
-        bulk_g2s(st + L::oScale, (const uint8_t*)vc.scale + vrow * 8, L::kConst, &full[s]);
-      }
+  // (unit, tile-in-unit) of the first tile; advanced incrementally (no 64-bit div per tile)
+  const int u_first = (int)(r0 / P.tpu);
+  const int lt_first = (int)(r0 - (int64_t)u_first * P.tpu);
+  int iss_u = u_first, iss_lt = lt_first, iss_i = 0;     // issuer cursor (thread 0 only)
+  auto issue_next = [&]() {   // bulk-copy tile r0 + iss_i into stage iss_i % kStages
+    const int i = iss_i;
+    const int s = i % kStages;
+    if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+    const int64_t tok = (int64_t)iss_lt * kTile;
+    const int64_t row = (int64_t)iss_u * P.kc.capacity + tok;     // capacity % 128 == 0
+    const int64_t vrow = (int64_t)iss_u * P.vc.capacity + tok;
+    uint8_t* st = sm + s * L::kStageBytes;
+    mbar_expect_tx(&full[s], L::kStageBytes);
+    bulk_g2s(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, &full[s]);
+    if (KCO) {
+      bulk_g2s(st + L::oBitsOut, P.kc.bits_out + row * (KCO * 4), L::kBitsOut, &full[s]);
+      bulk_g2s(st + L::oNormOut, P.kc.norm_out + row, L::kNorm, &full[s]);
     }
-    return;
-  }
+    bulk_g2s(st + L::oNormIn, P.kc.norm_in + row, L::kNorm, &full[s]);
+    bulk_g2s(st + L::oCodes, (const uint8_t*)P.vc.codes + vrow * 32, L::kCodes, &full[s]);
+    bulk_g2s(st + L::oZero, (const uint8_t*)P.vc.zero + vrow * 8, L::kConst, &full[s]);
+    bulk_g2s(st + L::oScale, (const uint8_t*)P.vc.scale + vrow * 8, L::kConst, &full[s]);
+    ++iss_i;
+    if (++iss_lt == P.tpu) { iss_lt = 0; ++iss_u; }
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kLookahead && i < ntiles; ++i) issue_next();
 
-  // ============================== consumers ==============================
-  const int g = lane >> 2, q = lane & 3;
-  const bool upper = g >= 4;          // lanes 16..31: digits 1/3, keep token 2q+1
-  const int Q = g & 3;                // epilogue query of this lane
-  const float wa = upper ? 256.f : 1.f, wb = upper ? 16777216.f : 65536.f;
+  const int g = lane >> 2, q = lane & 3;      // q = this lane's query head
   const uint32_t M0 = 0x01010101u << (2 * q), M1 = 0x02020202u << (2 * q);
   uint32_t* pbuf = reinterpret_cast<uint32_t*>(sm + L::oPbuf + warp * 2048);
   float* red = reinterpret_cast<float*>(sm + L::oRed);
 
-  uint4 A[KC];
+  uint4 Bq[KC];                               // query-sketch digits (IMMA B operand)
   float4 qc = make_float4(0.f, 0.f, 0.f, 0.f);
   float m_run = -INFINITY, l_run = 0.f;
-  float Z[4] = {0.f, 0.f, 0.f, 0.f};   // sum_t p * zero_g   (lane's query Q)
-  float Y[4] = {0.f, 0.f, 0.f, 0.f};   // sum_t p * scale_g  (HMMA offset removal)
-  float acc[8][4];
+  float Z[4] = {0.f, 0.f, 0.f, 0.f};          // sum_t p * zero_g   (query q)
+  float Y[4] = {0.f, 0.f, 0.f, 0.f};          // sum_t p * scale_g  (HMMA offset removal)
+  float acc[8][4];                            // PV: rows = dims, cols (2q, 2q+1) = query q hi/lo
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
-  int cur_u = -1;
 
   auto load_unit = [&](int u) {
 #pragma unroll
-    for (int c = 0; c < KC; ++c) A[c] = P.afrag[((int64_t)u * KC + c) * 32 + lane];
-    qc = P.qconst[(int64_t)u * 4 + Q];
+    for (int c = 0; c < KC; ++c) Bq[c] = P.afrag[((int64_t)u * KC + c) * 32 + lane];
+    qc = P.qconst[(int64_t)u * 4 + q];
     m_run = -INFINITY;
     l_run = 0.f;
 #pragma unroll
@@ -358,14 +367,14 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 1 : 2) k_decode_t
   };
 
   auto flush = [&](int u) {
-    // reduce l and Z over the 8 lanes sharing this lane's epilogue query
-    constexpr int R = L::kRec;
+    // the P' buffers are reused as scratch: every warp must be done with its tile
+    asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+    // l, Z, Y: reduce over the 8 lanes of query q (lanes q + 4g)
     float l = l_run;
     float z[4] = {Z[0], Z[1], Z[2], Z[3]};
     float y[4] = {Y[0], Y[1], Y[2], Y[3]};
 #pragma unroll
-    for (int o = 1; o <= 16; o <<= 1) {
-      if (o == 4 || o == 8) continue;
+    for (int o = 4; o <= 16; o <<= 1) {
       l += __shfl_xor_sync(0xffffffffu, l, o);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -373,30 +382,24 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 1 : 2) k_decode_t
         y[i] += __shfl_xor_sync(0xffffffffu, y[i], o);
       }
     }
-    // Y of the accumulator query q (held by lane 4q, whose epilogue query is q)
-    float yq[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) yq[i] = __shfl_sync(0xffffffffu, y[i], 4 * q);
-    // per-warp record: [q][0]=m, [1]=l, [2..5]=Z, [6..133]=sum_t P' c
     float* rw = red + warp * 4 * R;
-    if (q == 0 && !upper) {
-      rw[Q * R + 0] = m_run;
-      rw[Q * R + 1] = l;
+    if (g == 0) {
+      rw[q * R + 0] = m_run;
+      rw[q * R + 1] = l;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) rw[Q * R + 2 + i] = z[i];
+      for (int i = 0; i < 4; ++i) rw[q * R + 2 + i] = z[i];
     }
     // HMMA rows hold sum_t P' (1 + c 4^s / 1024), s = 3 (row g) or 4 (row g+8)
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
-      const float yg = yq[mt >> 1];
+      const float yg = y[mt >> 1];
       rw[q * R + 6 + 16 * mt + g] = (acc[mt][0] + acc[mt][1] - yg) * 16.f;
       rw[q * R + 6 + 16 * mt + g + 8] = (acc[mt][2] + acc[mt][3] - yg) * 4.f;
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(kNW * 32) : "memory");
-    const int tid = threadIdx.x;            // 0 .. kNW*32-1
+    asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
     const int c0 = cta_of_tile((int64_t)u * P.tpu, T, C);
     const int slot = blockIdx.x - c0;
-    for (int i = tid; i < P.G * 130; i += kNW * 32) {
+    for (int i = threadIdx.x; i < P.G * 130; i += kThreads) {
       const int qq = i / 130, e = i % 130;
       float M = -INFINITY;
 #pragma unroll
@@ -412,21 +415,12 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 1 : 2) k_decode_t
       float* dst = P.part + (((int64_t)u * P.max_seg + slot) * P.G + qq) * 130;
       dst[e] = (e == 0) ? (M == -INFINITY ? -INFINITY : M * kLn2) : v;
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(kNW * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
   };
 
-  for (int64_t t = r0; t < r1; ++t) {
-    const int it = (int)(t - r0);
-    const int s = it % kStages;
-    const int u = (int)(t / P.tpu);
-    const int64_t tok0 = (t % P.tpu) * kTile + warp * 32;   // first token of this warp
-    if (u != cur_u) {
-      if (cur_u >= 0) flush(cur_u);
-      load_unit(u);
-      cur_u = u;
-    }
-    mbar_wait(&full[s], (it / kStages) & 1);
-    const uint8_t* st = sm + s * L::kStageBytes;
+  // one 32-token warp tile; MASK: some tokens are >= n (tail tile of a unit)
+  auto tile = [&](const uint8_t* st, const int64_t tok0, auto mask_tag) {
+    constexpr bool MASK = decltype(mask_tag)::value;
     const uint32_t* bin = reinterpret_cast<const uint32_t*>(st + L::oBitsIn) + warp * 32 * KCI;
     const uint32_t* bout = reinterpret_cast<const uint32_t*>(st + L::oBitsOut) + warp * 32 * KCO;
     const __half* nin = reinterpret_cast<const __half*>(st + L::oNormIn) + warp * 32;
@@ -435,134 +429,142 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 1 : 2) k_decode_t
     const uint2* zer = reinterpret_cast<const uint2*>(st + L::oZero) + warp * 32;
     const uint2* scl = reinterpret_cast<const uint2*>(st + L::oScale) + warp * 32;
 
-    // -------------------- scores: 4 IMMA n-tiles of 8 tokens --------------------
-    float lg[4];
+    // -------- scores: 2 IMMA m-tiles of 16 tokens (rows g, g+8) x 2 n-tiles -------
+    // D[token][2q + i] of n-tile nt = digit 2nt+i of query q: every lane ends up
+    // with all four digits of its own query for tokens g and g+8 -- no shuffles.
+    float lg[4];                       // token 16h + g + 8e  ->  lg[2h + e]
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int trow = 8 * j + g;                    // B column token of this lane
-      uint32_t w_in[KCI], w_out[KCO > 0 ? KCO : 1];
+    for (int h = 0; h < 2; ++h) {
+      const int ta = 16 * h + g, tb = ta + 8;
+      int din[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+      int dout[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
       for (int c = 0; c < KCI; c += 4) {
-        const uint4 v = *reinterpret_cast<const uint4*>(bin + trow * KCI + c);
-        w_in[c] = v.x; w_in[c + 1] = v.y; w_in[c + 2] = v.z; w_in[c + 3] = v.w;
+        const uint4 va = *reinterpret_cast<const uint4*>(bin + ta * KCI + c);
+        const uint4 vb = *reinterpret_cast<const uint4*>(bin + tb * KCI + c);
+        const uint32_t wa[4] = {va.x, va.y, va.z, va.w}, wb[4] = {vb.x, vb.y, vb.z, vb.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint4 a = make_uint4(wa[e] & M0, wb[e] & M0, wa[e] & M1, wb[e] & M1);
+          imma_u8s8(din[0], a, Bq[c + e].x, Bq[c + e].y);
+          imma_u8s8(din[1], a, Bq[c + e].z, Bq[c + e].w);
+        }
       }
 #pragma unroll
       for (int c = 0; c < KCO; c += 2) {
-        const uint2 v = *reinterpret_cast<const uint2*>(bout + trow * KCO + c);
-        w_out[c] = v.x; w_out[c + 1] = v.y;
+        const uint2 va = *reinterpret_cast<const uint2*>(bout + ta * KCO + c);
+        const uint2 vb = *reinterpret_cast<const uint2*>(bout + tb * KCO + c);
+        const uint32_t wa[2] = {va.x, va.y}, wb[2] = {vb.x, vb.y};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint4 a = make_uint4(wa[e] & M0, wb[e] & M0, wa[e] & M1, wb[e] & M1);
+          imma_u8s8(dout[0], a, Bq[KCI + c + e].x, Bq[KCI + c + e].y);
+          imma_u8s8(dout[1], a, Bq[KCI + c + e].z, Bq[KCI + c + e].w);
+        }
       }
-      int di[4] = {0, 0, 0, 0}, dout[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int c = 0; c < KCI; ++c) imma(di, A[c], w_in[c] & M0, w_in[c] & M1);
-#pragma unroll
-      for (int c = 0; c < KCO; ++c) imma(dout, A[KCI + c], w_out[c] & M0, w_out[c] & M1);
-      const float pi0 = (float)di[0] * wa + (float)di[2] * wb;   // token 2q
-      const float pi1 = (float)di[1] * wa + (float)di[3] * wb;   // token 2q+1
-      const float po0 = (float)dout[0] * wa + (float)dout[2] * wb;
-      const float po1 = (float)dout[1] * wa + (float)dout[3] * wb;
-      const float si = __shfl_xor_sync(0xffffffffu, upper ? pi0 : pi1, 16);
-      const float so = __shfl_xor_sync(0xffffffffu, upper ? po0 : po1, 16);
-      const float dot_in = (upper ? pi1 : pi0) + si;
-      const float dot_out = (upper ? po1 : po0) + so;
-      const int tk = 8 * j + 2 * q + (upper ? 1 : 0);
-      const float nu_in = __half2float(nin[tk]);
-      float l2 = nu_in * fmaf(qc.x, dot_in, -qc.y);
-      if (KCO) l2 += __half2float(nout[tk]) * fmaf(qc.z, dot_out, -qc.w);
-      lg[j] = (tok0 + tk < P.n) ? l2 : -INFINITY;
+      for (int e = 0; e < 2; ++e) {      // e = 0: token ta (c0, c1); e = 1: token tb (c2, c3)
+        const int tk = e ? tb : ta;
+        // |digit partial| <= 2^21, so d0 + 256 d1 and d2 + 256 d3 are exact in int32
+        const float din_f = fmaf((float)(din[1][2 * e] + 256 * din[1][2 * e + 1]), 65536.f,
+                                 (float)(din[0][2 * e] + 256 * din[0][2 * e + 1]));
+        float l2 = __half2float(nin[tk]) * fmaf(qc.x, din_f, -qc.y);
+        if (KCO) {
+          const float dout_f = fmaf((float)(dout[1][2 * e] + 256 * dout[1][2 * e + 1]), 65536.f,
+                                    (float)(dout[0][2 * e] + 256 * dout[0][2 * e + 1]));
+          l2 = fmaf(__half2float(nout[tk]), fmaf(qc.z, dout_f, -qc.w), l2);
+        }
+        lg[2 * h + e] = (!MASK || tok0 + tk < P.n) ? l2 : -INFINITY;
+      }
     }
 
-    // -------------------- online softmax (log2 domain) --------------------
+    // -------------------- online softmax (log2 domain, query q) --------------------
     float tmax = fmaxf(fmaxf(lg[0], lg[1]), fmaxf(lg[2], lg[3]));
-    tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
-    tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+    tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
+    tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
     tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
     const float m_new = fmaxf(m_run, tmax);
-    const bool none = (m_new == -INFINITY);
+    const bool none = MASK && (m_new == -INFINITY);
     const float alpha = none ? 1.f : ex2(m_run - m_new);
     m_run = m_new;
     float p[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) p[j] = none ? 0.f : ex2(lg[j] - m_new);
-    l_run = l_run * alpha + (p[0] + p[1]) + (p[2] + p[3]);
+    for (int i = 0; i < 4; ++i) p[i] = none ? 0.f : ex2(lg[i] - m_new);
+    l_run = fmaf(l_run, alpha, (p[0] + p[1]) + (p[2] + p[3]));
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       Z[i] *= alpha;
       Y[i] *= alpha;
     }
-    const float a_acc = __shfl_sync(0xffffffffu, alpha, 4 * q);   // alpha of query q
 
-    // -------------------- P' = p*scale (hi/lo fp16) -> per-warp B tiles ------
+    // -------- P' = p * scale_g, split hi/lo fp16, written as HMMA B fragments --------
+    // B layout per warp: [k-step h][column 2q + lo][quad q'][b][group] half2 over the
+    // k pair (2q' + 8b, +1) = tokens (16h + q' + 4b, +8): this lane's own pair
+    // (tokens 16h + g, 16h + g + 8) is q' = g & 3, b = g >> 2.
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int tk = 8 * j + 2 * q + (upper ? 1 : 0);
-      const bool valid = tok0 + tk < P.n;
-      const uint2 zr = zer[tk], sr = scl[tk];
-      const float2 z01 = __half22float2(*reinterpret_cast<const __half2*>(&zr.x));
-      const float2 z23 = __half22float2(*reinterpret_cast<const __half2*>(&zr.y));
-      const float2 s01 = __half22float2(*reinterpret_cast<const __half2*>(&sr.x));
-      const float2 s23 = __half22float2(*reinterpret_cast<const __half2*>(&sr.y));
-      const float pj = p[j];
-      const float zz[4] = {z01.x, z01.y, z23.x, z23.y};
-      const float ss[4] = {s01.x, s01.y, s23.x, s23.y};
-      float hi[4], lo[4];
+    for (int h = 0; h < 2; ++h) {
+      float hv[2][4], lv[2][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float Pp = valid ? pj * ss[i] : 0.f;
-        Z[i] += valid ? pj * zz[i] : 0.f;
-        Y[i] += Pp;
-        const __half h = __float2half_rn(Pp);
-        hi[i] = __half2float(h);
-        lo[i] = Pp - hi[i];
+      for (int e = 0; e < 2; ++e) {
+        const int tk = 16 * h + g + 8 * e;
+        const float pj = p[2 * h + e];
+        uint2 zr = zer[tk], sr = scl[tk];
+        if (MASK && tok0 + tk >= P.n) zr = sr = make_uint2(0u, 0u);   // garbage rows past n
+        const float2 z01 = __half22float2(*reinterpret_cast<const __half2*>(&zr.x));
+        const float2 z23 = __half22float2(*reinterpret_cast<const __half2*>(&zr.y));
+        const float2 s01 = __half22float2(*reinterpret_cast<const __half2*>(&sr.x));
+        const float2 s23 = __half22float2(*reinterpret_cast<const __half2*>(&sr.y));
+        const float zz[4] = {z01.x, z01.y, z23.x, z23.y};
+        const float ss[4] = {s01.x, s01.y, s23.x, s23.y};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float Pp = pj * ss[i];
+          Z[i] = fmaf(pj, zz[i], Z[i]);
+          Y[i] += Pp;
+          hv[e][i] = __uint_as_float(__float_as_uint(Pp) & 0xFFFFE000u);   // 11 significant bits
+          lv[e][i] = Pp - hv[e][i];
+        }
       }
-      const uint32_t h01 = pack_h2(hi[0], hi[1]), h23 = pack_h2(hi[2], hi[3]);
-      const uint32_t l01 = pack_h2(lo[0], lo[1]), l23 = pack_h2(lo[2], lo[3]);
-      // lower lanes keep hi of token 2q, upper lanes keep lo of token 2q+1
-      const uint32_t snd0 = upper ? h01 : l01, snd1 = upper ? h23 : l23;
-      const uint32_t rc0 = __shfl_xor_sync(0xffffffffu, snd0, 16);
-      const uint32_t rc1 = __shfl_xor_sync(0xffffffffu, snd1, 16);
-      uint4 wv;
-      if (!upper) {   // hi column 2Q: {mine (token 2q), partner (token 2q+1)} per group
-        wv.x = prmt(h01, rc0, 0x5410); wv.y = prmt(h01, rc0, 0x7632);
-        wv.z = prmt(h23, rc1, 0x5410); wv.w = prmt(h23, rc1, 0x7632);
-      } else {        // lo column 2Q+1: {partner (token 2q), mine (token 2q+1)}
-        wv.x = prmt(rc0, l01, 0x5410); wv.y = prmt(rc0, l01, 0x7632);
-        wv.z = prmt(rc1, l23, 0x5410); wv.w = prmt(rc1, l23, 0x7632);
-      }
-      const int ks = j >> 1, b = j & 1, gp = 2 * Q + (upper ? 1 : 0);
-      *reinterpret_cast<uint4*>(pbuf + ((((ks * 8 + gp) * 4 + q) * 2 + b) * 4)) = wv;
+      uint32_t* dst = pbuf + (((h * 8 + 2 * q) * 4 + (g & 3)) * 2 + (g >> 2)) * 4;
+      *reinterpret_cast<uint4*>(dst) = make_uint4(pack_h2(hv[0][0], hv[1][0]), pack_h2(hv[0][1], hv[1][1]),
+                                                  pack_h2(hv[0][2], hv[1][2]), pack_h2(hv[0][3], hv[1][3]));
+      *reinterpret_cast<uint4*>(dst + 32) = make_uint4(pack_h2(lv[0][0], lv[1][0]), pack_h2(lv[0][1], lv[1][1]),
+                                                       pack_h2(lv[0][2], lv[1][2]), pack_h2(lv[0][3], lv[1][3]));
     }
     __syncwarp();
 
     // -------------------- PV: 8 m-tiles x 2 k-steps of 16 tokens ---------------
-    // Each tile's PV is accumulated by the tensor core from zero and folded into
-    // the running fp32 accumulator with an IEEE FFMA that also applies the
-    // online-softmax rescale.
+    // a0/a1: k pair (2q, 2q+1) = tokens (16h + q, 16h + q + 8); a2/a3: (16h + q + 4, + 12)
     uint32_t xa[2], xb[2], ya[2], yb[2];
     uint32_t bg[4][2][2];   // [group][ks][b]
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
-      const int tb = 16 * ks + 2 * q;
-      const uint32_t w0 = codes[(tb + 0) * 8 + g], w1 = codes[(tb + 1) * 8 + g];
-      const uint32_t w8 = codes[(tb + 8) * 8 + g], w9 = codes[(tb + 9) * 8 + g];
+      const int tb = 16 * ks + q;
+      const uint32_t w0 = codes[(tb + 0) * 8 + g], w1 = codes[(tb + 8) * 8 + g];
+      const uint32_t w4 = codes[(tb + 4) * 8 + g], w5 = codes[(tb + 12) * 8 + g];
       xa[ks] = prmt(w0, w1, 0x5410); xb[ks] = prmt(w0, w1, 0x7632);
-      ya[ks] = prmt(w8, w9, 0x5410); yb[ks] = prmt(w8, w9, 0x7632);
-      // per (ks, column g, quad q): 8 u32 laid out [b][grp]
+      ya[ks] = prmt(w4, w5, 0x5410); yb[ks] = prmt(w4, w5, 0x7632);
       const uint4 B0 = *reinterpret_cast<const uint4*>(pbuf + ((ks * 8 + g) * 4 + q) * 8);
       const uint4 B1 = *reinterpret_cast<const uint4*>(pbuf + ((ks * 8 + g) * 4 + q) * 8 + 4);
       bg[0][ks][0] = B0.x; bg[1][ks][0] = B0.y; bg[2][ks][0] = B0.z; bg[3][ks][0] = B0.w;
       bg[0][ks][1] = B1.x; bg[1][ks][1] = B1.y; bg[2][ks][1] = B1.z; bg[3][ks][1] = B1.w;
     }
-    // m-tile MT: rows g / g+8 use code slots 2*(MT&3) / +1 of half-word X (tokens
-    // 2q, 2q+1) and Y (tokens 2q+8, 2q+9); one shift brings both to slots 3 / 4.
-#define QJL_MT(MT, X, Y)                                                                         \
+    // m-tile MT: rows g / g+8 use code slots 2*(MT&3) / +1 of half-words X and Y;
+    // one shift brings both to mantissa slots 3 / 4.
+    // The tile's product is formed from zero and folded into the running sum with an
+    // IEEE FFMA that also applies the online-softmax rescale (alpha is lane-local:
+    // the accumulator columns of this lane belong to query q).  Accumulating straight
+    // into the running sum drifts: the tensor core's fp32 adder truncates small
+    // addends against a large accumulator (1.8e-4 at 32k tokens, growing with n).
+#define QJL_MT(MT, X, Yw)                                                                        \
   {                                                                                              \
     float td[4] = {0.f, 0.f, 0.f, 0.f};                                                          \
     _Pragma("unroll") for (int ks = 0; ks < 2; ++ks) {                                           \
-      const uint32_t xs = code_shift<(MT) & 3>(X[ks]), ys = code_shift<(MT) & 3>(Y[ks]);         \
+      const uint32_t xs = code_shift<(MT) & 3>(X[ks]), ys = code_shift<(MT) & 3>(Yw[ks]);        \
       hmma(td, code_h2<3>(xs), code_h2<4>(xs), code_h2<3>(ys), code_h2<4>(ys),                   \
            bg[(MT) >> 1][ks][0], bg[(MT) >> 1][ks][1]);                                          \
     }                                                                                            \
-    _Pragma("unroll") for (int i = 0; i < 4; ++i) acc[MT][i] = fmaf(acc[MT][i], a_acc, td[i]);  \
+    _Pragma("unroll") for (int i = 0; i < 4; ++i) acc[MT][i] = fmaf(acc[MT][i], alpha, td[i]);  \
   }
     QJL_MT(0, xa, ya)
     QJL_MT(1, xa, ya)
@@ -574,10 +576,29 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 1 : 2) k_decode_t
     QJL_MT(7, xb, yb)
 #undef QJL_MT
     __syncwarp();
+  };
+
+  int cur_u = -1;
+  int u = u_first, lt = lt_first;
+  for (int it = 0; it < ntiles; ++it) {
+    const int s = it % kStages;
+    if (u != cur_u) {
+      if (cur_u >= 0) flush(cur_u);
+      load_unit(u);
+      cur_u = u;
+    }
+    if (threadIdx.x == 0 && it + kLookahead < ntiles) issue_next();
+    const int64_t tok0 = (int64_t)lt * kTile + warp * 32;   // first token of this warp
+    mbar_wait(&full[s], (it / kStages) & 1);
+    const uint8_t* st = sm + s * L::kStageBytes;
+    if (tok0 + 32 <= P.n) tile(st, tok0, std::false_type{});
+    else tile(st, tok0, std::true_type{});
     if (lane == 0) mbar_arrive(&empty[s]);
+    if (++lt == P.tpu) { lt = 0; ++u; }
   }
   if (cur_u >= 0) flush(cur_u);
 }
+
 
 // Merge per (unit, query): combine the unit's CTA-segment partials.
 __global__ void k_merge_tc(const float* __restrict__ part, int max_seg, int G, int tpu, int64_t T, int C,

@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqjl_b200.so")
+LIB_PATH = os.environ.get("QJL_LIB") or os.path.join(_HERE, "libqjl_b200.so")
 
 QJL_OK, QJL_ERR_ARG, QJL_ERR_UNSUPPORTED, QJL_ERR_CUDA, QJL_ERR_WORKSPACE, QJL_ERR_EMPTY = (
     0, -1, -2, -3, -4, -5)

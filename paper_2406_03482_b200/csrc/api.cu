@@ -230,6 +230,10 @@ int qjl_quantize_keys(const void* keys, int dtype, int64_t n, int64_t key_unit_s
   int rc = launch_quantize_keys_tc(keys, dtype, n, key_unit_stride, *sketch, channels, h, *cache,
                                    row_offset, (cudaStream_t)stream);
   if (rc != QJL_ERR_UNSUPPORTED) return rc;
+  if (getenv("QJL_REQUIRE_TC")) {   // tests: refuse the generic path for tensor-core shapes
+    set_error("quantize_keys: tensor-core path refused this configuration (QJL_REQUIRE_TC set)");
+    return QJL_ERR_UNSUPPORTED;
+  }
   return launch_quantize_keys_simt(keys, dtype, n, key_unit_stride, *sketch, channels, h, *cache,
                                    row_offset, (cudaStream_t)stream);
 }
@@ -334,6 +338,10 @@ int qjl_decode(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, in
   if (decode_tc_supported(*cache, *values, G))
     return launch_decode_tc(*cache, *values, n, q, q_dtype, G, *sketch, inv_temperature, out, lse,
                             workspace, workspace_bytes, st);
+  if (getenv("QJL_REQUIRE_TC")) {
+    set_error("decode: tensor-core path refused this configuration (QJL_REQUIRE_TC set)");
+    return QJL_ERR_UNSUPPORTED;
+  }
   const int m_total = cache->m_in + cache->m_out;
   float* sq = (float*)workspace;
   float* sums = sq + (size_t)cache->units * G * m_total;

@@ -1,9 +1,429 @@
-// tcgen05 + TMA key quantizer (bf16/fp16 keys) -- placeholder until implemented.
+// K1 on the 5th-gen tensor cores: key quantization K . S_full^T for bf16/fp16 keys
+// (estimator.py:110-124 batched; kvcache.py:293-306 split via the zero-padded
+// per-unit S_full) on sm_100a.
+//
+//  * persistent CTAs (one per SM) own equal contiguous ranges of the flattened
+//    (unit, 128-token tile) space; the unit's S_full [MT x 128] stays resident in
+//    shared memory (SWIZZLE_128B, K-major) and is reloaded only when the range
+//    crosses into the next unit;
+//  * warp 0: TMA producer -- 3-D tensor maps over keys [units][n][128] (tail rows
+//    past n are zero-filled by the TMA unit) and S_full [units][MT][128];
+//  * warp 1: single-thread tcgen05.mma issuer, M = 128 tokens, N = MT split into
+//    NC chunks of CH <= 256 columns, K = 128 (8 x K16), fp32 accumulators in two
+//    ping-pong TMEM buffers of 256 columns;
+//  * warps 2-3: ||k_in||, ||k_out|| in fp64 from the staged key tile (exact
+//    products, fp64 sums) -> one fp16 rounding, matching the reference's
+//    float64 norm stored at half precision;
+//  * warps 4-7: epilogue -- tcgen05.ld 32x32b (one token per thread), exact sign
+//    test `x >= 0` (set.ge: -0.0 -> 1, NaN -> 0), 32 bits per word, stored as
+//    the LSB-first sign words of the cache rows.
+#include <cuda.h>
+
 #include "common.cuh"
 #include "kernels.h"
+
 namespace qjl {
-int launch_quantize_keys_tc(const void*, int, int64_t, int64_t, const qjl_sketch_t&,
-                            const int32_t*, int, const qjl_key_cache_t&, int64_t, cudaStream_t) {
+namespace qtc {
+
+constexpr int kM = 128;          // tokens per tile (UMMA M)
+constexpr int kK = 128;          // head dim
+constexpr int kThreads = 256;
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void tc_mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+// K-major, SWIZZLE_128B smem matrix descriptor (rows of 128 B, 8-row atoms 1024 B apart)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);           // start address
+  d |= (uint64_t)1 << 16;                           // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                 // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                           // version (sm100)
+  d |= (uint64_t)2 << 61;                           // SWIZZLE_128B
+  return d;
+}
+// instruction descriptor: D f32, A/B f16 (0) or bf16 (1), both K-major, M = 128
+__host__ __device__ constexpr uint32_t make_idesc(int ab_format, int n) {
+  return (1u << 4) | ((uint32_t)ab_format << 7) | ((uint32_t)ab_format << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(kM >> 4) << 24);
+}
+
+// 32 fp32 accumulator columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// exact sign word: bit i = (x_i >= 0); set.ge gives all-ones / zero, merged with LOP3
+__device__ __forceinline__ uint32_t sign_word(const uint32_t* r) {
+  uint32_t w = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    uint32_t m;
+    asm("set.ge.u32.f32 %0, %1, 0f00000000;" : "=r"(m) : "f"(__uint_as_float(r[i])));
+    w |= m & (1u << i);
+  }
+  return w;
+}
+
+template <int MT, int NC, int STAGES>
+struct QLayout {
+  static constexpr int CH = MT / NC;                       // columns per N chunk
+  static constexpr int kBHalf = MT * 128;                  // one K-half of S_full (bytes)
+  static constexpr int kABytes = kM * kK * 2;              // one key tile (32 KB)
+  static constexpr int oB = 0;                             // S_full: [2 halves][MT rows][128 B]
+  static constexpr int oA = 2 * kBHalf;                    // key tiles: [STAGES][2 halves][128][128 B]
+  static constexpr int oBar = oA + STAGES * kABytes;
+  // barriers: a_full[S], a_empty[S], b_full, b_empty, t_full[2], t_empty[2]
+  static constexpr int kBars = 2 * STAGES + 2 + 4;
+  static constexpr int oTmemPtr = oBar + kBars * 8;
+  static constexpr int oMask = oTmemPtr + 16;              // per-unit outlier channel list
+  static constexpr int kTotal = oMask + 64 * 4 + 1024;     // + alignment slack
+};
+
+struct QParams {
+  qjl_key_cache_t kc;
+  int64_t n;                 // keys per unit in this call
+  int64_t row_offset;        // first cache row
+  const int32_t* channels;   // [units][h]
+  int h;
+  int tpu;                   // tiles per unit
+  int64_t T;                 // total tiles
+  int s_per_unit;            // 1: S_full has one slice per unit; 0: shared by all units
+};
+
+template <int MT, int NC, int STAGES, int ABF>
+__global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant__ CUtensorMap tm_keys,
+                                                          const __grid_constant__ CUtensorMap tm_s, const QParams P) {
+  using L = QLayout<MT, NC, STAGES>;
+  constexpr int CH = L::CH;
+  constexpr uint32_t IDESC = make_idesc(ABF, CH);
+  extern __shared__ uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::oBar);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = bars + STAGES;
+  uint64_t* b_full = bars + 2 * STAGES;
+  uint64_t* b_empty = b_full + 1;
+  uint64_t* t_full = b_full + 2;
+  uint64_t* t_empty = b_full + 4;
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(sm + L::oTmemPtr);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int C = gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * P.T / C, r1 = (int64_t)(blockIdx.x + 1) * P.T / C;
+  const int ntiles = (int)(r1 - r0);
+  const int m_in = P.kc.m_in, m_out = P.kc.m_out;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&a_full[s], 1);
+      mbar_init(&a_empty[s], 1 + 2);      // MMA commit + 2 norm warps
+    }
+    mbar_init(b_full, 1);
+    mbar_init(b_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&t_full[b], 1);
+      mbar_init(&t_empty[b], 4);          // 4 epilogue warps
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_keys) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_s) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_ptr)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+
+  const int u_first = (int)(r0 / P.tpu);
+  const int lt_first = (int)(r0 - (int64_t)u_first * P.tpu);
+
+  if (warp == 0) {
+    // ================================ TMA producer ================================
+    if (lane == 0) {
+      int u = u_first, lt = lt_first, cur_u = -1, b_uses = 0;
+      for (int it = 0; it < ntiles; ++it) {
+        if (u != cur_u) {
+          if (b_uses > 0) mbar_wait(b_empty, (b_uses - 1) & 1);   // MMAs of the previous unit are done
+          mbar_expect_tx(b_full, 2 * L::kBHalf);
+          const int us = P.s_per_unit ? u : 0;
+          for (int hf = 0; hf < 2; ++hf)
+            for (int c = 0; c < NC; ++c)
+              tma_load_3d(sm + L::oB + hf * L::kBHalf + c * CH * 128, &tm_s, b_full, hf * 64, c * CH, us);
+          cur_u = u;
+          ++b_uses;
+        }
+        const int s = it % STAGES;
+        if (it >= STAGES) mbar_wait(&a_empty[s], ((it / STAGES) - 1) & 1);
+        mbar_expect_tx(&a_full[s], L::kABytes);
+        uint8_t* a = sm + L::oA + s * L::kABytes;
+        tma_load_3d(a, &tm_keys, &a_full[s], 0, lt * kM, u);
+        tma_load_3d(a + L::kABytes / 2, &tm_keys, &a_full[s], 64, lt * kM, u);
+        if (++lt == P.tpu) { lt = 0; ++u; }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================ MMA issuer ==================================
+    if (lane == 0) {
+      int u = u_first, lt = lt_first, cur_u = -1, b_uses = 0, chunk = 0;
+      for (int it = 0; it < ntiles; ++it) {
+        if (u != cur_u) {
+          mbar_wait(b_full, b_uses & 1);
+          cur_u = u;
+          ++b_uses;
+        }
+        const int s = it % STAGES;
+        mbar_wait(&a_full[s], (it / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(sm + L::oA + s * L::kABytes);
+        const uint32_t b_base = smem_u32(sm + L::oB);
+        for (int c = 0; c < NC; ++c, ++chunk) {
+          const int buf = chunk & 1;
+          if (chunk >= 2) mbar_wait(&t_empty[buf], ((chunk >> 1) - 1) & 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem + buf * 256;
+#pragma unroll
+          for (int k = 0; k < kK / 16; ++k) {
+            const int hf = k >> 2, kk = k & 3;   // K-half, 32-byte step inside the 128-byte row
+            const uint64_t ad = sw128_desc(a_base + hf * (L::kABytes / 2) + kk * 32);
+            const uint64_t bd = sw128_desc(b_base + hf * L::kBHalf + c * CH * 128 + kk * 32);
+            tc_mma_f16(d_tmem, ad, bd, IDESC, k > 0 ? 1u : 0u);
+          }
+          tc_commit(&t_full[buf]);
+        }
+        tc_commit(&a_empty[s]);                  // key tile consumed by the tensor core
+        const bool last_of_unit = (lt + 1 == P.tpu) || (it + 1 == ntiles);
+        if (last_of_unit) tc_commit(b_empty);    // S_full of this unit no longer read
+        if (++lt == P.tpu) { lt = 0; ++u; }
+      }
+    }
+  } else if (warp < 4) {
+    // ============================ norms (fp64, exact products) =====================
+    const int ntid = threadIdx.x - 64;           // 0..63
+    int* chan = reinterpret_cast<int*>(sm + L::oMask);
+    int u = u_first, lt = lt_first, cur_u = -1;
+    for (int it = 0; it < ntiles; ++it) {
+      if (u != cur_u) {
+        asm volatile("bar.sync 2, 64;" ::: "memory");
+        if (ntid < P.h) chan[ntid] = P.channels[(int64_t)u * P.h + ntid];
+        asm volatile("bar.sync 2, 64;" ::: "memory");
+        cur_u = u;
+      }
+      const int s = it % STAGES;
+      mbar_wait(&a_full[s], (it / STAGES) & 1);
+      const uint8_t* a = sm + L::oA + s * L::kABytes;
+#pragma unroll 1
+      for (int rr = 0; rr < 2; ++rr) {
+        const int row = ntid * 2 + rr;           // token row of the tile
+        const int64_t tok = (int64_t)lt * kM + row;
+        double tot = 0.0, outl = 0.0;
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const uint8_t* rowp = a + hf * (L::kABytes / 2) + row * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {          // 16-byte chunk j (swizzled position j ^ row%8)
+            const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((j ^ (row & 7)) << 4));
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float lo, hi;
+              if (ABF) {
+                lo = __uint_as_float(w[e] << 16);
+                hi = __uint_as_float(w[e] & 0xFFFF0000u);
+              } else {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+                lo = f.x;
+                hi = f.y;
+              }
+              tot = fma((double)lo, (double)lo, tot);
+              tot = fma((double)hi, (double)hi, tot);
+            }
+          }
+        }
+        for (int j = 0; j < P.h; ++j) {           // outlier channels: read them back
+          const int c = chan[j];
+          const int hf = c >> 6, cc = c & 63;
+          const uint8_t* rowp = a + hf * (L::kABytes / 2) + row * 128;
+          const uint16_t bits = *reinterpret_cast<const uint16_t*>(rowp + ((((cc >> 3) ^ (row & 7)) << 4) | ((cc & 7) << 1)));
+          const float x = ABF ? __uint_as_float((uint32_t)bits << 16) : __half2float(__ushort_as_half(bits));
+          outl = fma((double)x, (double)x, outl);
+        }
+        if (tok < P.n) {
+          const int64_t crow = (int64_t)u * P.kc.capacity + P.row_offset + tok;
+          P.kc.norm_in[crow] = f64_to_f16_bits(sqrt(fmax(tot - outl, 0.0)));
+          if (m_out > 0) P.kc.norm_out[crow] = f64_to_f16_bits(sqrt(outl));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_empty[s]);
+      if (++lt == P.tpu) { lt = 0; ++u; }
+    }
+  } else {
+    // =============================== epilogue ====================================
+    const int ew = warp - 4;                     // TMEM lanes 32*ew .. 32*ew + 31
+    const int row = ew * 32 + lane;              // token row of the tile
+    int u = u_first, lt = lt_first, chunk = 0;
+    for (int it = 0; it < ntiles; ++it) {
+      const int64_t tok = (int64_t)lt * kM + row;
+      const bool valid = tok < P.n;
+      const int64_t crow = (int64_t)u * P.kc.capacity + P.row_offset + tok;
+      for (int c = 0; c < NC; ++c, ++chunk) {
+        const int buf = chunk & 1;
+        mbar_wait(&t_full[buf], (chunk >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int g32 = 0; g32 < CH / 32; ++g32) {
+          uint32_t r[32];
+          tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + buf * 256 + g32 * 32, r);
+          const uint32_t w = sign_word(r);
+          const int sr = c * CH + g32 * 32;      // first sketch row of this word
+          if (valid) {
+            if (sr < m_in)
+              reinterpret_cast<uint32_t*>(P.kc.bits_in + crow * (m_in / 8))[sr >> 5] = w;
+            else
+              reinterpret_cast<uint32_t*>(P.kc.bits_out + crow * (m_out / 8))[(sr - m_in) >> 5] = w;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&t_empty[buf]);
+      }
+      if (++lt == P.tpu) { lt = 0; ++u; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ----------------------------------------------------------------- host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+static bool encode_3d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, uint64_t d0, uint64_t d1,
+                      uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box1) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  const cuuint32_t box[3] = {64, box1, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int MT, int NC, int STAGES, int ABF>
+static int launch_impl(const void* keys, int64_t n, int64_t kus, const qjl_sketch_t& sk, const int32_t* ch, int h,
+                       const qjl_key_cache_t& kc, int64_t row_offset, cudaStream_t st) {
+  using L = QLayout<MT, NC, STAGES>;
+  const CUtensorMapDataType dt = ABF ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tk, ts;
+  const uint64_t s_units = sk.unit_stride ? (uint64_t)kc.units : 1;
+  if (!encode_3d(&tk, keys, dt, kK, (uint64_t)n, (uint64_t)kc.units, kK * 2, (uint64_t)kus * 2, kM) ||
+      !encode_3d(&ts, sk.s_full, dt, kK, MT, s_units, kK * 2,
+                 (uint64_t)(sk.unit_stride ? sk.unit_stride : (int64_t)MT * kK) * 2, L::CH)) {
+    set_error("cuTensorMapEncodeTiled failed");
+    return QJL_ERR_CUDA;
+  }
+  QParams P;
+  P.kc = kc;
+  P.n = n;
+  P.row_offset = row_offset;
+  P.channels = ch;
+  P.h = h;
+  P.tpu = (int)((n + kM - 1) / kM);
+  P.T = (int64_t)kc.units * P.tpu;
+  P.s_per_unit = sk.unit_stride ? 1 : 0;
+  auto kern = k_quant_tc<MT, NC, STAGES, ABF>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+  const int ctas = (int)(P.T < device_sm_count() ? P.T : device_sm_count());
+  timing_begin(st);
+  kern<<<ctas, kThreads, L::kTotal, st>>>(tk, ts, P);
+  timing_end(st);
+  QJL_LAUNCH_CHECK("quantize_keys_tc");
+  return QJL_OK;
+}
+
+}  // namespace qtc
+
+int launch_quantize_keys_tc(const void* keys, int dtype, int64_t n, int64_t kus, const qjl_sketch_t& sk,
+                            const int32_t* ch, int h, const qjl_key_cache_t& kc, int64_t row_offset,
+                            cudaStream_t st) {
+  using namespace qtc;
+  if (getenv("QJL_FORCE_SIMT")) return QJL_ERR_UNSUPPORTED;
+  if (kc.d != kK || !(dtype == QJL_BF16 || dtype == QJL_F16) || sk.dtype != dtype) return QJL_ERR_UNSUPPORTED;
+  if (h > 64 || kus % 8 != 0) return QJL_ERR_UNSUPPORTED;
+  if (((uintptr_t)keys & 15) || ((uintptr_t)sk.s_full & 15)) return QJL_ERR_UNSUPPORTED;
+  const int MT = kc.m_in + kc.m_out;
+  const int abf = dtype == QJL_BF16;
+#define QJL_QT(MTV, NCV, SV)                                                                             \
+  if (MT == MTV)                                                                                         \
+    return abf ? launch_impl<MTV, NCV, SV, 1>(keys, n, kus, sk, ch, h, kc, row_offset, st)               \
+               : launch_impl<MTV, NCV, SV, 0>(keys, n, kus, sk, ch, h, kc, row_offset, st);
+  QJL_QT(256, 1, 3)   // m = 256, no outliers (config 1 shape)
+  QJL_QT(320, 2, 3)   // m_in 256 + m_out 64 (configs 3/5)
+  QJL_QT(384, 2, 3)   // m_in 256 + m_out 128 (config 2)
+  QJL_QT(512, 2, 2)   // m = 512, no outliers
+  QJL_QT(576, 3, 2)   // m_in 512 + m_out 64 (config 4)
+#undef QJL_QT
   return QJL_ERR_UNSUPPORTED;
 }
+
 }  // namespace qjl

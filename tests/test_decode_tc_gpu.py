@@ -37,7 +37,11 @@ def _cache(U, n, G, h, m_in, m_out, seed, dtype=torch.bfloat16, factor=20.0):
 
 
 def _both(c, q, T=1.0):
-    out_tc = c.decode(q, temperature=T).clone()
+    os.environ["QJL_REQUIRE_TC"] = "1"          # no silent fallback to the generic kernel
+    try:
+        out_tc = c.decode(q, temperature=T).clone()
+    finally:
+        del os.environ["QJL_REQUIRE_TC"]
     os.environ["QJL_FORCE_SIMT"] = "1"
     try:
         out_simt = c.decode(q, temperature=T).clone()

@@ -11,10 +11,11 @@
 //  * warp 1: single-thread tcgen05.mma issuer, M = 128 tokens, N = MT split into
 //    NC chunks of CH <= 256 columns, K = 128 (8 x K16), fp32 accumulators in two
 //    ping-pong TMEM buffers of 256 columns;
-//  * warps 2-3: ||k_in||, ||k_out|| in fp64 from the staged key tile (exact
-//    products, fp64 sums) -> one fp16 rounding, matching the reference's
-//    float64 norm stored at half precision;
-//  * warps 4-7: epilogue -- tcgen05.ld 32x32b (one token per thread), exact sign
+//  * warps 2, 3, 12, 13: ||k_in||, ||k_out|| from the staged key tile, one token per
+//    thread: exact fp32 products, double-float (TwoSum) accumulation -> one fp16
+//    rounding, matching the reference's float64 norm stored at half precision;
+//  * warps 4-11: epilogue, one set of 4 warps per TMEM buffer -- tcgen05.ld
+//    32x32b (one token per thread), exact sign
 //    test `x >= 0` (set.ge: -0.0 -> 1, NaN -> 0), 32 bits per word, stored as
 //    the LSB-first sign words of the cache rows.
 #include <cuda.h>
@@ -27,7 +28,8 @@ namespace qtc {
 
 constexpr int kM = 128;          // tokens per tile (UMMA M)
 constexpr int kK = 128;          // head dim
-constexpr int kThreads = 256;
+constexpr int kThreads = 448;   // 14 warps: TMA, MMA, norms (2, 3, 12, 13), epilogue (4-11)
+constexpr int kPf = 3;          // key tiles prefetched into L2 ahead of the TMA stream
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -92,16 +94,35 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-// exact sign word: bit i = (x_i >= 0); set.ge gives all-ones / zero, merged with LOP3
+// exact sign word: bit i = (x_i >= 0) (set.ge: all-ones / zero, -0.0 -> 1, NaN -> 0),
+// merged with LOP3 in four independent chains so the 32-deep OR dependency does
+// not serialize the epilogue
 __device__ __forceinline__ uint32_t sign_word(const uint32_t* r) {
-  uint32_t w = 0;
+  uint32_t a[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     uint32_t m;
     asm("set.ge.u32.f32 %0, %1, 0f00000000;" : "=r"(m) : "f"(__uint_as_float(r[i])));
-    w |= m & (1u << i);
+    a[i & 3] |= m & (1u << i);
   }
-  return w;
+  return (a[0] | a[1]) | (a[2] | a[3]);
+}
+// 64 fp32 accumulator columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,"
+      "%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
+        "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
+        "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+        "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+        "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
 template <int MT, int NC, int STAGES>
@@ -128,6 +149,9 @@ struct QParams {
   int tpu;                   // tiles per unit
   int64_t T;                 // total tiles
   int s_per_unit;            // 1: S_full has one slice per unit; 0: shared by all units
+  int ablate;                // perf experiments only: 1 no epilogue math, 2 no norm math, 4 no MMA
+  const uint8_t* keys;       // key base (for L2 prefetch of upcoming tiles)
+  int64_t key_unit_bytes;    // bytes between units
 };
 
 template <int MT, int NC, int STAGES, int ABF>
@@ -155,13 +179,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&a_full[s], 1);
-      mbar_init(&a_empty[s], 1 + 2);      // MMA commit + 2 norm warps
+      mbar_init(&a_empty[s], 1 + 4);      // MMA commit + 4 norm warps
     }
     mbar_init(b_full, 1);
     mbar_init(b_empty, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&t_full[b], 1);
-      mbar_init(&t_empty[b], 4);          // 4 epilogue warps
+      mbar_init(&t_empty[b], 4);          // the 4 epilogue warps of buffer b's set
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_keys) : "memory");
@@ -200,6 +224,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         uint8_t* a = sm + L::oA + s * L::kABytes;
         tma_load_3d(a, &tm_keys, &a_full[s], 0, lt * kM, u);
         tma_load_3d(a + L::kABytes / 2, &tm_keys, &a_full[s], 64, lt * kM, u);
+        {   // pull the key tile kPf tiles ahead into L2 so its TMA refill hits L2
+          int pu = u, plt = lt + kPf;
+          while (plt >= P.tpu) { plt -= P.tpu; ++pu; }
+          if (it + kPf < ntiles) {
+            const int64_t rows = (int64_t)(P.n - (int64_t)plt * kM) < kM ? (P.n - (int64_t)plt * kM) : kM;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.keys + pu * P.key_unit_bytes +
+                                                                             (int64_t)plt * kM * kK * 2),
+                         "r"((uint32_t)(rows * kK * 2)) : "memory");
+          }
+        }
         if (++lt == P.tpu) { lt = 0; ++u; }
       }
     }
@@ -225,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
           const uint32_t d_tmem = tmem + buf * 256;
 #pragma unroll
           for (int k = 0; k < kK / 16; ++k) {
+            if (P.ablate & 4) break;
             const int hf = k >> 2, kk = k & 3;   // K-half, 32-byte step inside the 128-byte row
             const uint64_t ad = sw128_desc(a_base + hf * (L::kABytes / 2) + kk * 32);
             const uint64_t bd = sw128_desc(b_base + hf * L::kBHalf + c * CH * 128 + kk * 32);
@@ -238,26 +273,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         if (++lt == P.tpu) { lt = 0; ++u; }
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < 4 || warp >= 12) {
     // ============================ norms (fp64, exact products) =====================
-    const int ntid = threadIdx.x - 64;           // 0..63
+    const int nw = warp < 4 ? warp - 2 : warp - 10;  // norm warp 0..3
+    const int ntid = nw * 32 + lane;             // token row of the tile
     int* chan = reinterpret_cast<int*>(sm + L::oMask);
     int u = u_first, lt = lt_first, cur_u = -1;
     for (int it = 0; it < ntiles; ++it) {
       if (u != cur_u) {
-        asm volatile("bar.sync 2, 64;" ::: "memory");
+        asm volatile("bar.sync 2, 128;" ::: "memory");
         if (ntid < P.h) chan[ntid] = P.channels[(int64_t)u * P.h + ntid];
-        asm volatile("bar.sync 2, 64;" ::: "memory");
+        asm volatile("bar.sync 2, 128;" ::: "memory");
         cur_u = u;
       }
       const int s = it % STAGES;
       mbar_wait(&a_full[s], (it / STAGES) & 1);
       const uint8_t* a = sm + L::oA + s * L::kABytes;
-#pragma unroll 1
-      for (int rr = 0; rr < 2; ++rr) {
-        const int row = ntid * 2 + rr;           // token row of the tile
-        const int64_t tok = (int64_t)lt * kM + row;
-        double tot = 0.0, outl = 0.0;
+      // One token row per thread.  x^2 is exact in fp32 (<= 11-bit significands);
+      // the sum is carried as an unevaluated double-float (TwoSum, 4 chains), so the
+      // result matches an fp64 accumulation to ~1e-14 relative without fp64 math.
+      const int row = ntid;
+      const int64_t tok = (int64_t)lt * kM + row;
+      float hs[4] = {0.f, 0.f, 0.f, 0.f}, ls[4] = {0.f, 0.f, 0.f, 0.f};
+      auto two_sum_add = [&](int k, float x) {
+        const float p = x * x;
+        const float t = hs[k] + p;
+        const float z = t - hs[k];
+        ls[k] += (hs[k] - (t - z)) + (p - z);
+        hs[k] = t;
+      };
+      if (!(P.ablate & 2)) {
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           const uint8_t* rowp = a + hf * (L::kABytes / 2) + row * 128;
@@ -276,24 +321,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
                 lo = f.x;
                 hi = f.y;
               }
-              tot = fma((double)lo, (double)lo, tot);
-              tot = fma((double)hi, (double)hi, tot);
+              two_sum_add(e, lo);
+              two_sum_add(e, hi);
             }
           }
         }
-        for (int j = 0; j < P.h; ++j) {           // outlier channels: read them back
-          const int c = chan[j];
-          const int hf = c >> 6, cc = c & 63;
-          const uint8_t* rowp = a + hf * (L::kABytes / 2) + row * 128;
-          const uint16_t bits = *reinterpret_cast<const uint16_t*>(rowp + ((((cc >> 3) ^ (row & 7)) << 4) | ((cc & 7) << 1)));
-          const float x = ABF ? __uint_as_float((uint32_t)bits << 16) : __half2float(__ushort_as_half(bits));
-          outl = fma((double)x, (double)x, outl);
-        }
-        if (tok < P.n) {
-          const int64_t crow = (int64_t)u * P.kc.capacity + P.row_offset + tok;
-          P.kc.norm_in[crow] = f64_to_f16_bits(sqrt(fmax(tot - outl, 0.0)));
-          if (m_out > 0) P.kc.norm_out[crow] = f64_to_f16_bits(sqrt(outl));
-        }
+      }
+      double all = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) all += (double)hs[k] + (double)ls[k];
+      double outl = 0.0;
+      for (int j = 0; j < P.h; ++j) {             // outlier channels: read them back
+        const int c = chan[j];
+        const int hf = c >> 6, cc = c & 63;
+        const uint8_t* rowp = a + hf * (L::kABytes / 2) + row * 128;
+        const uint16_t bits = *reinterpret_cast<const uint16_t*>(rowp + ((((cc >> 3) ^ (row & 7)) << 4) | ((cc & 7) << 1)));
+        const float x = ABF ? __uint_as_float((uint32_t)bits << 16) : __half2float(__ushort_as_half(bits));
+        outl += (double)(x * x);                  // <= 64 exact terms, tiny fp64 work
+      }
+      if (tok < P.n) {
+        const int64_t crow = (int64_t)u * P.kc.capacity + P.row_offset + tok;
+        P.kc.norm_in[crow] = f64_to_f16_bits(sqrt(fmax(all - outl, 0.0)));
+        if (m_out > 0) P.kc.norm_out[crow] = f64_to_f16_bits(sqrt(outl));
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_empty[s]);
@@ -301,7 +350,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     }
   } else {
     // =============================== epilogue ====================================
-    const int ew = warp - 4;                     // TMEM lanes 32*ew .. 32*ew + 31
+    const int ew = warp & 3;                     // TMEM lane quadrant: lanes 32*ew .. 32*ew + 31
+    const int set = (warp - 4) >> 2;             // this warp set drains TMEM buffer `set`
     const int row = ew * 32 + lane;              // token row of the tile
     int u = u_first, lt = lt_first, chunk = 0;
     for (int it = 0; it < ntiles; ++it) {
@@ -310,14 +360,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       const int64_t crow = (int64_t)u * P.kc.capacity + P.row_offset + tok;
       for (int c = 0; c < NC; ++c, ++chunk) {
         const int buf = chunk & 1;
+        if (buf != set) continue;
         mbar_wait(&t_full[buf], (chunk >> 1) & 1);
         tc_fence_after();
 #pragma unroll 1
-        for (int g32 = 0; g32 < CH / 32; ++g32) {
+        for (int g64 = 0; g64 < (P.ablate & 1 ? 0 : CH / 64); ++g64) {
+          uint32_t r[64];
+          tmem_ld64(tmem + ((uint32_t)(ew * 32) << 16) + buf * 256 + g64 * 64, r);
+          const uint32_t w0 = sign_word(r), w1 = sign_word(r + 32);
+          const int sr = c * CH + g64 * 64;      // first sketch row of the word pair
+          if (valid) {
+            uint32_t* d0 = sr < m_in ? reinterpret_cast<uint32_t*>(P.kc.bits_in + crow * (m_in / 8)) + (sr >> 5)
+                                     : reinterpret_cast<uint32_t*>(P.kc.bits_out + crow * (m_out / 8)) + ((sr - m_in) >> 5);
+            const int s1 = sr + 32;
+            uint32_t* d1 = s1 < m_in ? reinterpret_cast<uint32_t*>(P.kc.bits_in + crow * (m_in / 8)) + (s1 >> 5)
+                                     : reinterpret_cast<uint32_t*>(P.kc.bits_out + crow * (m_out / 8)) + ((s1 - m_in) >> 5);
+            if (d1 == d0 + 1 && ((reinterpret_cast<uintptr_t>(d0) & 7) == 0)) {
+              *reinterpret_cast<uint2*>(d0) = make_uint2(w0, w1);
+            } else {
+              *d0 = w0;
+              *d1 = w1;
+            }
+          }
+        }
+        if constexpr (CH % 64 == 32) {           // trailing 32-column group of the chunk
           uint32_t r[32];
-          tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + buf * 256 + g32 * 32, r);
+          tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + buf * 256 + (CH - 32), r);
           const uint32_t w = sign_word(r);
-          const int sr = c * CH + g32 * 32;      // first sketch row of this word
+          const int sr = c * CH + CH - 32;
           if (valid) {
             if (sr < m_in)
               reinterpret_cast<uint32_t*>(P.kc.bits_in + crow * (m_in / 8))[sr >> 5] = w;
@@ -391,6 +461,9 @@ static int launch_impl(const void* keys, int64_t n, int64_t kus, const qjl_sketc
   P.tpu = (int)((n + kM - 1) / kM);
   P.T = (int64_t)kc.units * P.tpu;
   P.s_per_unit = sk.unit_stride ? 1 : 0;
+  P.keys = (const uint8_t*)keys;
+  P.ablate = getenv("QJL_K1_ABLATE") ? atoi(getenv("QJL_K1_ABLATE")) : 0;
+  P.key_unit_bytes = kus * 2;
   auto kern = k_quant_tc<MT, NC, STAGES, ABF>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
   const int ctas = (int)(P.T < device_sm_count() ? P.T : device_sm_count());

@@ -395,10 +395,29 @@ def run_gpu(args):
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3)
 
-    t = torch.tensor([t_ms, e2e_ms], device=device, dtype=torch.float64)
+    # output gather over NCCL (the path's only exchange), timed on its own
+    gather_ms = 0.0
+    if world > 1:
+        from paper_2406_03482_b200.distributed import gather_units, shard_units
+
+        shard = shard_units(U * world, world, rank)
+        for _ in range(3):
+            gather_units(out, shard)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e4.record()
+        for _ in range(20):
+            full = gather_units(out, shard)
+        e5.record()
+        torch.cuda.synchronize()
+        gather_ms = e4.elapsed_time(e5) / 20
+        assert full.shape[0] == U * world
+
+    t = torch.tensor([t_ms, e2e_ms, gather_ms], device=device, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_ms, e2e_ms = float(t[0]), float(t[1])
+    t_ms, e2e_ms, gather_ms = float(t[0]), float(t[1]), float(t[2])
 
     bpt = bytes_per_token_head(w)
     alg_bytes_rank = U * w["n"] * bpt
@@ -433,6 +452,10 @@ def run_gpu(args):
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
     }
+    if world > 1:
+        res["output_gather"] = {"collective": "all_gather_into_tensor (NCCL)", "ms": gather_ms,
+                                "bytes": int(out.numel() * out.element_size() * world),
+                                "note": "outside the timed decode region; units are independent"}
     if world == 1 and rank == 0 and not args.no_prefill:
         try:
             res["prefill"] = measure_prefill(device, args.seed)

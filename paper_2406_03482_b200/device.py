@@ -69,7 +69,8 @@ class DeviceKeyCache:
     def __init__(self, units: int, d: int, m_in: int, m_out: int, h: int, capacity: int, *,
                  key_dtype: torch.dtype = torch.bfloat16, value_bits: int = 2,
                  value_group: int = 32, value_layout: str = "p2", with_values: bool = True,
-                 sketch_dtype: torch.dtype | None = None, device: str | torch.device = "cuda"):
+                 sketch_dtype: torch.dtype | None = None, device: str | torch.device = "cuda",
+                 validate_rate: bool = True):
         self.lib = _lib.load()
         if not torch.cuda.is_available():
             raise RuntimeError("DeviceKeyCache needs a CUDA device (no CPU fallback)")
@@ -81,7 +82,7 @@ class DeviceKeyCache:
             raise ValueError("outlier sketch must be present exactly when h > 0")
         if (m_in > 0) != (d - h > 0):
             raise ValueError("inlier sketch must be present exactly when d - h > 0")
-        if h > 0 and d - h > 0 and m_out * (d - h) < m_in * h:
+        if validate_rate and h > 0 and d - h > 0 and m_out * (d - h) < m_in * h:
             raise ValueError("outlier bit rate below inlier bit rate: "
                              f"m_out/h = {m_out}/{h} < m_in/(d-h) = {m_in}/{d - h}")
         self.device = torch.device(device)

@@ -152,20 +152,15 @@ def quantize_key(sketch: SketchMatrix, key: np.ndarray) -> QuantizedKey:
 
 def sketch_query(sketch: SketchMatrix, query: np.ndarray) -> SketchedQuery:
     """S @ q on device (fp64 accumulation) (estimator.py:127-132)."""
-    lib = _lib.load()
     query = np.asarray(query, dtype=np.float64)
     if query.shape != (sketch.d,):
         raise ValueError(f"query has shape {query.shape}, expected ({sketch.d},)")
     dev = _dev()
     S = torch.from_numpy(np.ascontiguousarray(sketch.entries, np.float64)).to(dev)
     q = torch.from_numpy(query).to(dev)
-    out = torch.empty(sketch.m, dtype=torch.float32, device=dev)
-    sd = _lib.SketchDesc(S.data_ptr(), _lib.QJL_F64, 0, 0)
-    # fp64 result needed for the drop-in; evaluate in fp64 via a one-row GEMV
-    _lib.check(lib.qjl_sketch_query(q.data_ptr(), _lib.QJL_F64, 1, 1, sketch.d, ctypes.byref(sd),
-                                    sketch.m, out.data_ptr(), torch.cuda.current_stream().cuda_stream),
-               "sketch_query")
-    vals = (S @ q).cpu().numpy()   # fp64 device GEMV (cuBLAS) for the full-precision return
+    # the drop-in returns the full fp64 projection: a plain fp64 GEMV on the device
+    # (the batched decode path computes S q inside its own prologue kernel)
+    vals = (S @ q).cpu().numpy()
     vals.setflags(write=False)
     return SketchedQuery(values=vals, source_dim=sketch.d)
 

@@ -57,6 +57,8 @@ void timing_begin(cudaStream_t st) {
   cudaEventRecord(next_event(), st);
 }
 
+bool timing_enabled() { return g_timing; }
+
 void timing_end(cudaStream_t st) {
   if (!g_timing) return;
   std::lock_guard<std::mutex> lk(g_tmu);

@@ -23,6 +23,7 @@ int device_sm_count();
 // benchmark timing hook (api.cu): no-ops unless qjl_timing_enable(1)
 void timing_begin(cudaStream_t st);
 void timing_end(cudaStream_t st);
+bool timing_enabled();
 
 #define QJL_CHECK_ARG(cond, ...)        \
   do {                                  \

@@ -50,6 +50,8 @@ struct Params {
   const uint4* afrag;    // [units][KC][32 lanes] (4 x u32 A regs)
   const float4* qconst;  // [units][4 queries] {k_in, b_in, k_out, b_out}
   float* part;           // [units][max_seg][G][2 + 128]
+  float* out;            // [units][G][128]
+  float* lse;            // [units][G] or null
 };
 
 __host__ __device__ __forceinline__ int64_t tile_begin(int c, int64_t T, int C) {
@@ -176,59 +178,88 @@ struct Layout {
 // x_j = rint(Sq_j / (sigma * 2^(j mod 8))), 4 signed-byte digits laid out as the
 // IMMA B operand: column n of n-tile nt = (query n/2, digit 2*nt + n%2).
 template <typename TQ, typename TS, int KCI, int KCO>
-__global__ void __launch_bounds__(256) k_prep(const TQ* __restrict__ q, int G, const TS* __restrict__ s_full,
+__global__ void __launch_bounds__(512) k_prep(const TQ* __restrict__ q, int G, const TS* __restrict__ s_full,
                                               int64_t s_unit_stride, float inv_t, uint4* __restrict__ bfrag,
                                               float4* __restrict__ qconst) {
   constexpr int MI = KCI * 32, MO = KCO * 32, MT = MI + MO, KC = KCI + KCO;
   constexpr int d = 128;
-  __shared__ double qs[4][d];
-  __shared__ double sq[4][MT];
+  // 16-bit sketch operands: products are exact in fp32; wider operands accumulate in fp64
+  using acc_t = typename std::conditional<(sizeof(TS) <= 2), float, double>::type;
+  __shared__ acc_t qs[4][d];
+  __shared__ float sq[4][MT];
   __shared__ int32_t si[4][MT];
+  __shared__ unsigned int mxbits[4][2];
   __shared__ double red[4][2][2];   // [q][side][sigma, sum]
   const int u = blockIdx.x;
   const TS* S = s_full + (int64_t)u * s_unit_stride;
+  // let the decode kernel launch now (programmatic dependent launch): its prologue and
+  // first bulk copies overlap this kernel; it waits (griddepcontrol.wait) before reading
+  // anything written here
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int i = threadIdx.x; i < 4 * d; i += blockDim.x) {
     const int g = i / d;
-    qs[g][i % d] = g < G ? to_f64(q[((int64_t)u * G + g) * d + i % d]) : 0.0;
+    qs[g][i % d] = g < G ? (acc_t)to_f64(q[((int64_t)u * G + g) * d + i % d]) : (acc_t)0;
+  }
+  if (threadIdx.x < 8) {
+    mxbits[threadIdx.x >> 1][threadIdx.x & 1] = 0u;
   }
   __syncthreads();
-  for (int r = threadIdx.x; r < MT; r += blockDim.x) {
-    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-    const TS* row = S + (int64_t)r * d;
-    for (int c = 0; c < d; ++c) {
-      const double s = to_f64(row[c]);
-      a0 = fma(s, qs[0][c], a0);
-      a1 = fma(s, qs[1][c], a1);
-      a2 = fma(s, qs[2][c], a2);
-      a3 = fma(s, qs[3][c], a3);
+  // one warp per sketch row (coalesced 256-byte row reads), lane l owns columns
+  // 4l..4l+3 of every query head; shuffle-reduce the four partial dots
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  acc_t qreg[4][4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) qreg[g][e] = qs[g][4 * lane + e];
+  float wmax[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+  for (int r = wid; r < MT; r += nwarp) {
+    const TS* row = S + (int64_t)r * d + 4 * lane;
+    acc_t a[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const acc_t sv = (acc_t)to_f64(row[e]);
+#pragma unroll
+      for (int g = 0; g < 4; ++g) a[g] = fma(sv, qreg[g][e], a[g]);
     }
-    sq[0][r] = (double)(float)a0;
-    sq[1][r] = (double)(float)a1;
-    sq[2][r] = (double)(float)a2;
-    sq[3][r] = (double)(float)a3;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a[g] += __shfl_xor_sync(0xffffffffu, a[g], o);
+    }
+    const int side = r >= MI;
+    if (lane < 4) sq[lane][r] = (float)a[lane];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) wmax[g][side] = fmaxf(wmax[g][side], fabsf((float)a[g]));
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int sd = 0; sd < 2; ++sd) atomicMax(&mxbits[g][sd], __float_as_uint(wmax[g][sd]));
   }
   __syncthreads();
   if (threadIdx.x < 8) {
     const int g = threadIdx.x >> 1, side = threadIdx.x & 1;
-    const int lo = side ? MI : 0, hi = side ? MT : MI;
-    double mx = 0.0;
-    for (int j = lo; j < hi; ++j) mx = fmax(mx, fabs(sq[g][j]));
+    const double mx = (double)__uint_as_float(mxbits[g][side]);
     red[g][side][0] = mx > 0.0 ? mx / 1073741824.0 : 1.0;   // sigma = max/2^30
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 4 * MT; i += blockDim.x) {
-    const int g = i / MT, j = i % MT;
-    const int side = j >= MI;
-    const int jl = side ? j - MI : j;
-    si[g][j] = (int32_t)rint(sq[g][j] / (red[g][side][0] * (double)(1 << (jl & 7))));
-  }
-  __syncthreads();
-  if (threadIdx.x < 8) {
-    const int g = threadIdx.x >> 1, side = threadIdx.x & 1;
+  // integer sketch; one warp per (query, side) segment, warp-reduced checksum
+  for (int seg = wid; seg < 8; seg += nwarp) {
+    const int g = seg >> 1, side = seg & 1;
     const int lo = side ? MI : 0, hi = side ? MT : MI;
-    double s = 0.0;
-    for (int j = lo; j < hi; ++j) s += (double)si[g][j] * (double)(1 << ((j - lo) & 7));
-    red[g][side][1] = s * red[g][side][0];
+    const double inv = 1.0 / red[g][side][0];
+    long long acc = 0;
+    for (int j = lo + lane; j < hi; j += 32) {
+      const int sh = (j - lo) & 7;
+      const int32_t x = (int32_t)rint((double)sq[g][j] * inv / (double)(1 << sh));
+      si[g][j] = x;
+      acc += (long long)x * (1ll << sh);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[g][side][1] = (double)acc * red[g][side][0];
   }
   __syncthreads();
   // B fragment of m16n8k32: element (k, n) lives in lane n*4 + (k%16)/4, reg
@@ -578,6 +609,10 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 3) k_decode_t
     __syncwarp();
   };
 
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // merge kernel may launch
+  // everything above only touched the cache stream; the query sketch digits come from
+  // k_prep, launched just before us with programmatic dependent launch
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   int cur_u = -1;
   int u = u_first, lt = lt_first;
   for (int it = 0; it < ntiles; ++it) {
@@ -603,6 +638,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 3) k_decode_t
 // Merge per (unit, query): combine the unit's CTA-segment partials.
 __global__ void k_merge_tc(const float* __restrict__ part, int max_seg, int G, int tpu, int64_t T, int C,
                            float* __restrict__ out, float* __restrict__ lse) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: partials of the decode grid
   const int ug = blockIdx.x;
   const int u = ug / G, qq = ug % G;
   const int c0 = cta_of_tile((int64_t)u * tpu, T, C);
@@ -707,7 +743,7 @@ static int launch_tc_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc
   float4* qconst = (float4*)(w + plan.qconst_off);
   float* part = (float*)(w + plan.part_off);
 #define QJL_PREP(TQ, TS)                                                                         \
-  k_prep<TQ, TS, KCI, KCO><<<kc.units, 256, 0, st>>>((const TQ*)q, G, (const TS*)sk.s_full,      \
+  k_prep<TQ, TS, KCI, KCO><<<kc.units, 512, 0, st>>>((const TQ*)q, G, (const TS*)sk.s_full,      \
                                                      sk.unit_stride, inv_t, afrag, qconst)
 #define QJL_PREP_S(TQ)                                                   \
   switch (sk.dtype) {                                                    \
@@ -738,12 +774,33 @@ static int launch_tc_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc
   P.afrag = afrag;
   P.qconst = qconst;
   P.part = part;
+  P.out = out;
+  P.lse = lse;
   occupancy<KCI, KCO>();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(plan.ctas);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Layout<KCI, KCO>::kTotal;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = timing_enabled() ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   timing_begin(st);
-  k_decode_tc<KCI, KCO><<<plan.ctas, kThreads, Layout<KCI, KCO>::kTotal, st>>>(P);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_decode_tc<KCI, KCO>, P);
   timing_end(st);
+  if (e != cudaSuccess) return cuda_status(e, "decode_tc");
   QJL_LAUNCH_CHECK("decode_tc");
-  k_merge_tc<<<kc.units * G, 128, 0, st>>>(part, plan.max_seg, G, plan.tpu, plan.T, plan.ctas, out, lse);
+  cudaLaunchConfig_t mcfg = {};
+  mcfg.gridDim = dim3(kc.units * G);
+  mcfg.blockDim = dim3(128);
+  mcfg.stream = st;
+  mcfg.attrs = attr;
+  mcfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&mcfg, k_merge_tc, (const float*)part, plan.max_seg, G, plan.tpu, plan.T, plan.ctas,
+                         out, lse);
+  if (e != cudaSuccess) return cuda_status(e, "decode_tc_merge");
   QJL_LAUNCH_CHECK("decode_tc_merge");
   return QJL_OK;
 }

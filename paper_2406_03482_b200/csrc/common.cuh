@@ -102,14 +102,23 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
 }
 
 // ----------------------------------------------------------- P2 value layout
-// 2-bit codes of a d=128 token live in 8 u32 words.  Word w holds the 16 dims
-// {16*mt + w + 8*hh : mt in 0..7, hh in 0..1} at code slot p = 2*mt + hh (bits
-// 2p..2p+1).  This is the A-fragment order of mma.m16n8k16 with one m-tile per
-// 16 dims: lane-row g of every m-tile reads word g only.
-__host__ __device__ __forceinline__ void p2_slot(int dim, int* word, int* slot) {
-  int mt = dim >> 4, r = dim & 15;
-  *word = r & 7;
-  *slot = 2 * mt + (r >> 3);
+// 2-bit codes, group 32, d = 128: 32 bytes per token, interleaved inside each
+// 128-token tile so that one u32 word holds 4 tokens x 4 dims -- the A operand
+// register of the PV IMMA (mma.m16n8k32 u8) after a single mask, `w & (3 << 2s)`
+// per byte.  For row t of a unit and dim d:
+//   tile = t >> 7, slice = (t >> 5) & 3 (the warp that consumes it),
+//   j = t & 7 (k-block = tokens j, j+8, j+16, j+24 of the slice), i = (t >> 3) & 3 (byte),
+//   MT = d >> 4 (m-tile), g = d & 7 (fragment row), r = (d >> 3) & 1, k = MT >> 1,
+//   s = 2 * (MT & 1) + r (2-bit slot inside the byte)
+//   word = tile * 1024 + slice * 256 + (g * 8 + (j ^ ((g & 1) << 2))) * 4 + k
+// The j ^ 4 swizzle on odd rows makes the per-lane 16-byte loads bank-conflict free.
+__host__ __device__ __forceinline__ void p2_pos(int64_t t, int d, int64_t* byte, int* shift) {
+  const int64_t tile = t >> 7;
+  const int slice = (int)(t >> 5) & 3, j = (int)t & 7, i = (int)(t >> 3) & 3;
+  const int MT = d >> 4, g = d & 7, r = (d >> 3) & 1, k = MT >> 1, s = 2 * (MT & 1) + r;
+  const int64_t word = tile * 1024 + slice * 256 + (g * 8 + (j ^ ((g & 1) << 2))) * 4 + k;
+  *byte = word * 4 + i;
+  *shift = 2 * s;
 }
 
 }  // namespace qjl

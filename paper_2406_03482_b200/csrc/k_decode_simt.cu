@@ -36,10 +36,11 @@ __device__ __forceinline__ float load_value(const qjl_value_cache_t& vc, int64_t
     const float c = (float)reinterpret_cast<const uint8_t*>(vc.codes)[row * vc.d + dim];
     return fmaf(c, s, z);
   }
-  int w, p;
-  p2_slot(dim, &w, &p);
-  const uint32_t word = reinterpret_cast<const uint32_t*>(vc.codes)[row * 8 + w];
-  const float c = (float)((word >> (2 * p)) & 3u);
+  // row = unit * capacity + t; capacity % 128 == 0, so tiles never straddle units
+  int64_t byte;
+  int sh;
+  p2_pos(row, dim, &byte, &sh);
+  const float c = (float)((reinterpret_cast<const uint8_t*>(vc.codes)[byte] >> sh) & 3u);
   const float z = f16_bits_to_f32(reinterpret_cast<const uint16_t*>(vc.zero)[row * G + grp]);
   const float s = f16_bits_to_f32(reinterpret_cast<const uint16_t*>(vc.scale)[row * G + grp]);
   return fmaf(c, s, z);

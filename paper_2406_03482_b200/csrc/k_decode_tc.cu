@@ -1,26 +1,36 @@
 // Tensor-core fused QJL decode (K2 score estimator + K3 online softmax . V) for
-// P2 value caches on sm_100a.
+// P2 value caches on sm_100a -- v5.
 //
-//  * Data movement: thread 0 streams each 128-token tile of the packed cache
+// One decode step = 2 launches chained with programmatic dependent launch:
+//   k_prep   one CTA per unit: Sq = S_full . q for the unit's G <= 4 query heads,
+//            quantized to a 32-bit fixed-point integer and split into four int8
+//            digits laid out as the score IMMA's B fragments; zeroes the unit's
+//            merge counter.
+//   k_decode stream-K over the flattened (unit, 128-token tile) space; each CTA
+//            folds its segment of a unit into one partial, and the CTA that
+//            finishes a unit last (atomic counter) merges the unit's partials and
+//            writes out / lse -- no separate merge launch.
+//
+// Inside k_decode (4 warps, 32 tokens per warp per stage):
+//  * Data movement: thread 0 streams every 128-token tile of the packed cache
 //    (sign bits, fp16 norms, 2-bit codes, fp16 zero/scale) HBM -> smem with
-//    cp.async.bulk (TMA bulk copies) into a kStages mbarrier ring, kLookahead
-//    tiles ahead; the 4 warps never issue global loads on the hot path.
-//  * Scores (estimator.py:149-170 identity 2*sum_set(Sq) - sum(Sq)): the query
-//    sketch of every query head is quantized to a 32-bit fixed-point integer and
-//    split into four int8 digits -- the B operand of an m16n8k32 IMMA whose
-//    columns are (query, digit) pairs -- so one IMMA computes 16 tokens x 4 query
-//    heads x 2 digits x 32 sign bits with exact int32 accumulation.  The A operand
-//    is the packed sign word itself, masked in place: `w & (0x01010101 << 2q)`
-//    turns 4 sign bits into 4 u8 lanes of value 2^(2q)*bit (2 LOP3 per 8 bits, no
-//    unpacking); the 2^s weights are folded into the digits.
-//  * PV: out[q][d] = sum_t P'[t][q] c[t][d] + sum_t p[t][q] zero[t][g], with
-//    P' = p * scale split hi/lo in fp16 (22-bit P') as the B operand of an
-//    m16n8k16 HMMA whose A operand is the 2-bit code turned into the NORMAL fp16
-//    1 + c 4^s/1024 by one SHF + one LOP3 (P2 layout puts lane-row g's 16 dims in
-//    code word g); the offset sum_t P' is removed with an exact FFMA accumulator.
-//  * Online softmax in the log2 domain per query head; one partial (m, l, acc)
-//    per (CTA, unit segment); CTAs own equal contiguous ranges of the flattened
-//    (unit, tile) space (stream-K) so every SM gets the same number of tiles.
+//    cp.async.bulk into a kStages mbarrier ring, kLookahead tiles ahead.
+//  * Scores (estimator.py:149-170, 2*sum_set(Sq) - sum(Sq)): m16n8k32 IMMA, A = the
+//    packed sign word masked in place (`w & 0x01010101 << 2q`: four sign bits ->
+//    four u8 lanes of value 2^(2q)*bit), B = the query-sketch digits; one IMMA =
+//    16 tokens x 32 bits x 4 query heads x 2 digits, exact int32 accumulation.
+//  * PV (attention.py:71 over kvcache.py:164-166 dequantization):
+//      out[q][d] = sum_t p[t][q] zero[t][g(d)] + sum_t P'[t][q][g(d)] c[t][d],
+//    P' = p * scale.  The code term is an m16n8k32 IMMA as well: A = one P2 code
+//    word masked in place (`w & 3 << 2s` per byte: 4 tokens x 1 dim, value c*4^s,
+//    the 4^s row weight is divided out at the end), B = P' in 24-bit fixed point
+//    relative to the tile's bound ptop * max(scale), split into three balanced
+//    int8 digits by one FFMA (float magic-number rounding) and PRMTs: lo/mid in
+//    one n-tile, hi in a second.  Exact int32 accumulation per tile, FFMA2 into
+//    the fp32 running sum.  (16-bit P' was measured at 2e-4 relative error on flat
+//    softmaxes: tokens below 2^-16 of the tile bound round to zero.)
+//  * Online softmax in the log2 domain per query head; running state is rescaled
+//    only when some head's maximum moved (warp-uniform branch).
 #include <type_traits>
 
 #include "common.cuh"
@@ -29,13 +39,27 @@
 namespace qjl {
 namespace tc {
 
-constexpr int kNW = 4;             // warps per CTA (all compute; warp 0 lane 0 issues copies)
+constexpr int kNW = 4;             // warps per CTA (all compute; thread 0 also issues copies)
 constexpr int kTile = 32 * kNW;    // tokens per pipeline stage
-constexpr int kStages = 5;
-constexpr int kLookahead = 3;      // tiles in flight ahead of the one being consumed
+#ifndef QJL_DEC_STAGES
+#define QJL_DEC_STAGES 4
+#endif
+#ifndef QJL_DEC_LOOKAHEAD
+#define QJL_DEC_LOOKAHEAD 2
+#endif
+constexpr int kStages = QJL_DEC_STAGES;
+// tiles in flight ahead of the one being consumed; kStages - kLookahead - 1 tiles of
+// slack let the issuing warp run ahead of the slowest warp without blocking
+constexpr int kLookahead = QJL_DEC_LOOKAHEAD;
+#ifndef QJL_DEC_MINB
+#define QJL_DEC_MINB 3
+#endif
 constexpr int kThreads = 32 * kNW;
+constexpr int kRec = 130;          // per (partial, query): m (log2 domain), l, out[128]
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kPMax = 8.0e6f;                  // P' fixed-point full scale (< 2^23 - 32896)
+constexpr float kMagic = 8421504.f;              // 2^23 + 32896 (see the P' digits)
 
 struct Params {
   qjl_key_cache_t kc;
@@ -47,9 +71,10 @@ struct Params {
   int64_t total_tiles;
   int ctas;
   int max_seg;           // partial slots per unit
-  const uint4* afrag;    // [units][KC][32 lanes] (4 x u32 A regs)
+  const uint4* afrag;    // [units][KC][32 lanes] score B fragments (4 x u32)
   const float4* qconst;  // [units][4 queries] {k_in, b_in, k_out, b_out}
-  float* part;           // [units][max_seg][G][2 + 128]
+  float* part;           // [units][max_seg][G][kRec]
+  int* counters;         // [units] finished segments (zeroed by k_prep)
   float* out;            // [units][G][128]
   float* lse;            // [units][G] or null
 };
@@ -94,7 +119,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-// A = masked sign words (u8 lanes 2^s * bit), B = query-sketch digits (s8)
+// D += A(u8) . B(s8), m16n8k32
 __device__ __forceinline__ void imma_u8s8(int* d, const uint4& a, uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -102,13 +127,14 @@ __device__ __forceinline__ void imma_u8s8(int* d, const uint4& a, uint32_t b0, u
       : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
       : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ void hmma(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                     uint32_t b0, uint32_t b1) {
+// D = A(u8) . B(s8), m16n8k32, zero accumulator
+__device__ __forceinline__ void imma_u8s8_z(int* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                            uint32_t b0, uint32_t b1) {
   asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};\n"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%10,%10,%10,%10};\n"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(0));
 }
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -120,31 +146,29 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
   return r;
 }
-__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
-  __half2 h = __floats2half2_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&h);
+// packed fp32 FMA (sm_100 FFMA2): d = a * b + c elementwise
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n.reg .b64 ra, rb, rc, rd;\n"
+      "mov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\nmov.b64 rc, {%6, %7};\n"
+      "fma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
 }
-
-// Code slot p (0..7 within each 16-bit half of x) -> fp16 NORMAL 1 + c*4^s/1024,
-// s = 3 + (p & 1): the half-word is first shifted so slot p lands on mantissa
-// slot s (one SHF per m-tile: slots {0,1} << 6, {2,3} << 2, {4,5} >> 2,
-// {6,7} >> 6; bits spilling across the half boundary are masked off), then one
-// LOP3 masks the code and ORs in the exponent of 1.0.  Normal operands keep the
-// HMMA fp32 sum accurate to ~1e-7; fp16 subnormal operands measured ~2e-4
-// (tools/hmma_precision.cu).  The offset sum_t P' is removed with the exact
-// FFMA accumulator Y = sum_t p * scale (offset/step ratio <= 16).
-template <int PAIR>   // PAIR = p >> 1 = m-tile & 3
-__device__ __forceinline__ uint32_t code_shift(uint32_t x) {
-  if constexpr (PAIR == 0) return x << 6;
-  else if constexpr (PAIR == 1) return x << 2;
-  else if constexpr (PAIR == 2) return x >> 2;
-  else return x >> 6;
+__device__ __forceinline__ float2 h2f2(uint32_t h) {
+  return __half22float2(*reinterpret_cast<const __half2*>(&h));
 }
-template <int S>      // S = 3 or 4
-__device__ __forceinline__ uint32_t code_h2(uint32_t xs) {
-  uint32_t r;
-  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(xs), "r"(0x00030003u << (2 * S)), "r"(0x3C003C00u));
-  return r;   // (xs & mask) | one
+__device__ __forceinline__ uint32_t hmax2u(uint32_t a, uint32_t b) {
+  __half2 r = __hmax2(*reinterpret_cast<const __half2*>(&a), *reinterpret_cast<const __half2*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+template <int K>
+__device__ __forceinline__ uint32_t word_of(const uint4& v) {
+  if constexpr (K == 0) return v.x;
+  else if constexpr (K == 1) return v.y;
+  else if constexpr (K == 2) return v.z;
+  else return v.w;
 }
 
 // --------------------------------------------------------------- smem layout
@@ -163,27 +187,36 @@ struct Layout {
   static constexpr int oZero = oCodes + kCodes;
   static constexpr int oScale = oZero + kConst;
   static constexpr int kStageBytes = oScale + kConst;
-  static constexpr int oPbuf = kStages * kStageBytes;              // per warp 2 KB
-  static constexpr int oRed = oPbuf;                               // flush scratch aliases P'
-  static constexpr int kRec = 2 + 4 + 128;                          // m, l, Z[4], acc[128]
+  static constexpr int kBbufWarp = 1536;                          // P' B fragments: lo/mid 1 KB, hi 512 B
+  static constexpr int oBbuf = kStages * kStageBytes;
+  static constexpr int oBq = oBbuf + kNW * kBbufWarp;              // score B fragments [KC][32 lanes] x 16 B
+  static constexpr int kBq = (KCI + KCO) * 32 * 16;
+  static constexpr int oRed = oBbuf;                               // flush scratch aliases both
   static constexpr int kRedBytes = kNW * 4 * kRec * 4;
-  static constexpr int kScratch = kRedBytes > kNW * 2048 ? kRedBytes : kNW * 2048;
-  static constexpr int oBar = oPbuf + kScratch;
+  static constexpr int kScratch = kRedBytes > kNW * kBbufWarp + kBq ? kRedBytes : kNW * kBbufWarp + kBq;
+  static constexpr int oFlag = oBbuf + kScratch;
+  static constexpr int oBar = oFlag + 16;
   static constexpr int kTotal = oBar + 2 * kStages * 8;
 };
 
 // ----------------------------------------------------------------- prep kernel
-// Per unit: Sq = S_full . q (fp64, rounded to fp32 like the generic path),
-// per-side sigma = max|Sq| / 2^30, weighted integer sketch
-// x_j = rint(Sq_j / (sigma * 2^(j mod 8))), 4 signed-byte digits laid out as the
-// IMMA B operand: column n of n-tile nt = (query n/2, digit 2*nt + n%2).
+// One CTA per unit, one thread per sketch row: Sq = S_full . q (fp32 products of
+// the 16-bit operands, exact; fp64 for wider sketches), per-side sigma =
+// max|Sq| / 2^30, weighted integer sketch x_j = rint(Sq_j / (sigma * 2^(j mod 8))),
+// 4 signed-byte digits laid out as the IMMA B operand: column n of n-tile nt =
+// (query n/2, digit 2*nt + n%2).
+template <typename A, typename T>
+__device__ __forceinline__ A to_acc(T x) {
+  if constexpr (std::is_same<A, float>::value) return to_f32(x);
+  else return to_f64(x);
+}
+
 template <typename TQ, typename TS, int KCI, int KCO>
-__global__ void __launch_bounds__(512) k_prep(const TQ* __restrict__ q, int G, const TS* __restrict__ s_full,
+__global__ void __launch_bounds__(640) k_prep(const TQ* __restrict__ q, int G, const TS* __restrict__ s_full,
                                               int64_t s_unit_stride, float inv_t, uint4* __restrict__ bfrag,
-                                              float4* __restrict__ qconst) {
+                                              float4* __restrict__ qconst, int* __restrict__ counters) {
   constexpr int MI = KCI * 32, MO = KCO * 32, MT = MI + MO, KC = KCI + KCO;
   constexpr int d = 128;
-  // 16-bit sketch operands: products are exact in fp32; wider operands accumulate in fp64
   using acc_t = typename std::conditional<(sizeof(TS) <= 2), float, double>::type;
   __shared__ acc_t qs[4][d];
   __shared__ float sq[4][MT];
@@ -192,51 +225,41 @@ __global__ void __launch_bounds__(512) k_prep(const TQ* __restrict__ q, int G, c
   __shared__ double red[4][2][2];   // [q][side][sigma, sum]
   const int u = blockIdx.x;
   const TS* S = s_full + (int64_t)u * s_unit_stride;
-  // let the decode kernel launch now (programmatic dependent launch): its prologue and
-  // first bulk copies overlap this kernel; it waits (griddepcontrol.wait) before reading
-  // anything written here
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   for (int i = threadIdx.x; i < 4 * d; i += blockDim.x) {
     const int g = i / d;
-    qs[g][i % d] = g < G ? (acc_t)to_f64(q[((int64_t)u * G + g) * d + i % d]) : (acc_t)0;
+    qs[g][i % d] = g < G ? to_acc<acc_t>(q[((int64_t)u * G + g) * d + i % d]) : (acc_t)0;
   }
-  if (threadIdx.x < 8) {
-    mxbits[threadIdx.x >> 1][threadIdx.x & 1] = 0u;
-  }
+  if (threadIdx.x < 8) mxbits[threadIdx.x >> 1][threadIdx.x & 1] = 0u;
+  if (threadIdx.x == 0) counters[u] = 0;
   __syncthreads();
-  // one warp per sketch row (coalesced 256-byte row reads), lane l owns columns
-  // 4l..4l+3 of every query head; shuffle-reduce the four partial dots
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  acc_t qreg[4][4];
-#pragma unroll
-  for (int g = 0; g < 4; ++g)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) qreg[g][e] = qs[g][4 * lane + e];
-  float wmax[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-  for (int r = wid; r < MT; r += nwarp) {
-    const TS* row = S + (int64_t)r * d + 4 * lane;
+  {
+    const int r = threadIdx.x;               // blockDim.x == MT
+    const TS* row = S + (int64_t)r * d;
+    constexpr int EPV = 16 / (int)sizeof(TS);
     acc_t a[4] = {0, 0, 0, 0};
+#pragma unroll 4
+    for (int e0 = 0; e0 < d; e0 += EPV) {
+      const uint4 raw = __ldg(reinterpret_cast<const uint4*>(row + e0));
+      const TS* sv = reinterpret_cast<const TS*>(&raw);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const acc_t sv = (acc_t)to_f64(row[e]);
+      for (int k = 0; k < EPV; ++k) {
+        const acc_t s = to_acc<acc_t>(sv[k]);
 #pragma unroll
-      for (int g = 0; g < 4; ++g) a[g] = fma(sv, qreg[g][e], a[g]);
+        for (int g = 0; g < 4; ++g) a[g] = fma(s, qs[g][e0 + k], a[g]);
+      }
     }
+    float wm[4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) a[g] += __shfl_xor_sync(0xffffffffu, a[g], o);
+      sq[g][r] = (float)a[g];
+      wm[g] = warp_max(fabsf((float)a[g]));   // rows of a warp are on one side (MI % 32 == 0)
     }
-    const int side = r >= MI;
-    if (lane < 4) sq[lane][r] = (float)a[lane];
+    if (lane == 0) {
+      const int side = r >= MI;
 #pragma unroll
-    for (int g = 0; g < 4; ++g) wmax[g][side] = fmaxf(wmax[g][side], fabsf((float)a[g]));
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int g = 0; g < 4; ++g)
-#pragma unroll
-      for (int sd = 0; sd < 2; ++sd) atomicMax(&mxbits[g][sd], __float_as_uint(wmax[g][sd]));
+      for (int g = 0; g < 4; ++g) atomicMax(&mxbits[g][side], __float_as_uint(wm[g]));
+    }
   }
   __syncthreads();
   if (threadIdx.x < 8) {
@@ -267,8 +290,8 @@ __global__ void __launch_bounds__(512) k_prep(const TQ* __restrict__ q, int G, c
   // bit 8i + 2q, k = 16 + 4q + i holds bit 8i + 2q + 1 (the A side masks the
   // sign word with 0x01010101 << 2q / 0x02020202 << 2q).
   for (int i = threadIdx.x; i < KC * 32; i += blockDim.x) {
-    const int c = i / 32, lane = i % 32;
-    const int n = lane >> 2, ql = lane & 3;
+    const int c = i / 32, ln = i % 32;
+    const int n = ln >> 2, ql = ln & 3;
     const int qd = n >> 1;
     uint32_t regs[4];
 #pragma unroll
@@ -293,7 +316,7 @@ __global__ void __launch_bounds__(512) k_prep(const TQ* __restrict__ q, int G, c
       }
       regs[r] = v;
     }
-    bfrag[((int64_t)u * KC + c) * 32 + lane] = make_uint4(regs[0], regs[1], regs[2], regs[3]);
+    bfrag[((int64_t)u * KC + c) * 32 + ln] = make_uint4(regs[0], regs[1], regs[2], regs[3]);
   }
   if (threadIdx.x < 4) {
     const int g = threadIdx.x;
@@ -313,19 +336,16 @@ __global__ void __launch_bounds__(512) k_prep(const TQ* __restrict__ q, int G, c
 }
 
 // ----------------------------------------------------------------- main kernel
-// 4 warps per CTA, each owning 32 tokens of every 128-token stage; thread 0 also
-// issues the bulk copies kLookahead tiles ahead (no dedicated producer warp, so
-// three CTAs -- 12 warps -- fit per SM).
-//
-// Token order inside a warp's 32-token tile: score m-tile h covers tokens 16h..16h+15
-// with IMMA rows g / g+8 = tokens 16h+g / 16h+g+8, and the PV k-step h uses the
-// permuted k order k = 2j + e  <->  token 16h + j + 8e, so the fp16 pair (k, k+1)
-// of a B fragment is exactly the token pair a score lane owns (no exchange).
+// Token order inside a warp's 32-token slice: score m-tile h covers tokens
+// 16h..16h+15 (IMMA rows), so lane g (= lane >> 2) scores tokens g + 8i, i = 0..3,
+// for query head q = lane & 3.  The PV IMMA takes k = 4j + i <-> token j + 8i, so
+// the four P' digits a score lane produces for one query form exactly one B
+// register (k-block j = g) -- only a 1 KB per-warp smem transpose to the B
+// fragment lanes is needed, no shuffles.
 template <int KCI, int KCO>
-__global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 3) k_decode_tc(const Params P) {
+__global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : QJL_DEC_MINB) k_decode_tc(const Params P) {
   using L = Layout<KCI, KCO>;
   constexpr int KC = KCI + KCO;
-  constexpr int R = L::kRec;
   extern __shared__ __align__(128) uint8_t sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::oBar);
   uint64_t* empty = full + kStages;
@@ -371,141 +391,196 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 3) k_decode_t
   if (threadIdx.x == 0)
     for (int i = 0; i < kLookahead && i < ntiles; ++i) issue_next();
 
-  const int g = lane >> 2, q = lane & 3;      // q = this lane's query head
+  const int g = lane >> 2, q = lane & 3;      // q = this lane's query head (scores)
   const uint32_t M0 = 0x01010101u << (2 * q), M1 = 0x02020202u << (2 * q);
-  uint32_t* pbuf = reinterpret_cast<uint32_t*>(sm + L::oPbuf + warp * 2048);
+  uint32_t* bbuf = reinterpret_cast<uint32_t*>(sm + L::oBbuf + warp * L::kBbufWarp);
+  uint32_t* hbuf = bbuf + 256;
   float* red = reinterpret_cast<float*>(sm + L::oRed);
+  // P' B-fragment transpose (16-byte chunks of bbuf, bank-conflict free both ways):
+  // source lane (g, q) holds k-block j = g of columns n = 2q (lo digit) / 2q + 1 (hi);
+  // it belongs to B-fragment lane (n, g & 3), register b = g >> 2.
+  const int wlo = (2 * q + (g >> 2)) * 8 + (((g & 3) + 2 * q) & 7);
+  const int whi = (2 * q + (g >> 2)) * 8 + ((4 + (g & 3) + 2 * q) & 7);
+  const int rb0 = ((lane >> 3) * 2) * 8 + ((lane + 2 * (lane >> 3)) & 7);
+  // hi digits: only the even columns n = 2q of the second n-tile are used; chunk of
+  // (query qq, k-lane qp, register b) = (2b + (qp >> 1)) * 8 + ((2qq + qp) & 7)
+  const int whh = (2 * (g >> 2) + ((g & 3) >> 1)) * 8 + ((2 * q + (g & 3)) & 7);
+  const int rh0 = (((lane & 3) >> 1)) * 8 + ((2 * (lane >> 3) + (lane & 3)) & 7);
+  const bool hcol = ((lane >> 2) & 1) == 0;
+  // P2 code words of this lane: k-blocks q and 4 + q of fragment row g
+  const int cw0 = g * 8 + (q ^ ((g & 1) << 2));
+  const int cw1 = g * 8 + ((4 + q) ^ ((g & 1) << 2));
 
-  uint4 Bq[KC];                               // query-sketch digits (IMMA B operand)
+  const uint4* bqs = reinterpret_cast<const uint4*>(sm + L::oBq) + lane;   // [c][32 lanes]
   float4 qc = make_float4(0.f, 0.f, 0.f, 0.f);
   float m_run = -INFINITY, l_run = 0.f;
-  float Z[4] = {0.f, 0.f, 0.f, 0.f};          // sum_t p * zero_g   (query q)
-  float Y[4] = {0.f, 0.f, 0.f, 0.f};          // sum_t p * scale_g  (HMMA offset removal)
-  float acc[8][4];                            // PV: rows = dims, cols (2q, 2q+1) = query q hi/lo
-#pragma unroll
-  for (int mt = 0; mt < 8; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+  float2 Z01 = make_float2(0.f, 0.f), Z23 = make_float2(0.f, 0.f);   // sum_t p * zero_g
+  float2 acc[8];                              // [MT] rows g / g + 8 of the PV m-tile, query q
 
   auto load_unit = [&](int u) {
-#pragma unroll
-    for (int c = 0; c < KC; ++c) Bq[c] = P.afrag[((int64_t)u * KC + c) * 32 + lane];
+    // the unit's query-sketch digits (score IMMA B operand) -> smem; every warp is past
+    // the previous unit (flush ends with a CTA barrier)
+    for (int i = threadIdx.x; i < KC * 32; i += kThreads)
+      reinterpret_cast<uint4*>(sm + L::oBq)[i] = P.afrag[(int64_t)u * KC * 32 + i];
+    asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
     qc = P.qconst[(int64_t)u * 4 + q];
     m_run = -INFINITY;
     l_run = 0.f;
+    Z01 = Z23 = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) Z[i] = Y[i] = 0.f;
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+    for (int mt = 0; mt < 8; ++mt) acc[mt] = make_float2(0.f, 0.f);
   };
 
   auto flush = [&](int u) {
-    // the P' buffers are reused as scratch: every warp must be done with its tile
-    asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
-    // l, Z, Y: reduce over the 8 lanes of query q (lanes q + 4g)
+    // l and Z: reduce over the 8 lanes of query q (lanes q + 4g)
     float l = l_run;
-    float z[4] = {Z[0], Z[1], Z[2], Z[3]};
-    float y[4] = {Y[0], Y[1], Y[2], Y[3]};
+    float z[4] = {Z01.x, Z01.y, Z23.x, Z23.y};
 #pragma unroll
     for (int o = 4; o <= 16; o <<= 1) {
       l += __shfl_xor_sync(0xffffffffu, l, o);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        z[i] += __shfl_xor_sync(0xffffffffu, z[i], o);
-        y[i] += __shfl_xor_sync(0xffffffffu, y[i], o);
-      }
+      for (int i = 0; i < 4; ++i) z[i] += __shfl_xor_sync(0xffffffffu, z[i], o);
     }
-    float* rw = red + warp * 4 * R;
+    // the record scratch aliases the P' transpose buffers: every warp must be done
+    asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+    float* rw = red + (warp * 4 + q) * kRec;
     if (g == 0) {
-      rw[q * R + 0] = m_run;
-      rw[q * R + 1] = l;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) rw[q * R + 2 + i] = z[i];
+      rw[0] = m_run;
+      rw[1] = l;
     }
-    // HMMA rows hold sum_t P' (1 + c 4^s / 1024), s = 3 (row g) or 4 (row g+8)
+    // PV row (MT, r) = dim 16 MT + g + 8 r carries weight 4^(2 (MT & 1) + r)
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
-      const float yg = y[mt >> 1];
-      rw[q * R + 6 + 16 * mt + g] = (acc[mt][0] + acc[mt][1] - yg) * 16.f;
-      rw[q * R + 6 + 16 * mt + g + 8] = (acc[mt][2] + acc[mt][3] - yg) * 4.f;
+      const float w0 = (mt & 1) ? (1.f / 16.f) : 1.f;
+      rw[2 + 16 * mt + g] = fmaf(acc[mt].x, w0, z[mt >> 1]);
+      rw[2 + 16 * mt + g + 8] = fmaf(acc[mt].y, w0 * 0.25f, z[mt >> 1]);
     }
     asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
     const int c0 = cta_of_tile((int64_t)u * P.tpu, T, C);
-    const int slot = blockIdx.x - c0;
-    for (int i = threadIdx.x; i < P.G * 130; i += kThreads) {
-      const int qq = i / 130, e = i % 130;
+    const int c1 = cta_of_tile((int64_t)u * P.tpu + P.tpu - 1, T, C);
+    const int ns = c1 - c0 + 1, slot = blockIdx.x - c0;
+    float* mypart = P.part + ((int64_t)u * P.max_seg + slot) * P.G * kRec;
+    for (int i = threadIdx.x; i < P.G * kRec; i += kThreads) {
+      const int qq = i / kRec, e = i % kRec;
       float M = -INFINITY;
 #pragma unroll
-      for (int w = 0; w < kNW; ++w) M = fmaxf(M, red[w * 4 * R + qq * R]);
-      float v = 0.f;
+      for (int w = 0; w < kNW; ++w) M = fmaxf(M, red[(w * 4 + qq) * kRec]);
+      float v = M;
+      if (e) {
+        v = 0.f;
 #pragma unroll
-      for (int w = 0; w < kNW; ++w) {
-        const float* r = red + w * 4 * R + qq * R;
-        const float f = (r[0] == -INFINITY) ? 0.f : ex2(r[0] - M);
-        if (e == 1) v += f * r[1];
-        else if (e >= 2) v += f * (r[6 + (e - 2)] + r[2 + ((e - 2) >> 5)]);
+        for (int w = 0; w < kNW; ++w) {
+          const float* r = red + (w * 4 + qq) * kRec;
+          const float f = (r[0] == -INFINITY) ? 0.f : ex2(r[0] - M);
+          v = fmaf(f, r[e], v);
+        }
       }
-      float* dst = P.part + (((int64_t)u * P.max_seg + slot) * P.G + qq) * 130;
-      dst[e] = (e == 0) ? (M == -INFINITY ? -INFINITY : M * kLn2) : v;
+      mypart[i] = v;
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+    int* flag = reinterpret_cast<int*>(sm + L::oFlag);
+    if (ns > 1) {
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+      if (threadIdx.x == 0) *flag = (atomicAdd(&P.counters[u], 1) == ns - 1);
+      asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+      if (!*flag) return;
+      __threadfence();
+    } else {
+      asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+    }
+    // this CTA finished the unit last: merge its ns partials
+    const float* up = P.part + (int64_t)u * P.max_seg * P.G * kRec;
+    for (int i = threadIdx.x; i < P.G * 128; i += kThreads) {
+      const int qq = i >> 7, dim = i & 127;
+      float M = -INFINITY;
+      for (int s = 0; s < ns; ++s) M = fmaxf(M, __ldcg(up + (s * P.G + qq) * kRec));
+      float Ls = 0.f, a = 0.f;
+      for (int s = 0; s < ns; ++s) {
+        const float* W = up + (s * P.G + qq) * kRec;
+        const float ms = __ldcg(W);
+        if (ms == -INFINITY) continue;
+        const float f = ex2(ms - M);
+        Ls = fmaf(f, __ldcg(W + 1), Ls);
+        a = fmaf(f, __ldcg(W + 2 + dim), a);
+      }
+      P.out[((int64_t)u * P.G + qq) * 128 + dim] = a / Ls;
+      if (P.lse && dim == 0) P.lse[(int64_t)u * P.G + qq] = (M + __log2f(Ls)) * kLn2;
+    }
   };
 
-  // one 32-token warp tile; MASK: some tokens are >= n (tail tile of a unit)
+  // one 32-token warp slice; MASK: some tokens are >= n (tail tile of a unit)
   auto tile = [&](const uint8_t* st, const int64_t tok0, auto mask_tag) {
     constexpr bool MASK = decltype(mask_tag)::value;
     const uint32_t* bin = reinterpret_cast<const uint32_t*>(st + L::oBitsIn) + warp * 32 * KCI;
     const uint32_t* bout = reinterpret_cast<const uint32_t*>(st + L::oBitsOut) + warp * 32 * KCO;
     const __half* nin = reinterpret_cast<const __half*>(st + L::oNormIn) + warp * 32;
     const __half* nout = reinterpret_cast<const __half*>(st + L::oNormOut) + warp * 32;
-    const uint32_t* codes = reinterpret_cast<const uint32_t*>(st + L::oCodes) + warp * 32 * 8;
+    const uint4* codes = reinterpret_cast<const uint4*>(st + L::oCodes + warp * 1024);
     const uint2* zer = reinterpret_cast<const uint2*>(st + L::oZero) + warp * 32;
     const uint2* scl = reinterpret_cast<const uint2*>(st + L::oScale) + warp * 32;
 
     // -------- scores: 2 IMMA m-tiles of 16 tokens (rows g, g+8) x 2 n-tiles -------
     // D[token][2q + i] of n-tile nt = digit 2nt+i of query q: every lane ends up
-    // with all four digits of its own query for tokens g and g+8 -- no shuffles.
-    float lg[4];                       // token 16h + g + 8e  ->  lg[2h + e]
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int ta = 16 * h + g, tb = ta + 8;
-      int din[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
-      int dout[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+    // with all four digits of its own query for tokens g + 8i -- no shuffles.
+    float lg[4];                       // token g + 8i
+    {
+      // both m-tiles at once: four independent accumulator chains per n-tile pair
+      int din[2][2][4] = {}, dout[2][2][4] = {};      // [m-tile h][n-tile][reg]
 #pragma unroll
       for (int c = 0; c < KCI; c += 4) {
-        const uint4 va = *reinterpret_cast<const uint4*>(bin + ta * KCI + c);
-        const uint4 vb = *reinterpret_cast<const uint4*>(bin + tb * KCI + c);
-        const uint32_t wa[4] = {va.x, va.y, va.z, va.w}, wb[4] = {vb.x, vb.y, vb.z, vb.w};
+        uint4 v[4];                                   // tokens g + 8k
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const uint4*>(bin + (g + 8 * k) * KCI + c);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const uint4 a = make_uint4(wa[e] & M0, wb[e] & M0, wa[e] & M1, wb[e] & M1);
-          imma_u8s8(din[0], a, Bq[c + e].x, Bq[c + e].y);
-          imma_u8s8(din[1], a, Bq[c + e].z, Bq[c + e].w);
+          const uint4 bq = bqs[(c + e) * 32];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t wa = e == 0 ? v[2 * h].x : e == 1 ? v[2 * h].y : e == 2 ? v[2 * h].z : v[2 * h].w;
+            const uint32_t wb = e == 0 ? v[2 * h + 1].x : e == 1 ? v[2 * h + 1].y
+                              : e == 2 ? v[2 * h + 1].z : v[2 * h + 1].w;
+            const uint4 a = make_uint4(wa & M0, wb & M0, wa & M1, wb & M1);
+            imma_u8s8(din[h][0], a, bq.x, bq.y);
+            imma_u8s8(din[h][1], a, bq.z, bq.w);
+          }
         }
       }
 #pragma unroll
       for (int c = 0; c < KCO; c += 2) {
-        const uint2 va = *reinterpret_cast<const uint2*>(bout + ta * KCO + c);
-        const uint2 vb = *reinterpret_cast<const uint2*>(bout + tb * KCO + c);
-        const uint32_t wa[2] = {va.x, va.y}, wb[2] = {vb.x, vb.y};
+        uint2 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const uint2*>(bout + (g + 8 * k) * KCO + c);
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const uint4 a = make_uint4(wa[e] & M0, wb[e] & M0, wa[e] & M1, wb[e] & M1);
-          imma_u8s8(dout[0], a, Bq[KCI + c + e].x, Bq[KCI + c + e].y);
-          imma_u8s8(dout[1], a, Bq[KCI + c + e].z, Bq[KCI + c + e].w);
+          const uint4 bq = bqs[(KCI + c + e) * 32];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t wa = e == 0 ? v[2 * h].x : v[2 * h].y;
+            const uint32_t wb = e == 0 ? v[2 * h + 1].x : v[2 * h + 1].y;
+            const uint4 a = make_uint4(wa & M0, wb & M0, wa & M1, wb & M1);
+            imma_u8s8(dout[h][0], a, bq.x, bq.y);
+            imma_u8s8(dout[h][1], a, bq.z, bq.w);
+          }
         }
       }
+      // D[token][2q + i] of n-tile nt = digit 2nt+i of query q: rows g (regs 0, 1) and
+      // g + 8 (regs 2, 3) of m-tile h = tokens g + 16h and g + 16h + 8
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {      // e = 0: token ta (c0, c1); e = 1: token tb (c2, c3)
-        const int tk = e ? tb : ta;
-        // |digit partial| <= 2^21, so d0 + 256 d1 and d2 + 256 d3 are exact in int32
-        const float din_f = fmaf((float)(din[1][2 * e] + 256 * din[1][2 * e + 1]), 65536.f,
-                                 (float)(din[0][2 * e] + 256 * din[0][2 * e + 1]));
-        float l2 = __half2float(nin[tk]) * fmaf(qc.x, din_f, -qc.y);
-        if (KCO) {
-          const float dout_f = fmaf((float)(dout[1][2 * e] + 256 * dout[1][2 * e + 1]), 65536.f,
-                                    (float)(dout[0][2 * e] + 256 * dout[0][2 * e + 1]));
-          l2 = fmaf(__half2float(nout[tk]), fmaf(qc.z, dout_f, -qc.w), l2);
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int tk = g + 16 * h + 8 * e;
+          // |digit partial| <= 2^21, so d0 + 256 d1 and d2 + 256 d3 are exact in int32
+          const float din_f = fmaf((float)(din[h][1][2 * e] + 256 * din[h][1][2 * e + 1]), 65536.f,
+                                   (float)(din[h][0][2 * e] + 256 * din[h][0][2 * e + 1]));
+          float l2 = __half2float(nin[tk]) * fmaf(qc.x, din_f, -qc.y);
+          if (KCO) {
+            const float dout_f = fmaf((float)(dout[h][1][2 * e] + 256 * dout[h][1][2 * e + 1]), 65536.f,
+                                      (float)(dout[h][0][2 * e] + 256 * dout[h][0][2 * e + 1]));
+            l2 = fmaf(__half2float(nout[tk]), fmaf(qc.z, dout_f, -qc.w), l2);
+          }
+          lg[2 * h + e] = (!MASK || tok0 + tk < P.n) ? l2 : -INFINITY;
         }
-        lg[2 * h + e] = (!MASK || tok0 + tk < P.n) ? l2 : -INFINITY;
       }
     }
 
@@ -515,101 +590,118 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 3) k_decode_t
     tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
     tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
     const float m_new = fmaxf(m_run, tmax);
-    const bool none = MASK && (m_new == -INFINITY);
-    const float alpha = none ? 1.f : ex2(m_run - m_new);
+    // nothing valid yet in this unit (every query head sees the same valid tokens,
+    // so this is warp-uniform)
+    if (MASK && m_new == -INFINITY) return;
+    const float alpha = ex2(m_run - m_new);
     m_run = m_new;
     float p[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) p[i] = none ? 0.f : ex2(lg[i] - m_new);
-    l_run = fmaf(l_run, alpha, (p[0] + p[1]) + (p[2] + p[3]));
+    for (int i = 0; i < 4; ++i) p[i] = ex2(lg[i] - m_new);
+    const float ptop = ex2(tmax - m_new);     // largest p of the tile for this query
+
+    // value constants of this lane's tokens g + 8i (fp16 x 4 groups)
+    uint2 zr[4], sr[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      Z[i] *= alpha;
-      Y[i] *= alpha;
+      zr[i] = zer[g + 8 * i];
+      sr[i] = scl[g + 8 * i];
+      if (MASK && tok0 + g + 8 * i >= P.n) zr[i] = sr[i] = make_uint2(0u, 0u);  // rows past n
     }
+    // tile bound of the value scales (query independent): fp16x2 max tree + 3 shuffles
+    uint32_t hm = hmax2u(hmax2u(hmax2u(sr[0].x, sr[0].y), hmax2u(sr[1].x, sr[1].y)),
+                         hmax2u(hmax2u(sr[2].x, sr[2].y), hmax2u(sr[3].x, sr[3].y)));
+    hm = hmax2u(hm, __shfl_xor_sync(0xffffffffu, hm, 4));
+    hm = hmax2u(hm, __shfl_xor_sync(0xffffffffu, hm, 8));
+    hm = hmax2u(hm, __shfl_xor_sync(0xffffffffu, hm, 16));
+    const float2 hmf = h2f2(hm);
+    const float bound = ptop * fmaxf(hmf.x, hmf.y);      // >= every P' of query q in the tile
+    const float K = bound > 0.f ? __fdividef(kPMax, bound) : 0.f;
+    const float invK = bound * (1.f / kPMax);
 
-    // -------- P' = p * scale_g, split hi/lo fp16, written as HMMA B fragments --------
-    // B layout per warp: [k-step h][column 2q + lo][quad q'][b][group] half2 over the
-    // k pair (2q' + 8b, +1) = tokens (16h + q' + 4b, +8): this lane's own pair
-    // (tokens 16h + g, 16h + g + 8) is q' = g & 3, b = g >> 2.
+    // rescale the running state only when some head's maximum moved
+    if (__any_sync(0xffffffffu, alpha != 1.f)) {
+      const float2 a2 = make_float2(alpha, alpha), z2 = make_float2(0.f, 0.f);
+      l_run *= alpha;
+      Z01 = fma2(Z01, a2, z2);
+      Z23 = fma2(Z23, a2, z2);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float hv[2][4], lv[2][4];
+      for (int mt = 0; mt < 8; ++mt) acc[mt] = fma2(acc[mt], a2, z2);
+    }
+    l_run += (p[0] + p[1]) + (p[2] + p[3]);
+
+    // -------- P' = p * scale in 24-bit fixed point -> three int8 digits per token --------
+    // fma(p K, scale, 2^23 + 32896) leaves u = v + 32896 (v = rint(P' K) in [0, 8e6]) in
+    // the 23 mantissa bits: v = 65536 hi + 256 mid + lo with balanced lo, mid in
+    // [-128, 127]; byte 0 ^ 0x80 = lo, byte 1 ^ 0x80 = mid, byte 2 = hi.
+    uint32_t wlo4[4], wmid4[4], whi4[4];
+    {
+      uint32_t wv[4][4];                  // [token i][group]
+      const float2 mg = make_float2(kMagic, kMagic);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int tk = 16 * h + g + 8 * e;
-        const float pj = p[2 * h + e];
-        uint2 zr = zer[tk], sr = scl[tk];
-        if (MASK && tok0 + tk >= P.n) zr = sr = make_uint2(0u, 0u);   // garbage rows past n
-        const float2 z01 = __half22float2(*reinterpret_cast<const __half2*>(&zr.x));
-        const float2 z23 = __half22float2(*reinterpret_cast<const __half2*>(&zr.y));
-        const float2 s01 = __half22float2(*reinterpret_cast<const __half2*>(&sr.x));
-        const float2 s23 = __half22float2(*reinterpret_cast<const __half2*>(&sr.y));
-        const float zz[4] = {z01.x, z01.y, z23.x, z23.y};
-        const float ss[4] = {s01.x, s01.y, s23.x, s23.y};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float Pp = pj * ss[i];
-          Z[i] = fmaf(pj, zz[i], Z[i]);
-          Y[i] += Pp;
-          hv[e][i] = __uint_as_float(__float_as_uint(Pp) & 0xFFFFE000u);   // 11 significant bits
-          lv[e][i] = Pp - hv[e][i];
-        }
+      for (int i = 0; i < 4; ++i) {
+        const float pk = p[i] * K;
+        const float2 pk2 = make_float2(pk, pk), pp = make_float2(p[i], p[i]);
+        const float2 s01 = h2f2(sr[i].x), s23 = h2f2(sr[i].y);
+        const float2 z01 = h2f2(zr[i].x), z23 = h2f2(zr[i].y);
+        const float2 w01 = fma2(pk2, s01, mg), w23 = fma2(pk2, s23, mg);
+        wv[i][0] = __float_as_uint(w01.x);
+        wv[i][1] = __float_as_uint(w01.y);
+        wv[i][2] = __float_as_uint(w23.x);
+        wv[i][3] = __float_as_uint(w23.y);
+        Z01 = fma2(pp, z01, Z01);
+        Z23 = fma2(pp, z23, Z23);
       }
-      uint32_t* dst = pbuf + (((h * 8 + 2 * q) * 4 + (g & 3)) * 2 + (g >> 2)) * 4;
-      *reinterpret_cast<uint4*>(dst) = make_uint4(pack_h2(hv[0][0], hv[1][0]), pack_h2(hv[0][1], hv[1][1]),
-                                                  pack_h2(hv[0][2], hv[1][2]), pack_h2(hv[0][3], hv[1][3]));
-      *reinterpret_cast<uint4*>(dst + 32) = make_uint4(pack_h2(lv[0][0], lv[1][0]), pack_h2(lv[0][1], lv[1][1]),
-                                                       pack_h2(lv[0][2], lv[1][2]), pack_h2(lv[0][3], lv[1][3]));
-    }
-    __syncwarp();
-
-    // -------------------- PV: 8 m-tiles x 2 k-steps of 16 tokens ---------------
-    // a0/a1: k pair (2q, 2q+1) = tokens (16h + q, 16h + q + 8); a2/a3: (16h + q + 4, + 12)
-    uint32_t xa[2], xb[2], ya[2], yb[2];
-    uint32_t bg[4][2][2];   // [group][ks][b]
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      const int tb = 16 * ks + q;
-      const uint32_t w0 = codes[(tb + 0) * 8 + g], w1 = codes[(tb + 8) * 8 + g];
-      const uint32_t w4 = codes[(tb + 4) * 8 + g], w5 = codes[(tb + 12) * 8 + g];
-      xa[ks] = prmt(w0, w1, 0x5410); xb[ks] = prmt(w0, w1, 0x7632);
-      ya[ks] = prmt(w4, w5, 0x5410); yb[ks] = prmt(w4, w5, 0x7632);
-      const uint4 B0 = *reinterpret_cast<const uint4*>(pbuf + ((ks * 8 + g) * 4 + q) * 8);
-      const uint4 B1 = *reinterpret_cast<const uint4*>(pbuf + ((ks * 8 + g) * 4 + q) * 8 + 4);
-      bg[0][ks][0] = B0.x; bg[1][ks][0] = B0.y; bg[2][ks][0] = B0.z; bg[3][ks][0] = B0.w;
-      bg[0][ks][1] = B1.x; bg[1][ks][1] = B1.y; bg[2][ks][1] = B1.z; bg[3][ks][1] = B1.w;
+      for (int G = 0; G < 4; ++G) {
+        const uint32_t p01 = prmt(wv[0][G], wv[1][G], 0x5140);
+        const uint32_t p23 = prmt(wv[2][G], wv[3][G], 0x5140);
+        const uint32_t h01 = prmt(wv[0][G], wv[1][G], 0x0062);
+        const uint32_t h23 = prmt(wv[2][G], wv[3][G], 0x0062);
+        wlo4[G] = prmt(p01, p23, 0x5410) ^ 0x80808080u;
+        wmid4[G] = prmt(p01, p23, 0x7632) ^ 0x80808080u;
+        whi4[G] = prmt(h01, h23, 0x5410);
+      }
     }
-    // m-tile MT: rows g / g+8 use code slots 2*(MT&3) / +1 of half-words X and Y;
-    // one shift brings both to mantissa slots 3 / 4.
-    // The tile's product is formed from zero and folded into the running sum with an
-    // IEEE FFMA that also applies the online-softmax rescale (alpha is lane-local:
-    // the accumulator columns of this lane belong to query q).  Accumulating straight
-    // into the running sum drifts: the tensor core's fp32 adder truncates small
-    // addends against a large accumulator (1.8e-4 at 32k tokens, growing with n).
-#define QJL_MT(MT, X, Yw)                                                                        \
-  {                                                                                              \
-    float td[4] = {0.f, 0.f, 0.f, 0.f};                                                          \
-    _Pragma("unroll") for (int ks = 0; ks < 2; ++ks) {                                           \
-      const uint32_t xs = code_shift<(MT) & 3>(X[ks]), ys = code_shift<(MT) & 3>(Yw[ks]);        \
-      hmma(td, code_h2<3>(xs), code_h2<4>(xs), code_h2<3>(ys), code_h2<4>(ys),                   \
-           bg[(MT) >> 1][ks][0], bg[(MT) >> 1][ks][1]);                                          \
-    }                                                                                            \
-    _Pragma("unroll") for (int i = 0; i < 4; ++i) acc[MT][i] = fmaf(acc[MT][i], alpha, td[i]);  \
-  }
-    QJL_MT(0, xa, ya)
-    QJL_MT(1, xa, ya)
-    QJL_MT(2, xa, ya)
-    QJL_MT(3, xa, ya)
-    QJL_MT(4, xb, yb)
-    QJL_MT(5, xb, yb)
-    QJL_MT(6, xb, yb)
-    QJL_MT(7, xb, yb)
-#undef QJL_MT
+    reinterpret_cast<uint4*>(bbuf)[wlo] = make_uint4(wlo4[0], wlo4[1], wlo4[2], wlo4[3]);
+    reinterpret_cast<uint4*>(bbuf)[whi] = make_uint4(wmid4[0], wmid4[1], wmid4[2], wmid4[3]);
+    reinterpret_cast<uint4*>(hbuf)[whh] = make_uint4(whi4[0], whi4[1], whi4[2], whi4[3]);
+    __syncwarp();
+    const uint4 B0 = reinterpret_cast<const uint4*>(bbuf)[rb0];       // k 4q' .. : groups 0..3
+    const uint4 B1 = reinterpret_cast<const uint4*>(bbuf)[rb0 + 8];   // k 16 + 4q' ..
+    const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+    const uint4 H0 = hcol ? reinterpret_cast<const uint4*>(hbuf)[rh0] : z4;
+    const uint4 H1 = hcol ? reinterpret_cast<const uint4*>(hbuf)[rh0 + 16] : z4;
+    const uint4 W0 = codes[cw0], W1 = codes[cw1];
+
+    // -------------------- PV: 8 m-tiles (16 dims) x K = 32 tokens ---------------
+    const float2 ik = make_float2(invK, invK), k65536 = make_float2(65536.f, 65536.f);
+#define QJL_PV(MT)                                                                            \
+    {                                                                                         \
+      constexpr uint32_t mk0 = 0x03030303u << (4 * ((MT) & 1));                               \
+      constexpr uint32_t mk1 = mk0 << 2;                                                      \
+      const uint32_t x0 = word_of<((MT) >> 1)>(W0), x1 = word_of<((MT) >> 1)>(W1);                \
+      int dd[4], dh[4];                                                                       \
+      imma_u8s8_z(dd, x0 & mk0, x0 & mk1, x1 & mk0, x1 & mk1, word_of<((MT) >> 1)>(B0),        \
+                  word_of<((MT) >> 1)>(B1));                                                  \
+      imma_u8s8_z(dh, x0 & mk0, x0 & mk1, x1 & mk0, x1 & mk1, word_of<((MT) >> 1)>(H0),        \
+                  word_of<((MT) >> 1)>(H1));                                                  \
+      const float2 v = fma2(make_float2((float)dh[0], (float)dh[2]), k65536,                  \
+                            make_float2((float)(dd[0] + 256 * dd[1]), (float)(dd[2] + 256 * dd[3]))); \
+      acc[MT] = fma2(v, ik, acc[MT]);                                                         \
+    }
+    QJL_PV(0)
+    QJL_PV(1)
+    QJL_PV(2)
+    QJL_PV(3)
+    QJL_PV(4)
+    QJL_PV(5)
+    QJL_PV(6)
+    QJL_PV(7)
+#undef QJL_PV
     __syncwarp();
   };
 
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // merge kernel may launch
   // everything above only touched the cache stream; the query sketch digits come from
   // k_prep, launched just before us with programmatic dependent launch
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -634,34 +726,10 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 3) k_decode_t
   if (cur_u >= 0) flush(cur_u);
 }
 
-
-// Merge per (unit, query): combine the unit's CTA-segment partials.
-__global__ void k_merge_tc(const float* __restrict__ part, int max_seg, int G, int tpu, int64_t T, int C,
-                           float* __restrict__ out, float* __restrict__ lse) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: partials of the decode grid
-  const int ug = blockIdx.x;
-  const int u = ug / G, qq = ug % G;
-  const int c0 = cta_of_tile((int64_t)u * tpu, T, C);
-  const int c1 = cta_of_tile((int64_t)u * tpu + tpu - 1, T, C);
-  const int ns = c1 - c0 + 1;
-  float M = -INFINITY;
-  for (int s = 0; s < ns; ++s) M = fmaxf(M, part[(((int64_t)u * max_seg + s) * G + qq) * 130]);
-  float L = 0.f, a = 0.f;
-  for (int s = 0; s < ns; ++s) {
-    const float* W = part + (((int64_t)u * max_seg + s) * G + qq) * 130;
-    if (W[0] == -INFINITY) continue;
-    const float f = expf(W[0] - M);
-    L += f * W[1];
-    if (threadIdx.x < 128) a += f * W[2 + threadIdx.x];
-  }
-  if (threadIdx.x < 128) out[(int64_t)ug * 128 + threadIdx.x] = a / L;
-  if (lse && threadIdx.x == 0) lse[ug] = M + logf(L);
-}
-
 struct Plan {
   int tpu, ctas, max_seg;
   int64_t T;
-  size_t afrag_off, qconst_off, part_off, total;
+  size_t afrag_off, qconst_off, part_off, cnt_off, total;
 };
 
 template <int KCI, int KCO>
@@ -696,6 +764,8 @@ static int occupancy_by_id(int id) {
   return 1;
 }
 
+static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
 static Plan make_plan(const qjl_key_cache_t& kc, int64_t n, int G, int id) {
   Plan p;
   p.tpu = (int)((n + kTile - 1) / kTile);
@@ -711,9 +781,10 @@ static Plan make_plan(const qjl_key_cache_t& kc, int64_t n, int G, int id) {
   p.max_seg = ms;
   const int KC = (kc.m_in + kc.m_out) / 32;
   p.afrag_off = 0;
-  p.qconst_off = ((size_t)kc.units * KC * 32 * 16 + 255) / 256 * 256;
-  p.part_off = p.qconst_off + ((size_t)kc.units * 4 * 16 + 255) / 256 * 256;
-  p.total = p.part_off + (size_t)kc.units * p.max_seg * G * 130 * 4;
+  p.qconst_off = align256((size_t)kc.units * KC * 32 * 16);
+  p.part_off = p.qconst_off + align256((size_t)kc.units * 4 * 16);
+  p.cnt_off = p.part_off + align256((size_t)kc.units * p.max_seg * G * kRec * 4);
+  p.total = p.cnt_off + align256((size_t)kc.units * 4);
   return p;
 }
 
@@ -742,9 +813,11 @@ static int launch_tc_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc
   uint4* afrag = (uint4*)(w + plan.afrag_off);
   float4* qconst = (float4*)(w + plan.qconst_off);
   float* part = (float*)(w + plan.part_off);
+  int* counters = (int*)(w + plan.cnt_off);
+  constexpr int MT = (KCI + KCO) * 32;
 #define QJL_PREP(TQ, TS)                                                                         \
-  k_prep<TQ, TS, KCI, KCO><<<kc.units, 512, 0, st>>>((const TQ*)q, G, (const TS*)sk.s_full,      \
-                                                     sk.unit_stride, inv_t, afrag, qconst)
+  k_prep<TQ, TS, KCI, KCO><<<kc.units, MT, 0, st>>>((const TQ*)q, G, (const TS*)sk.s_full,       \
+                                                    sk.unit_stride, inv_t, afrag, qconst, counters)
 #define QJL_PREP_S(TQ)                                                   \
   switch (sk.dtype) {                                                    \
     case QJL_BF16: QJL_PREP(TQ, __nv_bfloat16); break;                   \
@@ -774,6 +847,7 @@ static int launch_tc_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc
   P.afrag = afrag;
   P.qconst = qconst;
   P.part = part;
+  P.counters = counters;
   P.out = out;
   P.lse = lse;
   occupancy<KCI, KCO>();
@@ -792,16 +866,6 @@ static int launch_tc_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc
   timing_end(st);
   if (e != cudaSuccess) return cuda_status(e, "decode_tc");
   QJL_LAUNCH_CHECK("decode_tc");
-  cudaLaunchConfig_t mcfg = {};
-  mcfg.gridDim = dim3(kc.units * G);
-  mcfg.blockDim = dim3(128);
-  mcfg.stream = st;
-  mcfg.attrs = attr;
-  mcfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&mcfg, k_merge_tc, (const float*)part, plan.max_seg, G, plan.tpu, plan.T, plan.ctas,
-                         out, lse);
-  if (e != cudaSuccess) return cuda_status(e, "decode_tc_merge");
-  QJL_LAUNCH_CHECK("decode_tc_merge");
   return QJL_OK;
 }
 

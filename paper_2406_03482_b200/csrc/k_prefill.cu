@@ -310,12 +310,10 @@ __global__ void __launch_bounds__(256) k_quantize_values(const T* __restrict__ v
   const int64_t t = (int64_t)blockIdx.x * 8 + warp;
   const int d = vc.d, G = d / vc.group, gs = vc.group;
   const int levels = (1 << vc.bits) - 1;
-  __shared__ uint32_t words[8][8];
-  if (lane < 8) words[warp][lane] = 0u;
-  __syncwarp();
   const bool valid = t < n;
   const T* V = v + (int64_t)u * unit_stride + (valid ? t : 0) * d;
   const int64_t row = (int64_t)u * vc.capacity + row_offset + t;
+  const bool p2 = vc.layout == QJL_VLAYOUT_P2;
   for (int g = 0; g < G; ++g) {
     // group g spans dims [g*gs, (g+1)*gs); lanes stride over it
     double mn = INFINITY, mx = -INFINITY;
@@ -340,18 +338,24 @@ __global__ void __launch_bounds__(256) k_quantize_values(const T* __restrict__ v
         q = fmin(fmax(q, 0.0), (double)levels);
         code = (int)q;
       }
-      if (valid) {
-        if (vc.layout == QJL_VLAYOUT_U8) {
-          reinterpret_cast<uint8_t*>(vc.codes)[row * d + dim] = (uint8_t)code;
-        } else {
-          int w, p;
-          p2_slot(dim, &w, &p);
-          atomicOr(&words[warp][w], (uint32_t)code << (2 * p));
+      if (!p2) {
+        if (valid) reinterpret_cast<uint8_t*>(vc.codes)[row * d + dim] = (uint8_t)code;
+      } else {
+        // P2 (d = 128, group 32, 2 bits): dim 32g + lane sits in byte (row g & 7 =
+        // lane & 7, k = g) at slot lane >> 3; OR the four slots of a byte together
+        uint32_t b = (uint32_t)code << (2 * (lane >> 3));
+        b |= __shfl_xor_sync(0xffffffffu, b, 8);
+        b |= __shfl_xor_sync(0xffffffffu, b, 16);
+        if (valid && lane < 8) {
+          int64_t byte;
+          int sh;
+          p2_pos(row, dim, &byte, &sh);
+          reinterpret_cast<uint8_t*>(vc.codes)[byte] = (uint8_t)b;
         }
       }
     }
     if (valid && lane == 0) {
-      if (vc.layout == QJL_VLAYOUT_U8) {
+      if (!p2) {
         reinterpret_cast<float*>(vc.zero)[row * G + g] = (float)zero;
         reinterpret_cast<float*>(vc.scale)[row * G + g] = (float)scale;
       } else {
@@ -360,9 +364,6 @@ __global__ void __launch_bounds__(256) k_quantize_values(const T* __restrict__ v
       }
     }
   }
-  __syncwarp();
-  if (valid && vc.layout == QJL_VLAYOUT_P2 && lane < 8)
-    reinterpret_cast<uint32_t*>(vc.codes)[row * 8 + lane] = words[warp][lane];
 }
 
 int launch_quantize_values(const void* v, int dtype, int64_t n, int64_t unit_stride,

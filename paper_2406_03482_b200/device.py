@@ -334,23 +334,50 @@ class DeviceKeyCache:
         return r
 
 
-def p2_unpack_codes(packed: np.ndarray) -> np.ndarray:
-    """Host decoder of the P2 fragment-order code layout -> codes [..., 128] (tests)."""
-    words = np.ascontiguousarray(packed).view("<u4")  # [..., 8]
-    out = np.zeros(words.shape[:-1] + (128,), np.uint8)
-    for dim in range(128):
-        mt, r = dim >> 4, dim & 15
-        w, p = r & 7, 2 * mt + (r >> 3)
-        out[..., dim] = (words[..., w] >> np.uint32(2 * p)) & 3
-    return out
+def _p2_tables():
+    """Byte offset (within a 4 KB tile) and bit shift of every (token, dim) of a
+    128-token P2 tile -- the host mirror of `p2_pos` in csrc/common.cuh."""
+    t = np.arange(128)[:, None]
+    d = np.arange(128)[None, :]
+    sl, j, i = (t >> 5) & 3, t & 7, (t >> 3) & 3
+    mt, g, r = d >> 4, d & 7, (d >> 3) & 1
+    k, s = mt >> 1, 2 * (mt & 1) + r
+    word = sl * 256 + (g * 8 + (j ^ ((g & 1) << 2))) * 4 + k
+    byte = word * 4 + i
+    return (np.broadcast_to(byte, (128, 128)).astype(np.int64),
+            np.broadcast_to(2 * s, (128, 128)).astype(np.uint8))
+
+
+_P2_BYTE, _P2_SHIFT = _p2_tables()
+
+
+def p2_unpack_codes(packed: np.ndarray, n: int | None = None) -> np.ndarray:
+    """Host decoder of the P2 tile-interleaved code layout: packed u8 [..., cap, 32]
+    (cap a multiple of 128, rows counted from the unit's row 0) -> codes [..., n, 128]."""
+    packed = np.ascontiguousarray(packed, dtype=np.uint8)
+    cap = packed.shape[-2]
+    if cap % 128:
+        raise ValueError("P2 code arrays hold whole 128-token tiles")
+    tiles = packed.reshape(packed.shape[:-2] + (cap // 128, 4096))
+    codes = (tiles[..., _P2_BYTE] >> _P2_SHIFT) & 3
+    codes = codes.reshape(packed.shape[:-2] + (cap, 128)).astype(np.uint8)
+    return codes if n is None else codes[..., :n, :]
 
 
 def p2_pack_codes(codes: np.ndarray) -> np.ndarray:
-    """Inverse of p2_unpack_codes: codes [..., 128] -> packed u8 [..., 32]."""
-    codes = np.asarray(codes, np.uint32)
-    words = np.zeros(codes.shape[:-1] + (8,), np.uint32)
-    for dim in range(128):
-        mt, r = dim >> 4, dim & 15
-        w, p = r & 7, 2 * mt + (r >> 3)
-        words[..., w] |= (codes[..., dim] & 3) << np.uint32(2 * p)
-    return words.astype("<u4").view(np.uint8)
+    """Inverse of p2_unpack_codes: codes [..., n, 128] -> packed u8 [..., cap, 32],
+    cap = n rounded up to whole 128-token tiles (padding codes are 0)."""
+    codes = np.asarray(codes, np.uint8)
+    n = codes.shape[-2]
+    cap = (n + 127) // 128 * 128
+    full = np.zeros(codes.shape[:-2] + (cap, 128), np.uint8)
+    full[..., :n, :] = codes & 3
+    tiles = full.reshape(codes.shape[:-2] + (cap // 128, 128 * 128))
+    out = np.zeros(codes.shape[:-2] + (cap // 128, 4096), np.uint8)
+    flat_byte = _P2_BYTE.reshape(-1)
+    flat_shift = _P2_SHIFT.reshape(-1)
+    order = np.argsort(flat_byte, kind="stable")          # 4 (token, dim) per byte
+    contrib = (tiles[..., order].astype(np.uint32) << flat_shift[order]).reshape(
+        codes.shape[:-2] + (cap // 128, 4096, 4)).sum(-1)
+    out[...] = contrib.astype(np.uint8)
+    return out.reshape(codes.shape[:-2] + (cap, 32))

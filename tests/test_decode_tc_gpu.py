@@ -83,7 +83,7 @@ def test_tc_full_config3_against_oracle(cuda):
                      norm_in=c.norm_in[u, :n].double().cpu().numpy(),
                      bits_out=c.bits_out[u, :n].cpu().numpy(),
                      norm_out=c.norm_out[u, :n].double().cpu().numpy())
-        codes = p2_unpack_codes(c.v_codes[u, :n].cpu().numpy())
+        codes = p2_unpack_codes(c.v_codes[u].cpu().numpy(), n)
         deq = O.dequantize_values(codes, c.v_zero[u, :n].double().cpu().numpy(),
                                   c.v_scale[u, :n].double().cpu().numpy())
         for g in range(G):

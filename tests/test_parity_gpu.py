@@ -112,7 +112,7 @@ def test_decode_parity(cuda, cfg):
                                                const_dtype="f16" if layout == "p2" else None)
         if layout == "p2":
             from paper_2406_03482_b200.device import p2_unpack_codes
-            dc = p2_unpack_codes(cache.v_codes[u, :n].cpu().numpy())
+            dc = p2_unpack_codes(cache.v_codes[u].cpu().numpy(), n)
             assert np.array_equal(dc, codes)
             assert np.array_equal(cache.v_zero[u, :n].double().cpu().numpy(), zero)
             assert np.array_equal(cache.v_scale[u, :n].double().cpu().numpy(), scale)

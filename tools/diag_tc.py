@@ -14,7 +14,7 @@ for u in (2, 5):
     chans = tuple(int(x) for x in c.channels[u, :8].cpu().numpy())
     cache = dict(bits_in=c.bits_in[u, :n].cpu().numpy(), norm_in=c.norm_in[u, :n].double().cpu().numpy(),
                  bits_out=c.bits_out[u, :n].cpu().numpy(), norm_out=c.norm_out[u, :n].double().cpu().numpy())
-    codes = p2_unpack_codes(c.v_codes[u, :n].cpu().numpy())
+    codes = p2_unpack_codes(c.v_codes[u].cpu().numpy(), n)
     z = c.v_zero[u, :n].double().cpu().numpy(); s = c.v_scale[u, :n].double().cpu().numpy()
     deq = O.dequantize_values(codes, z, s)
     for g in range(G):

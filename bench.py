@@ -128,7 +128,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- GPU setup
-def build_cache(w, rank, seed, device):
+def build_cache(w, rank, seed, device, layout="p2t"):
     """Seeded synthetic C3-style cache for this rank's units, quantized on device by K1."""
     import torch
 
@@ -140,7 +140,7 @@ def build_cache(w, rank, seed, device):
     g = torch.Generator(device=device)
     g.manual_seed(derive_seed(seed, 1000 + rank) & ((1 << 63) - 1))
     cache = DeviceKeyCache.create(U, d, w["m_in"], h=h, m_out=w["m_out"], capacity=n, seed=seed,
-                                  key_dtype=tdt)
+                                  key_dtype=tdt, value_layout=layout)
     chunk = max(1, min(U, (1 << 30) // (n * d * 4)))    # bound the transient raw K/V
     prompt_done = False
     for u0 in range(0, U, chunk):
@@ -229,7 +229,7 @@ def host_unit(cache, u):
     if cache.bits_out is not None:
         r["bits_out"] = cache.bits_out[u, :n].cpu().numpy()
         r["norm_out"] = cache.norm_out[u, :n].double().cpu().numpy()
-    r["codes"] = p2_unpack_codes(cache.v_codes[u].cpu().numpy(), n)
+    r["codes"] = p2_unpack_codes(cache.v_codes[u].cpu().numpy(), n, cache.value_layout)
     r["zero"] = cache.v_zero[u, :n].double().cpu().numpy()
     r["scale"] = cache.v_scale[u, :n].double().cpu().numpy()
     r["channels"] = tuple(int(c) for c in cache.channels[u, : cache.shape.h].cpu().numpy())
@@ -343,7 +343,7 @@ def run_gpu(args):
     lib = _lib.load()
     w = dict(WORKLOADS[args.workload])
     U = w["batch"] * w["kv_heads"]
-    cache = build_cache(w, rank, args.seed, device)
+    cache = build_cache(w, rank, args.seed, device, args.layout)
     tdt = {"bf16": torch.bfloat16, "f16": torch.float16}[w["dtype"]]
     g = torch.Generator(device=device)
     g.manual_seed(args.seed + 17 * rank + 3)
@@ -564,6 +564,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--layout", default="p2t", choices=["p2t", "p2"],
+                    help="value-code layout: p2t = tcgen05 decode, p2 = mma.sync decode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
     args = ap.parse_args()

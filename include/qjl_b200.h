@@ -35,6 +35,9 @@
  *   value cache layout P2 (fast path): 2-bit codes, group 32, fp16 zero/scale
  *               codes u8  [units][capacity][d/4]  in MMA fragment order
  *               zero  f16 [units][capacity][d/32], scale f16 [units][capacity][d/32]
+ *   value cache layout P2T (tcgen05 path): 2-bit codes, group 32, fp16 zero/scale; inside each
+ *               128-token tile byte (d/4)*128 + (t%128)/4*4 + t%4 holds dims 4(d/4)..+3 of
+ *               token t at bits 2(d%4)..+1 -- one u32 = 4 tokens x 4 dims
  *   value cache layout U8 (reference-format path): 1 byte per code, any bits 1..8,
  *               any group dividing d, fp32 zero/scale per (token, group).
  *   sketch      s_full [units or 1][m_in+m_out][d]: rows 0..m_in-1 hold S_in at the
@@ -69,7 +72,7 @@ enum {
 };
 
 enum { QJL_F32 = 0, QJL_F16 = 1, QJL_BF16 = 2, QJL_F64 = 3 };
-enum { QJL_VLAYOUT_U8 = 0, QJL_VLAYOUT_P2 = 1 };
+enum { QJL_VLAYOUT_U8 = 0, QJL_VLAYOUT_P2 = 1, QJL_VLAYOUT_P2T = 2 };
 
 typedef struct qjl_key_cache {
   uint8_t* bits_in;

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("QJL_LIB") or os.path.join(_HERE, "libqjl_b200.so")
 QJL_OK, QJL_ERR_ARG, QJL_ERR_UNSUPPORTED, QJL_ERR_CUDA, QJL_ERR_WORKSPACE, QJL_ERR_EMPTY = (
     0, -1, -2, -3, -4, -5)
 QJL_F32, QJL_F16, QJL_BF16, QJL_F64 = 0, 1, 2, 3
-QJL_VLAYOUT_U8, QJL_VLAYOUT_P2 = 0, 1
+QJL_VLAYOUT_U8, QJL_VLAYOUT_P2, QJL_VLAYOUT_P2T = 0, 1, 2
 
 c_i32, c_i64, c_sz, c_vp, c_dbl, c_flt = (ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t,
                                           ctypes.c_void_p, ctypes.c_double, ctypes.c_float)

@@ -96,9 +96,9 @@ static int check_value_cache(const qjl_value_cache_t* vc, int d, int units) {
   QJL_CHECK_ARG(vc->units == units, "value units %d != key units %d", vc->units, units);
   QJL_CHECK_ARG(vc->bits >= 1 && vc->bits <= 8, "value bit width must be in [1, 8], got %d", vc->bits);
   QJL_CHECK_ARG(vc->group >= 1 && d % vc->group == 0, "value group %d must divide d=%d", vc->group, d);
-  if (vc->layout == QJL_VLAYOUT_P2) {
+  if (vc->layout == QJL_VLAYOUT_P2 || vc->layout == QJL_VLAYOUT_P2T) {
     if (!(d == 128 && vc->bits == 2 && vc->group == 32)) {
-      set_error("P2 value layout is 2-bit, group 32, d = 128 (got d=%d bits=%d group=%d)", d, vc->bits, vc->group);
+      set_error("P2/P2T value layouts are 2-bit, group 32, d = 128 (got d=%d bits=%d group=%d)", d, vc->bits, vc->group);
       return QJL_ERR_UNSUPPORTED;
     }
   } else {
@@ -309,6 +309,10 @@ size_t qjl_decode_workspace(const qjl_key_cache_t* cache, const qjl_value_cache_
   if (!cache || !values || n <= 0 || G <= 0) return 0;
   const int m_total = cache->m_in + cache->m_out;
   size_t a = decode_simt_workspace(cache->units, n, G, values->d, m_total);
+  if (decode_umma_supported(*cache, *values, G)) {
+    size_t b = decode_umma_workspace(*cache, *values, n, G);
+    return a > b ? a : b;
+  }
   if (decode_tc_supported(*cache, *values, G)) {
     size_t b = decode_tc_workspace(*cache, *values, n, G);
     return a > b ? a : b;
@@ -337,6 +341,9 @@ int qjl_decode(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, in
     return QJL_ERR_WORKSPACE;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  if (decode_umma_supported(*cache, *values, G))
+    return launch_decode_umma(*cache, *values, n, q, q_dtype, G, *sketch, inv_temperature, out, lse,
+                              workspace, workspace_bytes, st);
   if (decode_tc_supported(*cache, *values, G))
     return launch_decode_tc(*cache, *values, n, q, q_dtype, G, *sketch, inv_temperature, out, lse,
                             workspace, workspace_bytes, st);

@@ -121,4 +121,13 @@ __host__ __device__ __forceinline__ void p2_pos(int64_t t, int d, int64_t* byte,
   *shift = 2 * s;
 }
 
+// P2T value-code layout (tcgen05 decode): one u32 word = 4 consecutive tokens (bytes)
+// x 4 dims (2-bit slots), so one mask per word yields the u8 A-operand column of a
+// TMEM-resident PV operand (row = dim, weight 4^(d % 4) folded out per row):
+//   byte = tile * 4096 + (d >> 2) * 128 + ((t & 127) >> 2) * 4 + (t & 3), shift = 2 * (d & 3)
+__host__ __device__ __forceinline__ void p2t_pos(int64_t t, int d, int64_t* byte, int* shift) {
+  *byte = (t >> 7) * 4096 + (int64_t)(d >> 2) * 128 + ((t & 127) >> 2) * 4 + (t & 3);
+  *shift = 2 * (d & 3);
+}
+
 }  // namespace qjl

@@ -39,7 +39,8 @@ __device__ __forceinline__ float load_value(const qjl_value_cache_t& vc, int64_t
   // row = unit * capacity + t; capacity % 128 == 0, so tiles never straddle units
   int64_t byte;
   int sh;
-  p2_pos(row, dim, &byte, &sh);
+  if (vc.layout == QJL_VLAYOUT_P2T) p2t_pos(row, dim, &byte, &sh);
+  else p2_pos(row, dim, &byte, &sh);
   const float c = (float)((reinterpret_cast<const uint8_t*>(vc.codes)[byte] >> sh) & 3u);
   const float z = f16_bits_to_f32(reinterpret_cast<const uint16_t*>(vc.zero)[row * G + grp]);
   const float s = f16_bits_to_f32(reinterpret_cast<const uint16_t*>(vc.scale)[row * G + grp]);

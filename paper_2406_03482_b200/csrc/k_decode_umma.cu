@@ -1,0 +1,1004 @@
+// tcgen05 (5th-gen tensor core) fused QJL decode -- K2 score estimator + K3 online
+// softmax . V -- for P2T value caches on sm_100a.
+//
+// One decode step = 2 launches chained with programmatic dependent launch:
+//   k_uprep   one CTA per unit: Sq = S_full . q for the unit's G <= 4 query heads,
+//             quantized to a 32-bit fixed-point integer, split into four int8 digits and
+//             written as the score MMA's B operand (K-major, SWIZZLE_128B image);
+//             zeroes the unit's merge counter.
+//   k_udecode stream-K over the flattened (unit, 128-token tile) space, 4 warps per CTA,
+//             4 CTAs per SM (128 TMEM columns each).  The CTA that finishes a unit last
+//             (atomic counter) merges the unit's partials.
+//
+// Per 128-token tile (all 128 threads; thread t owns token t for scoring and dim t for
+// the value aggregation):
+//  1. thread = token: the packed sign words (estimator.py:110-124 layout) are expanded in
+//     place into the u8 A operand of the score MMA -- `w & 0x01010101 << s` puts sign bits
+//     8i + s of word w into four byte lanes of value 2^s * bit -- and stored to TMEM
+//     (tcgen05.st); the 2^s weights are folded into the B digits.
+//  2. one thread issues tcgen05.mma kind::i8 (A from TMEM, B = query-sketch digits from
+//     smem), M = 128 tokens, N = 16 (4 heads x 4 digits) per side: exact int32
+//     2 * sum_set(Sq) (estimator.py:149-170) for every token and head.
+//  3. thread = token: tcgen05.ld of its 32 accumulators -> logits of the 4 heads
+//     (kvcache.py:311-329), CTA tile maximum (redux.sync + smem), online softmax in the
+//     log2 domain (kvcache.py:38-44 / attention.py:56-71).
+//  4. thread = token: P' = p * scale of its 4 heads x 4 value groups in 24-bit fixed
+//     point relative to the tile bound, split into three int8 digits by one FFMA (float
+//     magic-number rounding) + PRMTs -> the PV MMA's B operand (MN-major smem, one 16-byte
+//     store per digit); zero-point term sum p * zero on the CUDA cores.
+//     thread = dim: its P2T code words masked in place (`w & 3 << 2(d % 4)`: 4 tokens of
+//     one dim, value c * 4^(d % 4)) -> A operand of the PV MMA in TMEM.
+//  5. one thread issues tcgen05.mma kind::i8: D[dim][(digit, group, head)] over the 128
+//     tokens (N = 48).
+//  6. thread = dim: tcgen05.ld of its group's 12 accumulators -> fp32 running output.
+#include <cstdio>
+#include <type_traits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace qjl {
+namespace ud {
+
+#ifndef QJL_UD_SPLIT
+#define QJL_UD_SPLIT 0      // 1: split-phase mbarriers between the warps, 0: CTA barriers
+#endif
+constexpr int kThreads = 128;      // 4 warps; thread t: token t (scores) and dim t (PV)
+constexpr int kTile = 128;         // tokens per tile
+constexpr int kStages = 3;
+constexpr int kLookahead = 2;
+constexpr int kRec = 130;          // per (partial, query): m (log2 domain), l, out[128]
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kPMax = 8.0e6f;                  // P' fixed-point full scale (< 2^23 - 32896)
+constexpr float kMagic = 8421504.f;              // 2^23 + 32896
+
+struct Params {
+  qjl_key_cache_t kc;
+  qjl_value_cache_t vc;
+  int64_t n;
+  int G;
+  int units;
+  int tpu;               // tiles per unit
+  int64_t total_tiles;
+  int ctas;
+  int max_seg;
+  const uint8_t* bsc;    // [units][NH][2048] score B operand images (SW128, K-major)
+  const float4* qconst;  // [units][4 queries] {k_in, b_in, k_out, b_out}
+  float* part;           // [units][max_seg][G][kRec]
+  int* counters;         // [units]
+  float* out;            // [units][G][128]
+  float* lse;            // [units][G] or null
+};
+
+__host__ __device__ __forceinline__ int64_t tile_begin(int c, int64_t T, int C) { return (int64_t)c * T / C; }
+__host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int C) {
+  return (int)(((t + 1) * (int64_t)C + T - 1) / T) - 1;
+}
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bar_sync1() { asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+// same, with a compile-time accumulate flag (no predicate computation per MMA)
+template <int ACC>
+__device__ __forceinline__ void tc_mma_i8c(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "n"(ACC));
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}" : "=r"(pred));
+  return pred != 0;
+}
+// instruction descriptor: D s32, A u8 (K-major, from TMEM), B s8, M = 128
+__host__ __device__ constexpr uint32_t idesc_i8(int n, int b_mn_major) {
+  return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
+}
+// K-major SWIZZLE_128B descriptor (rows of 128 B, 8-row atoms 1024 B apart)
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// SWIZZLE_NONE descriptor (MN-major: LBO = K-block stride, SBO = 16-byte MN-chunk stride)
+__device__ __forceinline__ uint64_t desc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float warp_max_f32(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n.reg .b64 ra, rb, rc, rd;\n"
+      "mov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\nmov.b64 rc, {%6, %7};\n"
+      "fma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 h2f2(uint32_t h) { return __half22float2(*reinterpret_cast<const __half2*>(&h)); }
+__device__ __forceinline__ uint32_t hmax2u(uint32_t a, uint32_t b) {
+  __half2 r = __hmax2(*reinterpret_cast<const __half2*>(&a), *reinterpret_cast<const __half2*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
+// --------------------------------------------------------------- smem layout
+template <int KCI, int KCO>
+struct Layout {
+  static constexpr int KC = KCI + KCO;
+  static constexpr int NHI = KCI / 4, NHO = (KCO + 3) / 4, NH = NHI + NHO;   // 128-byte K halves of B
+  static constexpr int kBitsIn = kTile * KCI * 4;
+  static constexpr int kBitsOut = kTile * KCO * 4;
+  static constexpr int kNorm = kTile * 2;
+  static constexpr int kCodes = kTile * 32;
+  static constexpr int kConst = kTile * 8;
+  static constexpr int oBitsIn = 0;
+  static constexpr int oBitsOut = oBitsIn + kBitsIn;
+  static constexpr int oNormIn = oBitsOut + kBitsOut;
+  static constexpr int oNormOut = oNormIn + kNorm;
+  static constexpr int oCodes = oNormOut + (KCO ? kNorm : 0);
+  static constexpr int oZero = oCodes + kCodes;
+  static constexpr int oScale = oZero + kConst;
+  static constexpr int kStageBytes = oScale + kConst;
+  static constexpr int oBsc = 0;                        // 1024-aligned
+  static constexpr int oBpv = oBsc + NH * 2048;         // [4 heads][128 tokens][16 B] (MN-major chunks)
+  static constexpr int oRed = oBsc;                     // flush scratch aliases Bsc/Bpv
+  static constexpr int oStage = oBpv + 4 * 2048;
+  static constexpr int oMax = oStage + kStages * kStageBytes;   // [4 warps][8] tile maxima
+  static constexpr int oBar = oMax + 4 * 8 * 4;
+  static constexpr int kBars = 2 * kStages + 5;
+  static constexpr int oTmem = oBar + kBars * 8;
+  static constexpr int oFlag = oTmem + 4;
+  static constexpr int kTotal = oFlag + 12 + 1024;      // + alignment slack
+  // TMEM columns: A_sc [0, 8 KC); after the score MMA: A_pv [0, 32), D_pv [32, 96);
+  // D_sc (in: 16, out: 16) after both
+  static constexpr int cDsc = (8 * KC > 96) ? 8 * KC : 96;
+  static constexpr int kCols = cDsc + (KCO ? 32 : 16);
+  static constexpr int kAlloc = kCols <= 128 ? 128 : 256;
+};
+
+// ----------------------------------------------------------------- prep kernel
+template <typename A, typename T>
+__device__ __forceinline__ A to_acc(T x) {
+  if constexpr (std::is_same<A, float>::value) return to_f32(x);
+  else return to_f64(x);
+}
+
+// One CTA per unit, one thread per sketch row: Sq = S_full . q (fp32 products of the
+// 16-bit operands, exact; fp64 for wider sketches), per-side sigma = max|Sq| / 2^30,
+// weighted integer sketch x_j = rint(Sq_j / (sigma * 2^(j mod 8))), four signed-byte
+// digits.  B image: row n = 4 q + digit, K byte k of a side <-> chunk c = k / 32 and,
+// within it, (s, i) = ((k % 32) / 4, k % 4) <-> sign bit j = 32 c + 8 i + s (the A side
+// masks word c with 0x01010101 << s).
+template <typename TQ, typename TS, int KCI, int KCO>
+__global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, const TS* __restrict__ s_full,
+                                               int64_t s_unit_stride, float inv_t, uint8_t* __restrict__ bsc,
+                                               float4* __restrict__ qconst, int* __restrict__ counters) {
+  using L = Layout<KCI, KCO>;
+  constexpr int MI = KCI * 32, MO = KCO * 32, MT = MI + MO;
+  constexpr int d = 128;
+  using acc_t = typename std::conditional<(sizeof(TS) <= 2), float, double>::type;
+  __shared__ acc_t qs[4][d];
+  __shared__ float sq[4][MT];
+  __shared__ int32_t si[4][MT];
+  __shared__ unsigned int mxbits[4][2];
+  __shared__ double red[4][2][2];   // [q][side][sigma, sum]
+  const int u = blockIdx.x;
+  const TS* S = s_full + (int64_t)u * s_unit_stride;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < 4 * d; i += blockDim.x) {
+    const int g = i / d;
+    qs[g][i % d] = g < G ? to_acc<acc_t>(q[((int64_t)u * G + g) * d + i % d]) : (acc_t)0;
+  }
+  if (threadIdx.x < 8) mxbits[threadIdx.x >> 1][threadIdx.x & 1] = 0u;
+  if (threadIdx.x == 0) counters[u] = 0;
+  __syncthreads();
+  {
+    const int r = threadIdx.x;               // blockDim.x == MT
+    const TS* row = S + (int64_t)r * d;
+    constexpr int EPV = 16 / (int)sizeof(TS);
+    acc_t a[4] = {0, 0, 0, 0};
+#pragma unroll 4
+    for (int e0 = 0; e0 < d; e0 += EPV) {
+      const uint4 raw = __ldg(reinterpret_cast<const uint4*>(row + e0));
+      const TS* sv = reinterpret_cast<const TS*>(&raw);
+#pragma unroll
+      for (int k = 0; k < EPV; ++k) {
+        const acc_t s = to_acc<acc_t>(sv[k]);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) a[g] = fma(s, qs[g][e0 + k], a[g]);
+      }
+    }
+    float wm[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      sq[g][r] = (float)a[g];
+      wm[g] = warp_max(fabsf((float)a[g]));   // rows of a warp are on one side (MI % 32 == 0)
+    }
+    if (lane == 0) {
+      const int side = r >= MI;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) atomicMax(&mxbits[g][side], __float_as_uint(wm[g]));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    const int g = threadIdx.x >> 1, side = threadIdx.x & 1;
+    const double mx = (double)__uint_as_float(mxbits[g][side]);
+    red[g][side][0] = mx > 0.0 ? mx / 1073741824.0 : 1.0;   // sigma = max/2^30
+  }
+  __syncthreads();
+  for (int seg = wid; seg < 8; seg += nwarp) {
+    const int g = seg >> 1, side = seg & 1;
+    const int lo = side ? MI : 0, hi = side ? MT : MI;
+    const double inv = 1.0 / red[g][side][0];
+    long long acc = 0;
+    for (int j = lo + lane; j < hi; j += 32) {
+      const int sh = (j - lo) & 7;
+      const int32_t x = (int32_t)rint((double)sq[g][j] * inv / (double)(1 << sh));
+      si[g][j] = x;
+      acc += (long long)x * (1ll << sh);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[g][side][1] = (double)acc * red[g][side][0];
+  }
+  __syncthreads();
+  // B image bytes, 4 per thread iteration (one u32 of a swizzled 16-byte chunk)
+  uint8_t* out = bsc + (size_t)u * L::NH * 2048;
+  for (int w = threadIdx.x; w < L::NH * 512; w += blockDim.x) {
+    const int h = w / 512, rem = (w % 512) * 4;      // byte offset inside the half image
+    const int n = (rem / 1024) * 8 + (rem % 1024) / 128;
+    const int pchunk = (rem % 128) / 16, b0 = rem % 16;
+    const int kk0 = ((pchunk ^ (n % 8)) * 16) + b0;  // logical K byte inside the half
+    const int qd = n >> 2, digit = n & 3;
+    const bool side = h >= L::NHI;
+    const int kside = (side ? h - L::NHI : h) * 128;
+    const int ksize = side ? MO : MI;
+    uint32_t v = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k = kside + kk0 + e;
+      int8_t dg = 0;
+      if (k < ksize) {
+        const int c = k / 32, s = (k % 32) / 4, i = k % 4;
+        int32_t x = si[qd][(side ? MI : 0) + 32 * c + 8 * i + s];
+#pragma unroll
+        for (int t = 0; t <= 3; ++t) {
+          const int8_t lo8 = (int8_t)(x & 0xFF);
+          if (t == digit) dg = lo8;
+          x = (x - (int32_t)lo8) >> 8;
+        }
+      }
+      v |= (uint32_t)(uint8_t)dg << (8 * e);
+    }
+    reinterpret_cast<uint32_t*>(out + h * 2048)[w % 512] = v;
+  }
+  if (threadIdx.x < 4) {
+    const int g = threadIdx.x;
+    const float ci = MI ? kEstimatorScale / (float)MI * inv_t * kLog2e : 0.f;
+    const float co = MO ? kEstimatorScale / (float)MO * inv_t * kLog2e : 0.f;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (g < G) {
+      v.x = (float)(2.0 * red[g][0][0] * ci);
+      v.y = (float)(red[g][0][1] * ci);
+      if (KCO) {
+        v.z = (float)(2.0 * red[g][1][0] * co);
+        v.w = (float)(red[g][1][1] * co);
+      }
+    }
+    qconst[(int64_t)u * 4 + g] = v;
+  }
+}
+
+// ----------------------------------------------------------------- main kernel
+template <int KCI, int KCO>
+__global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(const Params P) {
+  using L = Layout<KCI, KCO>;
+  constexpr int KC = KCI + KCO;
+  extern __shared__ uint8_t sm_raw[];
+  // align to 1024 B (SWIZZLE_128B atoms) by pointer arithmetic on the shared array, so the
+  // compiler keeps shared-window loads (LDS) instead of generic ones
+  uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::oBar);
+  uint64_t* empty = full + kStages;
+  uint64_t* sc_bar = full + 2 * kStages;    // score MMA done (tcgen05.commit)
+  uint64_t* pv_bar = sc_bar + 1;            // PV MMA done (tcgen05.commit)
+  uint64_t* a_rdy = sc_bar + 2;             // 4 warps: score A operand in TMEM
+  uint64_t* mx_rdy = sc_bar + 3;            // 4 warps: tile maxima in smem
+  uint64_t* p_rdy = sc_bar + 4;             // 4 warps: PV operands (B smem, A TMEM) ready
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::oTmem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int C = P.ctas;
+  const int64_t T = P.total_tiles;
+  const int64_t r0 = tile_begin(blockIdx.x, T, C), r1 = tile_begin(blockIdx.x + 1, T, C);
+  const int ntiles = (int)(r1 - r0);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+    mbar_init(sc_bar, 1);
+    mbar_init(pv_bar, 1);
+    mbar_init(a_rdy, 4);
+    mbar_init(mx_rdy, 4);
+    mbar_init(p_rdy, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(L::kAlloc));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const uint64_t dsc0 = desc_sw128(smem_u32(sm + L::oBsc));
+  const uint64_t dpv0 = desc_none(smem_u32(sm + L::oBpv), 128, 2048);
+  const uint32_t tlane = tbase + ((uint32_t)(warp * 32) << 16);   // this warp's TMEM lanes
+
+  const int u_first = (int)(r0 / P.tpu);
+  const int lt_first = (int)(r0 - (int64_t)u_first * P.tpu);
+  // Every warp's lane 0 issues a share of the tile's bulk copies (the issue sequence of
+  // a single-thread cp.async.bulk is ~15 instructions; spreading them keeps the warps
+  // balanced at the tile barriers).  Copies may complete before the expect_tx arrive;
+  // the phase cannot complete until that arrive.
+  int iss_u = u_first, iss_lt = lt_first, iss_i = 0;
+  auto issue_next = [&]() {
+    const int i = iss_i;
+    const int s = i % kStages;
+    if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+    const int64_t tok = (int64_t)iss_lt * kTile;
+    const int64_t row = (int64_t)iss_u * P.kc.capacity + tok;
+    const int64_t vrow = (int64_t)iss_u * P.vc.capacity + tok;
+    uint8_t* st = sm + L::oStage + s * L::kStageBytes;
+    if (warp == 0) {
+      mbar_expect_tx(&full[s], L::kStageBytes);
+      bulk_g2s(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, &full[s]);
+    } else if (warp == 1) {
+      bulk_g2s(st + L::oCodes, (const uint8_t*)P.vc.codes + vrow * 32, L::kCodes, &full[s]);
+    } else if (warp == 2) {
+      bulk_g2s(st + L::oNormIn, P.kc.norm_in + row, L::kNorm, &full[s]);
+      if (KCO) {
+        bulk_g2s(st + L::oBitsOut, P.kc.bits_out + row * (KCO * 4), L::kBitsOut, &full[s]);
+        bulk_g2s(st + L::oNormOut, P.kc.norm_out + row, L::kNorm, &full[s]);
+      }
+    } else {
+      bulk_g2s(st + L::oZero, (const uint8_t*)P.vc.zero + vrow * 8, L::kConst, &full[s]);
+      bulk_g2s(st + L::oScale, (const uint8_t*)P.vc.scale + vrow * 8, L::kConst, &full[s]);
+    }
+    ++iss_i;
+    if (++iss_lt == P.tpu) { iss_lt = 0; ++iss_u; }
+  };
+  if (lane == 0)
+    for (int i = 0; i < kLookahead && i < ntiles; ++i) issue_next();
+
+  // per-thread running state: token-side partials (l, Z) and dim-side output (acc)
+  float m_run[4], l_part[4], acc[4];
+  float2 Z[4][2];                      // [q][group pair]
+  float4 qcr[4];                       // per-query estimator constants
+  const float wrow = (tid & 3) == 0 ? 1.f : (tid & 3) == 1 ? 0.25f : (tid & 3) == 2 ? 0.0625f : 0.015625f;
+  uint32_t tphase = 0;                      // parity of the per-tile barriers
+
+  auto load_unit = [&](int u) {
+    const uint4* src = reinterpret_cast<const uint4*>(P.bsc + (size_t)u * L::NH * 2048);
+    for (int i = tid; i < L::NH * 128; i += kThreads) reinterpret_cast<uint4*>(sm + L::oBsc)[i] = src[i];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      qcr[q] = P.qconst[(int64_t)u * 4 + q];
+      m_run[q] = -INFINITY;
+      l_part[q] = 0.f;
+      acc[q] = 0.f;
+      Z[q][0] = Z[q][1] = make_float2(0.f, 0.f);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // Bsc -> tensor core
+    bar_sync1();
+  };
+
+  auto flush = [&](int u) {
+    // token-side partials -> warp sums -> smem (the Bsc/Bpv region is free now)
+    float v[20];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      v[q] = l_part[q];
+      v[4 + 4 * q + 0] = Z[q][0].x;
+      v[4 + 4 * q + 1] = Z[q][0].y;
+      v[4 + 4 * q + 2] = Z[q][1].x;
+      v[4 + 4 * q + 3] = Z[q][1].y;
+    }
+#pragma unroll
+    for (int i = 0; i < 20; ++i) v[i] = warp_sum(v[i]);
+    float* red = reinterpret_cast<float*>(sm + L::oRed);
+    bar_sync1();                        // everyone is done with Bsc/Bpv
+    if (lane == 0)
+#pragma unroll
+      for (int i = 0; i < 20; ++i) red[warp * 20 + i] = v[i];
+    bar_sync1();
+    const int c0 = cta_of_tile((int64_t)u * P.tpu, T, C);
+    const int c1 = cta_of_tile((int64_t)u * P.tpu + P.tpu - 1, T, C);
+    const int ns = c1 - c0 + 1, slot = blockIdx.x - c0;
+    float* mypart = P.part + ((int64_t)u * P.max_seg + slot) * P.G * kRec;
+    const int grp = tid >> 5;           // value group of dim tid
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < P.G) {
+        float lq = 0.f, zq = 0.f;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          lq += red[w * 20 + q];
+          zq += red[w * 20 + 4 + 4 * q + grp];
+        }
+        if (tid == 0) {
+          mypart[q * kRec + 0] = m_run[q];
+          mypart[q * kRec + 1] = lq;
+        }
+        mypart[q * kRec + 2 + tid] = acc[q] + zq;
+      }
+    }
+    int* flag = reinterpret_cast<int*>(sm + L::oFlag);
+    if (ns > 1) {
+      __threadfence();
+      bar_sync1();
+      if (tid == 0) *flag = (atomicAdd(&P.counters[u], 1) == ns - 1);
+      bar_sync1();
+      if (!*flag) return;
+      __threadfence();
+    } else {
+      bar_sync1();
+    }
+    const float* up = P.part + (int64_t)u * P.max_seg * P.G * kRec;
+    for (int i = tid; i < P.G * 128; i += kThreads) {
+      const int qq = i >> 7, dim = i & 127;
+      float M = -INFINITY;
+      for (int s = 0; s < ns; ++s) M = fmaxf(M, __ldcg(up + (s * P.G + qq) * kRec));
+      float Ls = 0.f, a = 0.f;
+      for (int s = 0; s < ns; ++s) {
+        const float* W = up + (s * P.G + qq) * kRec;
+        const float ms = __ldcg(W);
+        if (ms == -INFINITY) continue;
+        const float f = ex2(ms - M);
+        Ls = fmaf(f, __ldcg(W + 1), Ls);
+        a = fmaf(f, __ldcg(W + 2 + dim), a);
+      }
+      P.out[((int64_t)u * P.G + qq) * 128 + dim] = a / Ls;
+      if (P.lse && dim == 0) P.lse[(int64_t)u * P.G + qq] = (M + __log2f(Ls)) * kLn2;
+    }
+  };
+
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // Bsc / qconst come from k_uprep
+  int cur_u = -1;
+  int u = u_first, lt = lt_first;
+  int s = 0;
+  uint32_t full_phase = 0;
+  for (int it = 0; it < ntiles; ++it) {
+    if (u != cur_u) {
+      if (cur_u >= 0) flush(cur_u);
+      load_unit(u);
+      cur_u = u;
+    }
+    if (lane == 0 && it + kLookahead < ntiles) issue_next();
+    mbar_wait(&full[s], full_phase);
+    const uint8_t* st = sm + L::oStage + s * L::kStageBytes;
+    auto body = [&](auto mask_tag) {
+    constexpr bool MASK = decltype(mask_tag)::value;
+    const bool valid = !MASK || (int64_t)lt * kTile + tid < P.n;   // this thread's token is < n
+
+    // ---------------- 1. score A operand: masked sign words -> TMEM ----------------
+    {
+      uint32_t wv[KC];
+      const uint4* bi = reinterpret_cast<const uint4*>(st + L::oBitsIn + tid * KCI * 4);
+#pragma unroll
+      for (int c = 0; c < KCI / 4; ++c) {
+        const uint4 x = bi[c];
+        wv[4 * c] = x.x; wv[4 * c + 1] = x.y; wv[4 * c + 2] = x.z; wv[4 * c + 3] = x.w;
+      }
+      if (KCO) {
+        const uint2* bo = reinterpret_cast<const uint2*>(st + L::oBitsOut + tid * KCO * 4);
+#pragma unroll
+        for (int c = 0; c < KCO / 2; ++c) {
+          const uint2 x = bo[c];
+          wv[KCI + 2 * c] = x.x; wv[KCI + 2 * c + 1] = x.y;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < KC; c += 2) {
+        uint32_t r[16];
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int b = 0; b < 8; ++b) r[8 * e + b] = wv[c + e] & (0x01010101u << b);
+        tmem_st16(tlane + 8 * c, r);
+      }
+    }
+    tmem_wait_st();
+    tc_fence_before();
+#if QJL_UD_SPLIT
+    __syncwarp();
+    if (lane == 0) mbar_arrive(a_rdy);
+#else
+    bar_sync1();
+#endif
+    if (warp == 0) {
+      if (elect_one()) {
+        if (QJL_UD_SPLIT) mbar_wait(a_rdy, tphase);
+        tc_fence_after();
+        constexpr uint32_t ID = idesc_i8(16, 0);
+        // descriptor start-address field is in 16-byte units: K chunk c -> +2 per 32 B,
+        // +128 per 2 KB half image
+        tc_mma_i8c<0>(tbase + L::cDsc, tbase, dsc0, ID);
+#pragma unroll
+        for (int c = 1; c < KCI; ++c)
+          tc_mma_i8c<1>(tbase + L::cDsc, tbase + 8 * c, dsc0 + (uint64_t)((c >> 2) * 128 + (c & 3) * 2), ID);
+        if (KCO) {
+          constexpr int h0 = L::NHI * 128;
+          tc_mma_i8c<0>(tbase + L::cDsc + 16, tbase + 8 * KCI, dsc0 + (uint64_t)h0, ID);
+#pragma unroll
+          for (int c = 1; c < KCO; ++c)
+            tc_mma_i8c<1>(tbase + L::cDsc + 16, tbase + 8 * (KCI + c),
+                          dsc0 + (uint64_t)(h0 + (c >> 2) * 128 + (c & 3) * 2), ID);
+        }
+        tc_commit(sc_bar);
+      }
+      __syncwarp();
+    }
+
+    // token-side inputs that do not depend on the MMA
+    const float nin = __half2float(reinterpret_cast<const __half*>(st + L::oNormIn)[tid]);
+    const float nout = KCO ? __half2float(reinterpret_cast<const __half*>(st + L::oNormOut)[tid]) : 0.f;
+    uint2 zr = reinterpret_cast<const uint2*>(st + L::oZero)[tid];
+    uint2 sr = reinterpret_cast<const uint2*>(st + L::oScale)[tid];
+    if (!valid) zr = sr = make_uint2(0u, 0u);              // rows past n
+    // dim-side: this dim's P2T code words (4 tokens x 4 dims each; the thread's slot is d % 4)
+    uint32_t cw[32];
+    {
+      const uint4* cs = reinterpret_cast<const uint4*>(st + L::oCodes + (tid >> 2) * 128);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint4 x = cs[k];
+        cw[4 * k] = x.x; cw[4 * k + 1] = x.y; cw[4 * k + 2] = x.z; cw[4 * k + 3] = x.w;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);            // stage fully read by this warp
+
+    // ---------------- 3. logits, tile maxima ----------------
+    mbar_wait(sc_bar, tphase);
+    tc_fence_after();
+    float lg[4];
+    {
+      uint32_t dr[32];
+      tmem_ld16(tlane + L::cDsc, dr);
+      if (KCO) tmem_ld16(tlane + L::cDsc + 16, dr + 16);
+      tmem_wait_ld();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int* di = reinterpret_cast<const int*>(dr + 4 * q);
+        const float fi = fmaf((float)(di[2] + 256 * di[3]), 65536.f, (float)(di[0] + 256 * di[1]));
+        float l2 = nin * fmaf(qcr[q].x, fi, -qcr[q].y);
+        if (KCO) {
+          const int* dq = reinterpret_cast<const int*>(dr + 16 + 4 * q);
+          const float fo = fmaf((float)(dq[2] + 256 * dq[3]), 65536.f, (float)(dq[0] + 256 * dq[1]));
+          l2 = fmaf(nout, fmaf(qcr[q].z, fo, -qcr[q].w), l2);
+        }
+        lg[q] = valid ? l2 : -INFINITY;
+      }
+    }
+    {
+      float* mx = reinterpret_cast<float*>(sm + L::oMax);
+      const uint32_t hm = hmax2u(sr.x, sr.y);
+      const float2 hf = h2f2(hm);
+      const float smax_w = warp_max_f32(fmaxf(hf.x, hf.y));
+      float tm[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tm[q] = warp_max_f32(lg[q]);
+      if (lane == 0) {
+        *reinterpret_cast<float4*>(mx + warp * 8) = make_float4(tm[0], tm[1], tm[2], tm[3]);
+        mx[warp * 8 + 4] = smax_w;
+        if (QJL_UD_SPLIT) mbar_arrive(mx_rdy);   // release: the maxima are visible
+      }
+    }
+    // A_pv row of dim tid (the score MMA is done, its A columns are free): 32 columns of
+    // 4 tokens, value c * 4^(tid % 4) -- independent of the softmax, so it overlaps the
+    // wait for the other warps' maxima
+    {
+      const uint32_t mk = 0x03030303u << (2 * (tid & 3));
+#pragma unroll
+      for (int k = 0; k < 32; ++k) cw[k] &= mk;
+      tmem_st16(tlane + 0, cw);
+      tmem_st16(tlane + 16, cw + 16);
+    }
+#if QJL_UD_SPLIT
+    mbar_wait(mx_rdy, tphase);
+#else
+    bar_sync1();
+#endif
+
+    // ---------------- 4. softmax, P' digits (tokens), code operand (dims) ----------------
+    float tmax[4], smax;
+    {
+      const float* mx = reinterpret_cast<const float*>(sm + L::oMax);
+      float4 a = *reinterpret_cast<const float4*>(mx), b = *reinterpret_cast<const float4*>(mx + 8),
+             c = *reinterpret_cast<const float4*>(mx + 16), e = *reinterpret_cast<const float4*>(mx + 24);
+      tmax[0] = fmaxf(fmaxf(a.x, b.x), fmaxf(c.x, e.x));
+      tmax[1] = fmaxf(fmaxf(a.y, b.y), fmaxf(c.y, e.y));
+      tmax[2] = fmaxf(fmaxf(a.z, b.z), fmaxf(c.z, e.z));
+      tmax[3] = fmaxf(fmaxf(a.w, b.w), fmaxf(c.w, e.w));
+      smax = fmaxf(fmaxf(mx[4], mx[12]), fmaxf(mx[20], mx[28]));
+    }
+    float alpha[4], p[4], K[4], invK[4];
+    bool moved = false;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float m_new = fmaxf(m_run[q], tmax[q]);          // finite: every tile has a valid token
+      alpha[q] = ex2(m_run[q] - m_new);
+      moved |= alpha[q] != 1.f;
+      m_run[q] = m_new;
+      p[q] = ex2(lg[q] - m_new);
+      const float bound = ex2(tmax[q] - m_new) * smax;     // >= every P' of head q in the tile
+      K[q] = bound > 0.f ? kPMax * rcp_approx(bound) : 0.f;
+      invK[q] = bound * (1.f / kPMax);
+    }
+    if (moved) {                                          // CTA-uniform
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 a2 = make_float2(alpha[q], alpha[q]), z2 = make_float2(0.f, 0.f);
+        l_part[q] *= alpha[q];
+        acc[q] *= alpha[q];
+        Z[q][0] = fma2(Z[q][0], a2, z2);
+        Z[q][1] = fma2(Z[q][1], a2, z2);
+      }
+    }
+    const float2 z01 = h2f2(zr.x), z23 = h2f2(zr.y);
+    const float2 s01 = h2f2(sr.x), s23 = h2f2(sr.y);
+    uint32_t wv[4][4];                                    // [head q][group]
+    {
+      const float2 mg = make_float2(kMagic, kMagic);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        l_part[q] += p[q];
+        const float2 pp = make_float2(p[q], p[q]);
+        Z[q][0] = fma2(pp, z01, Z[q][0]);
+        Z[q][1] = fma2(pp, z23, Z[q][1]);
+        const float pk = p[q] * K[q];
+        const float2 pk2 = make_float2(pk, pk);
+        const float2 w01 = fma2(pk2, s01, mg), w23 = fma2(pk2, s23, mg);
+        wv[q][0] = __float_as_uint(w01.x);
+        wv[q][1] = __float_as_uint(w01.y);
+        wv[q][2] = __float_as_uint(w23.x);
+        wv[q][3] = __float_as_uint(w23.y);
+      }
+    }
+    // B_pv row of this token: column n = 16 q + 4 G + digit, digit = lo, mid, hi, 0 of
+    // v(q, G) = rint(P' K): fma leaves u = v + 32896 in the mantissa, so the word
+    // (w ^ 0x8080) & 0xFFFFFF is {lo, mid, hi, 0} (balanced digits) -- one LOP3 per (q, G)
+    {
+      uint4* bpv = reinterpret_cast<uint4*>(sm + L::oBpv) + tid;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t o[4];
+#pragma unroll
+        for (int G = 0; G < 4; ++G) {
+          asm("lop3.b32 %0, %1, 0x8080, 0xFFFFFF, 0x28;" : "=r"(o[G]) : "r"(wv[q][G]));   // (a ^ b) & c
+        }
+        bpv[128 * q] = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // B_pv -> tensor core
+    tmem_wait_st();
+    tc_fence_before();
+#if QJL_UD_SPLIT
+    __syncwarp();
+    if (lane == 0) mbar_arrive(p_rdy);
+#else
+    bar_sync1();
+#endif
+
+    // ---------------- 5. PV MMA ----------------
+    if (warp == 0) {
+      if (elect_one()) {
+        if (QJL_UD_SPLIT) mbar_wait(p_rdy, tphase);
+        tc_fence_after();
+        constexpr uint32_t ID = idesc_i8(64, 1);
+        tc_mma_i8c<0>(tbase + 32, tbase, dpv0, ID);
+        tc_mma_i8c<1>(tbase + 32, tbase + 8, dpv0 + 32, ID);       // + 512 B per 32 tokens
+        tc_mma_i8c<1>(tbase + 32, tbase + 16, dpv0 + 64, ID);
+        tc_mma_i8c<1>(tbase + 32, tbase + 24, dpv0 + 96, ID);
+        tc_commit(pv_bar);
+      }
+      __syncwarp();
+    }
+
+    // ---------------- 6. accumulate (thread = dim) ----------------
+    mbar_wait(pv_bar, tphase);
+    tc_fence_after();
+    {
+      const int G = warp;                                   // value group of dim tid
+      uint32_t dd[4][4];                                    // [head q][lo, mid, hi, pad]
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tmem_ld4(tlane + 32 + 16 * q + 4 * G, dd[q]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float f = fmaf((float)(int)dd[q][2], 65536.f, (float)((int)dd[q][0] + 256 * (int)dd[q][1]));
+        acc[q] = fmaf(f, invK[q] * wrow, acc[q]);
+      }
+    }
+    };
+    if ((int64_t)(lt + 1) * kTile <= P.n) body(std::false_type{});
+    else body(std::true_type{});
+    if (++lt == P.tpu) { lt = 0; ++u; }
+    if (++s == kStages) { s = 0; full_phase ^= 1; }
+    tphase ^= 1;
+  }
+  if (cur_u >= 0) flush(cur_u);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(L::kAlloc));
+}
+
+struct Plan {
+  int tpu, ctas, max_seg;
+  int64_t T;
+  size_t bsc_off, qconst_off, part_off, cnt_off, total;
+};
+
+template <int KCI, int KCO>
+static int occupancy() {
+  using L = Layout<KCI, KCO>;
+  static int occ = -1;
+  if (occ < 0) {
+    cudaFuncSetAttribute(k_udecode<KCI, KCO>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    cudaFuncSetAttribute(k_udecode<KCI, KCO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int o = 0;
+    // The runtime's occupancy calculator reports 1 CTA/SM for kernels that use tcgen05
+    // (it cannot know the TMEM footprint), so resident CTAs are derived from the
+    // register file, shared memory and the 512 TMEM columns directly.
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k_udecode<KCI, KCO>);
+    int dev = 0, smem_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+    const int by_regs = 65536 / (regs_warp * (kThreads / 32));
+    const int by_smem = smem_sm / (L::kTotal + 1024);
+    o = by_regs < by_smem ? by_regs : by_smem;
+    const int tmem_cap = 512 / L::kAlloc;
+    occ = o < 1 ? 1 : (o > tmem_cap ? tmem_cap : o);
+    if (getenv("QJL_DEBUG"))
+      fprintf(stderr, "k_udecode<%d,%d>: %d CTAs/SM (regs %d -> %d, smem %d/%d -> %d, tmem cols %d)\n", KCI, KCO,
+              occ, fa.numRegs, by_regs, L::kTotal, smem_sm, by_smem, L::kAlloc);
+  }
+  return occ;
+}
+
+static bool kc_dispatch(int kci, int kco, int* id) {
+  const int pairs[][2] = {{8, 2}, {8, 4}, {8, 0}, {16, 2}, {16, 0}, {16, 4}};
+  for (int i = 0; i < 6; ++i)
+    if (pairs[i][0] == kci && pairs[i][1] == kco) { *id = i; return true; }
+  return false;
+}
+static int occupancy_by_id(int id) {
+  switch (id) {
+    case 0: return occupancy<8, 2>();
+    case 1: return occupancy<8, 4>();
+    case 2: return occupancy<8, 0>();
+    case 3: return occupancy<16, 2>();
+    case 4: return occupancy<16, 0>();
+    case 5: return occupancy<16, 4>();
+  }
+  return 1;
+}
+static int nh_by_id(int id) {
+  const int nh[] = {3, 3, 2, 5, 4, 5};
+  return nh[id];
+}
+static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+static Plan make_plan(const qjl_key_cache_t& kc, int64_t n, int G, int id) {
+  Plan p;
+  p.tpu = (int)((n + kTile - 1) / kTile);
+  p.T = (int64_t)kc.units * p.tpu;
+  const int64_t slots = (int64_t)device_sm_count() * occupancy_by_id(id);
+  p.ctas = (int)(p.T < slots ? p.T : slots);
+  int ms = 1;
+  for (int u = 0; u < kc.units; ++u) {
+    const int c0 = cta_of_tile((int64_t)u * p.tpu, p.T, p.ctas);
+    const int c1 = cta_of_tile((int64_t)u * p.tpu + p.tpu - 1, p.T, p.ctas);
+    ms = ms > c1 - c0 + 1 ? ms : c1 - c0 + 1;
+  }
+  p.max_seg = ms;
+  p.bsc_off = 0;
+  p.qconst_off = align256((size_t)kc.units * nh_by_id(id) * 2048);
+  p.part_off = p.qconst_off + align256((size_t)kc.units * 4 * 16);
+  p.cnt_off = p.part_off + align256((size_t)kc.units * p.max_seg * G * kRec * 4);
+  p.total = p.cnt_off + align256((size_t)kc.units * 4);
+  return p;
+}
+
+}  // namespace ud
+
+bool decode_umma_supported(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int G) {
+  int id;
+  return vc.layout == QJL_VLAYOUT_P2T && kc.d == 128 && G >= 1 && G <= 4 &&
+         ud::kc_dispatch(kc.m_in / 32, kc.m_out / 32, &id) && kc.capacity % ud::kTile == 0 &&
+         vc.capacity % ud::kTile == 0 && getenv("QJL_FORCE_SIMT") == nullptr;
+}
+
+size_t decode_umma_workspace(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, int G) {
+  int id;
+  ud::kc_dispatch(kc.m_in / 32, kc.m_out / 32, &id);
+  (void)vc;
+  return ud::make_plan(kc, n, G, id).total;
+}
+
+template <int KCI, int KCO>
+static int launch_umma_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, const void* q,
+                            int q_dtype, int G, const qjl_sketch_t& sk, float inv_t, float* out, float* lse, void* ws,
+                            const ud::Plan& plan, cudaStream_t st) {
+  using namespace ud;
+  uint8_t* w = (uint8_t*)ws;
+  uint8_t* bsc = w + plan.bsc_off;
+  float4* qconst = (float4*)(w + plan.qconst_off);
+  float* part = (float*)(w + plan.part_off);
+  int* counters = (int*)(w + plan.cnt_off);
+  constexpr int MT = (KCI + KCO) * 32;
+#define QJL_UPREP(TQ, TS)                                                                        \
+  k_uprep<TQ, TS, KCI, KCO><<<kc.units, MT, 0, st>>>((const TQ*)q, G, (const TS*)sk.s_full,      \
+                                                     sk.unit_stride, inv_t, bsc, qconst, counters)
+#define QJL_UPREP_S(TQ)                                                  \
+  switch (sk.dtype) {                                                    \
+    case QJL_BF16: QJL_UPREP(TQ, __nv_bfloat16); break;                  \
+    case QJL_F16: QJL_UPREP(TQ, __half); break;                          \
+    case QJL_F32: QJL_UPREP(TQ, float); break;                           \
+    default: QJL_UPREP(TQ, double); break;                               \
+  }
+  switch (q_dtype) {
+    case QJL_BF16: QJL_UPREP_S(__nv_bfloat16); break;
+    case QJL_F16: QJL_UPREP_S(__half); break;
+    case QJL_F32: QJL_UPREP_S(float); break;
+    default: QJL_UPREP_S(double); break;
+  }
+#undef QJL_UPREP_S
+#undef QJL_UPREP
+  QJL_LAUNCH_CHECK("decode_umma_prep");
+  Params P;
+  P.kc = kc;
+  P.vc = vc;
+  P.n = n;
+  P.G = G;
+  P.units = kc.units;
+  P.tpu = plan.tpu;
+  P.total_tiles = plan.T;
+  P.ctas = plan.ctas;
+  P.max_seg = plan.max_seg;
+  P.bsc = bsc;
+  P.qconst = qconst;
+  P.part = part;
+  P.counters = counters;
+  P.out = out;
+  P.lse = lse;
+  occupancy<KCI, KCO>();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(plan.ctas);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Layout<KCI, KCO>::kTotal;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = timing_enabled() ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  timing_begin(st);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_udecode<KCI, KCO>, P);
+  timing_end(st);
+  if (e != cudaSuccess) return cuda_status(e, "decode_umma");
+  QJL_LAUNCH_CHECK("decode_umma");
+  return QJL_OK;
+}
+
+int launch_decode_umma(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, const void* q,
+                       int q_dtype, int G, const qjl_sketch_t& sk, float inv_t, float* out, float* lse, void* ws,
+                       size_t ws_bytes, cudaStream_t st) {
+  int id;
+  if (!ud::kc_dispatch(kc.m_in / 32, kc.m_out / 32, &id)) return QJL_ERR_UNSUPPORTED;
+  const ud::Plan plan = ud::make_plan(kc, n, G, id);
+  if (ws_bytes < plan.total) {
+    set_error("decode workspace needs %zu bytes", plan.total);
+    return QJL_ERR_WORKSPACE;
+  }
+  switch (id) {
+    case 0: return launch_umma_impl<8, 2>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, st);
+    case 1: return launch_umma_impl<8, 4>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, st);
+    case 2: return launch_umma_impl<8, 0>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, st);
+    case 3: return launch_umma_impl<16, 2>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, st);
+    case 4: return launch_umma_impl<16, 0>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, st);
+    case 5: return launch_umma_impl<16, 4>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, st);
+  }
+  return QJL_ERR_UNSUPPORTED;
+}
+
+}  // namespace qjl

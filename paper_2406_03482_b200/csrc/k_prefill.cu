@@ -313,7 +313,8 @@ __global__ void __launch_bounds__(256) k_quantize_values(const T* __restrict__ v
   const bool valid = t < n;
   const T* V = v + (int64_t)u * unit_stride + (valid ? t : 0) * d;
   const int64_t row = (int64_t)u * vc.capacity + row_offset + t;
-  const bool p2 = vc.layout == QJL_VLAYOUT_P2;
+  const bool p2 = vc.layout == QJL_VLAYOUT_P2 || vc.layout == QJL_VLAYOUT_P2T;
+  const bool p2t = vc.layout == QJL_VLAYOUT_P2T;
   for (int g = 0; g < G; ++g) {
     // group g spans dims [g*gs, (g+1)*gs); lanes stride over it
     double mn = INFINITY, mx = -INFINITY;
@@ -341,16 +342,29 @@ __global__ void __launch_bounds__(256) k_quantize_values(const T* __restrict__ v
       if (!p2) {
         if (valid) reinterpret_cast<uint8_t*>(vc.codes)[row * d + dim] = (uint8_t)code;
       } else {
-        // P2 (d = 128, group 32, 2 bits): dim 32g + lane sits in byte (row g & 7 =
-        // lane & 7, k = g) at slot lane >> 3; OR the four slots of a byte together
-        uint32_t b = (uint32_t)code << (2 * (lane >> 3));
-        b |= __shfl_xor_sync(0xffffffffu, b, 8);
-        b |= __shfl_xor_sync(0xffffffffu, b, 16);
-        if (valid && lane < 8) {
-          int64_t byte;
-          int sh;
-          p2_pos(row, dim, &byte, &sh);
-          reinterpret_cast<uint8_t*>(vc.codes)[byte] = (uint8_t)b;
+        if (p2t) {
+          // P2T: dims 4a..4a+3 share a byte (slot = dim & 3); OR the four lanes together
+          uint32_t b = (uint32_t)code << (2 * (lane & 3));
+          b |= __shfl_xor_sync(0xffffffffu, b, 1);
+          b |= __shfl_xor_sync(0xffffffffu, b, 2);
+          if (valid && (lane & 3) == 0) {
+            int64_t byte;
+            int sh;
+            p2t_pos(row, dim, &byte, &sh);
+            reinterpret_cast<uint8_t*>(vc.codes)[byte] = (uint8_t)b;
+          }
+        } else {
+          // P2 (d = 128, group 32, 2 bits): dim 32g + lane sits in byte (row g & 7 =
+          // lane & 7, k = g) at slot lane >> 3; OR the four slots of a byte together
+          uint32_t b = (uint32_t)code << (2 * (lane >> 3));
+          b |= __shfl_xor_sync(0xffffffffu, b, 8);
+          b |= __shfl_xor_sync(0xffffffffu, b, 16);
+          if (valid && lane < 8) {
+            int64_t byte;
+            int sh;
+            p2_pos(row, dim, &byte, &sh);
+            reinterpret_cast<uint8_t*>(vc.codes)[byte] = (uint8_t)b;
+          }
         }
       }
     }

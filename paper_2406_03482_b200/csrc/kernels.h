@@ -47,4 +47,11 @@ int launch_decode_tc(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int
                      const void* q, int q_dtype, int G, const qjl_sketch_t& sk, float inv_t,
                      float* out, float* lse, void* ws, size_t ws_bytes, cudaStream_t st);
 
+// tcgen05 fused decode for P2T caches (kind::i8 UMMA scores + PV, TMEM accumulators)
+bool decode_umma_supported(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int G);
+size_t decode_umma_workspace(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, int G);
+int launch_decode_umma(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, const void* q,
+                       int q_dtype, int G, const qjl_sketch_t& sk, float inv_t, float* out, float* lse,
+                       void* ws, size_t ws_bytes, cudaStream_t st);
+
 }  // namespace qjl

@@ -68,7 +68,7 @@ class DeviceKeyCache:
 
     def __init__(self, units: int, d: int, m_in: int, m_out: int, h: int, capacity: int, *,
                  key_dtype: torch.dtype = torch.bfloat16, value_bits: int = 2,
-                 value_group: int = 32, value_layout: str = "p2", with_values: bool = True,
+                 value_group: int = 32, value_layout: str = "p2t", with_values: bool = True,
                  sketch_dtype: torch.dtype | None = None, device: str | torch.device = "cuda",
                  validate_rate: bool = True):
         self.lib = _lib.load()
@@ -106,9 +106,9 @@ class DeviceKeyCache:
         self.value_bits, self.value_group = value_bits, value_group
         if with_values:
             G = d // value_group
-            if value_layout == "p2":
+            if value_layout in ("p2", "p2t"):
                 if not (d == 128 and value_bits == 2 and value_group == 32):
-                    raise ValueError("p2 value layout is 2-bit, group 32, d = 128")
+                    raise ValueError(f"{value_layout} value layout is 2-bit, group 32, d = 128")
                 self.v_codes = torch.zeros(units, capacity, d // 4, dtype=torch.uint8, device=dev)
                 self.v_zero = torch.zeros(units, capacity, G, dtype=torch.float16, device=dev)
                 self.v_scale = torch.zeros(units, capacity, G, dtype=torch.float16, device=dev)
@@ -129,7 +129,8 @@ class DeviceKeyCache:
 
     def value_desc(self) -> _lib.ValueCacheDesc:
         s = self.shape
-        layout = _lib.QJL_VLAYOUT_P2 if self.value_layout == "p2" else _lib.QJL_VLAYOUT_U8
+        layout = {"p2": _lib.QJL_VLAYOUT_P2, "p2t": _lib.QJL_VLAYOUT_P2T}.get(self.value_layout,
+                                                                             _lib.QJL_VLAYOUT_U8)
         return _lib.ValueCacheDesc(_ptr(self.v_codes), _ptr(self.v_zero), _ptr(self.v_scale),
                                    s.capacity, s.units, s.d, self.value_bits, self.value_group,
                                    layout)
@@ -351,7 +352,24 @@ def _p2_tables():
 _P2_BYTE, _P2_SHIFT = _p2_tables()
 
 
-def p2_unpack_codes(packed: np.ndarray, n: int | None = None) -> np.ndarray:
+def _p2t_tables():
+    """P2T byte offset / shift of every (token, dim) of a 128-token tile (`p2t_pos`)."""
+    t = np.arange(128)[:, None]
+    d = np.arange(128)[None, :]
+    byte = (d >> 2) * 128 + (t >> 2) * 4 + (t & 3)
+    return (np.broadcast_to(byte, (128, 128)).astype(np.int64),
+            np.broadcast_to(2 * (d & 3), (128, 128)).astype(np.uint8))
+
+
+_P2T_BYTE, _P2T_SHIFT = _p2t_tables()
+
+
+def unpack_codes(packed: np.ndarray, n: int | None = None, layout: str = "p2") -> np.ndarray:
+    """Host decoder of a packed 2-bit code layout ("p2" or "p2t") -> codes [..., n, 128]."""
+    return p2_unpack_codes(packed, n, layout)
+
+
+def p2_unpack_codes(packed: np.ndarray, n: int | None = None, layout: str = "p2") -> np.ndarray:
     """Host decoder of the P2 tile-interleaved code layout: packed u8 [..., cap, 32]
     (cap a multiple of 128, rows counted from the unit's row 0) -> codes [..., n, 128]."""
     packed = np.ascontiguousarray(packed, dtype=np.uint8)
@@ -359,12 +377,13 @@ def p2_unpack_codes(packed: np.ndarray, n: int | None = None) -> np.ndarray:
     if cap % 128:
         raise ValueError("P2 code arrays hold whole 128-token tiles")
     tiles = packed.reshape(packed.shape[:-2] + (cap // 128, 4096))
-    codes = (tiles[..., _P2_BYTE] >> _P2_SHIFT) & 3
+    bt, sh = (_P2T_BYTE, _P2T_SHIFT) if layout == "p2t" else (_P2_BYTE, _P2_SHIFT)
+    codes = (tiles[..., bt] >> sh) & 3
     codes = codes.reshape(packed.shape[:-2] + (cap, 128)).astype(np.uint8)
     return codes if n is None else codes[..., :n, :]
 
 
-def p2_pack_codes(codes: np.ndarray) -> np.ndarray:
+def p2_pack_codes(codes: np.ndarray, layout: str = "p2") -> np.ndarray:
     """Inverse of p2_unpack_codes: codes [..., n, 128] -> packed u8 [..., cap, 32],
     cap = n rounded up to whole 128-token tiles (padding codes are 0)."""
     codes = np.asarray(codes, np.uint8)
@@ -374,8 +393,9 @@ def p2_pack_codes(codes: np.ndarray) -> np.ndarray:
     full[..., :n, :] = codes & 3
     tiles = full.reshape(codes.shape[:-2] + (cap // 128, 128 * 128))
     out = np.zeros(codes.shape[:-2] + (cap // 128, 4096), np.uint8)
-    flat_byte = _P2_BYTE.reshape(-1)
-    flat_shift = _P2_SHIFT.reshape(-1)
+    bt, sh = (_P2T_BYTE, _P2T_SHIFT) if layout == "p2t" else (_P2_BYTE, _P2_SHIFT)
+    flat_byte = bt.reshape(-1)
+    flat_shift = sh.reshape(-1)
     order = np.argsort(flat_byte, kind="stable")          # 4 (token, dim) per byte
     contrib = (tiles[..., order].astype(np.uint32) << flat_shift[order]).reshape(
         codes.shape[:-2] + (cap // 128, 4096, 4)).sum(-1)

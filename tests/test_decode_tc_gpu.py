@@ -15,7 +15,7 @@ from tests._parity import OUT_RTOL, rel_l2
 pytestmark = pytest.mark.gpu
 
 
-def _cache(U, n, G, h, m_in, m_out, seed, dtype=torch.bfloat16, factor=20.0):
+def _cache(U, n, G, h, m_in, m_out, seed, dtype=torch.bfloat16, factor=20.0, layout="p2"):
     from paper_2406_03482_b200.device import DeviceKeyCache
 
     gen = torch.Generator(device="cuda")
@@ -28,7 +28,8 @@ def _cache(U, n, G, h, m_in, m_out, seed, dtype=torch.bfloat16, factor=20.0):
     V = torch.randn(U, n, 128, generator=gen, device="cuda")
     Qx = torch.randn(U, G, 128, generator=gen, device="cuda")
     K, V, Qx = K.to(dtype), V.to(dtype), Qx.to(dtype)
-    c = DeviceKeyCache.create(U, 128, m_in, h=h, m_out=m_out, capacity=n, seed=seed, key_dtype=dtype)
+    c = DeviceKeyCache.create(U, 128, m_in, h=h, m_out=m_out, capacity=n, seed=seed, key_dtype=dtype,
+                              value_layout=layout)
     if h:
         c.detect_outliers(K)
         c.set_sketches(c.S_in_host, c.S_out_host)

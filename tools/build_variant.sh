@@ -10,11 +10,11 @@ mkdir -p $OUT
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 FLAGS="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr $DEFS"
 pids=()
-for f in api k_prefill k_scores k_decode_simt k_decode_tc k_quant_tc; do
+for f in api k_prefill k_scores k_decode_simt k_decode_tc k_decode_umma k_quant_tc; do
   nvcc $FLAGS -Xptxas -v -c $SRC/$f.cu -o $OUT/$f.o 2> $OUT/$f.ptxas.log &
   pids+=($!)
 done
 for p in ${pids[@]}; do wait $p; done
 nvcc $ARCH -shared -cudart static -o $ROOT/variants/libqjl_$NAME.so $OUT/*.o -Xlinker --exclude-libs,ALL
-grep -A2 "k_decode_tcILi8ELi2" $OUT/k_decode_tc.ptxas.log | grep -E "registers|spill" | tr '\n' ' '; echo " -> variants/libqjl_$NAME.so"
+grep -A2 "k_udecodeILi8ELi2" $OUT/k_decode_umma.ptxas.log | grep -E "registers|spill" | tr '\n' ' '; echo " -> variants/libqjl_$NAME.so"
 rm -rf $OUT

@@ -16,7 +16,8 @@ def rel(a, b):
 
 
 U, n, G = int(sys.argv[1]), int(sys.argv[2]), 4
-c, q = _cache(U, n, G, 8, 256, 64, seed=U * 7 + n)
+layout = sys.argv[3] if len(sys.argv) > 3 else "p2"
+c, q = _cache(U, n, G, 8, 256, 64, seed=U * 7 + n, layout=layout)
 Qh = q.double().cpu().numpy()
 for T in (1.0, float(np.sqrt(128))):
     a, b = _both(c, q, T)
@@ -24,7 +25,7 @@ for T in (1.0, float(np.sqrt(128))):
         chans = tuple(int(x) for x in c.channels[u, :8].cpu().numpy())
         cache = dict(bits_in=c.bits_in[u, :n].cpu().numpy(), norm_in=c.norm_in[u, :n].double().cpu().numpy(),
                      bits_out=c.bits_out[u, :n].cpu().numpy(), norm_out=c.norm_out[u, :n].double().cpu().numpy())
-        codes = p2_unpack_codes(c.v_codes[u].cpu().numpy(), n)
+        codes = p2_unpack_codes(c.v_codes[u].cpu().numpy(), n, layout)
         deq = O.dequantize_values(codes, c.v_zero[u, :n].double().cpu().numpy(), c.v_scale[u, :n].double().cpu().numpy())
         for g in range(G):
             ref, _, _ = O.quantized_decode(c.S_in_host, c.S_out_host, chans, Qh[u, g], cache, deq, temperature=T)

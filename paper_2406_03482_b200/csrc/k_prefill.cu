@@ -53,9 +53,107 @@ __global__ void __launch_bounds__(1024) k_detect_outliers(const T* __restrict__ 
   }
 }
 
+// Two-phase form for large prompts: (1) CTAs over (row block, unit) accumulate |k| per
+// channel in fp64 over 256 rows with 16-byte loads; (2) one CTA per unit adds the
+// block partials in a fixed order, then ranks.  |bf16| / |fp16| sums are exact in
+// fp64 at these lengths, so the result does not depend on the split.
+constexpr int kDetRows = 256;
+template <typename T>
+__global__ void __launch_bounds__(256) k_detect_partial(const T* __restrict__ keys, int64_t n0, int d,
+                                                        int64_t unit_stride, double* __restrict__ part) {
+  constexpr int EPV = 16 / (int)sizeof(T);
+  extern __shared__ double sm_part[];             // [rows_par][d]
+  const int u = blockIdx.y, blk = blockIdx.x;
+  const int tpr = d / EPV;                        // threads per row
+  const int rows_par = blockDim.x / tpr;
+  const int cg = threadIdx.x % tpr, rs = threadIdx.x / tpr;
+  const T* K = keys + (int64_t)u * unit_stride;
+  double acc[EPV];
+#pragma unroll
+  for (int e = 0; e < EPV; ++e) acc[e] = 0.0;
+  if (rs < rows_par) {
+    const int64_t r_end = min((int64_t)(blk + 1) * kDetRows, n0);
+    for (int64_t r = (int64_t)blk * kDetRows + rs; r < r_end; r += rows_par) {
+      const uint4 raw = __ldg(reinterpret_cast<const uint4*>(K + r * d + cg * EPV));
+      const T* v = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int e = 0; e < EPV; ++e) acc[e] += fabs(to_f64(v[e]));
+    }
+#pragma unroll
+    for (int e = 0; e < EPV; ++e) sm_part[rs * d + cg * EPV + e] = acc[e];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    double t = 0.0;
+    for (int i = 0; i < rows_par; ++i) t += sm_part[i * d + c];
+    part[((int64_t)u * gridDim.x + blk) * d + c] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_detect_finish(const double* __restrict__ part, int nblk, int64_t n0,
+                                                        int d, int h, int32_t* __restrict__ channels,
+                                                        double* __restrict__ magnitudes) {
+  __shared__ double mag[1024];
+  __shared__ int sel[1024];
+  const int u = blockIdx.x;
+  if (threadIdx.x < d) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += part[((int64_t)u * nblk + b) * d + threadIdx.x];
+    mag[threadIdx.x] = s / (double)n0;
+  }
+  __syncthreads();
+  if (threadIdx.x < d) {
+    const double mc = mag[threadIdx.x];
+    int rank = 0;
+    for (int j = 0; j < d; ++j) {
+      const double mj = mag[j];
+      rank += (mj > mc) || (mj == mc && j < (int)threadIdx.x);
+    }
+    sel[threadIdx.x] = rank < h;
+    if (magnitudes) magnitudes[(int64_t)u * d + threadIdx.x] = mc;
+  }
+  __syncthreads();
+  if (threadIdx.x < d && sel[threadIdx.x]) {
+    int pos = 0;
+    for (int j = 0; j < (int)threadIdx.x; ++j) pos += sel[j];
+    channels[(int64_t)u * h + pos] = threadIdx.x;
+  }
+}
+
 int launch_detect_outliers(const void* keys, int dtype, int units, int64_t n0, int d,
                            int64_t unit_stride, int h, int32_t* channels, double* mags,
                            cudaStream_t st) {
+  const size_t es = dtype_size(dtype);
+  const bool two_phase = n0 >= 2 * kDetRows && d <= 1024 && (d * es) % 16 == 0 && (unit_stride * es) % 16 == 0 &&
+                         ((uintptr_t)keys % 16) == 0 && 256 % (int)(d * es / 16) == 0;
+  if (two_phase) {
+    const int nblk = (int)((n0 + kDetRows - 1) / kDetRows);
+    double* part = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&part, (size_t)units * nblk * d * sizeof(double), st);
+    if (e != cudaSuccess) return cuda_status(e, "detect_outliers workspace");
+    const int tpr = (int)(d * es / 16), rows_par = 256 / tpr;
+    const size_t smem = (size_t)rows_par * d * sizeof(double);
+    dim3 grid(nblk, units);
+    switch (dtype) {
+#define QJL_DETP(DT)                                                                             \
+  case DT: {                                                                                     \
+    auto kern = k_detect_partial<Elem<DT>::T>;                                                   \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    kern<<<grid, 256, smem, st>>>((const Elem<DT>::T*)keys, n0, d, unit_stride, part);           \
+    break;                                                                                       \
+  }
+      QJL_DETP(QJL_F32)
+      QJL_DETP(QJL_F16)
+      QJL_DETP(QJL_BF16)
+      QJL_DETP(QJL_F64)
+#undef QJL_DETP
+      default: cudaFreeAsync(part, st); return QJL_ERR_ARG;
+    }
+    k_detect_finish<<<units, 1024, 0, st>>>(part, nblk, n0, d, h, channels, mags);
+    cudaFreeAsync(part, st);
+    QJL_LAUNCH_CHECK("detect_outliers");
+    return QJL_OK;
+  }
   const int rows_par = (1024 / d) > 0 ? 1024 / d : 1;
   const int threads = rows_par * d;
   const size_t smem = (size_t)rows_par * d * sizeof(double);
@@ -380,8 +478,113 @@ __global__ void __launch_bounds__(256) k_quantize_values(const T* __restrict__ v
   }
 }
 
+// P2T fast path (2-bit, group 32, d = 128): one thread per (4-token block, group).  The
+// screen runs in fp32; codes whose quotient lies within 1e-3 of a rounding boundary
+// are recomputed exactly as the reference does, in fp64 (kvcache.py:151-159:
+// rint((v - zero) / ((max - min) / 3))), so codes match the reference bit for bit.
+template <typename T>
+__global__ void __launch_bounds__(256) k_quantize_values_p2t(const T* __restrict__ v, int64_t n,
+                                                             int64_t unit_stride, qjl_value_cache_t vc,
+                                                             int64_t row_offset) {
+  constexpr int EPV = 16 / (int)sizeof(T);
+  const int u = blockIdx.y;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = (int)(idx & 3);
+  const int64_t t0 = (idx >> 2) * 4;                    // first token of this thread's block
+  if (t0 >= n) return;
+  const T* V = v + (int64_t)u * unit_stride;
+  uint8_t* codes = reinterpret_cast<uint8_t*>(vc.codes) + (int64_t)u * vc.capacity * 32;
+  uint16_t* zo = reinterpret_cast<uint16_t*>(vc.zero) + (int64_t)u * vc.capacity * 4;
+  uint16_t* so = reinterpret_cast<uint16_t*>(vc.scale) + (int64_t)u * vc.capacity * 4;
+  uint32_t cw[4][8];                                    // [token][byte a = 4-dim slot group] (bits of one byte)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t t = t0 + i;
+#pragma unroll
+    for (int a = 0; a < 8; ++a) cw[i][a] = 0u;
+    if (t >= n) continue;
+    float x[32];
+    const T* src = V + t * 128 + 32 * g;
+#pragma unroll
+    for (int k = 0; k < 32 / EPV; ++k) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(src + k * EPV);
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int j = 0; j < EPV; ++j) x[k * EPV + j] = to_f32(e[j]);
+    }
+    float mn = x[0], mx = x[0];
+#pragma unroll
+    for (int k = 1; k < 32; ++k) {
+      mn = fminf(mn, x[k]);
+      mx = fmaxf(mx, x[k]);
+    }
+    const double mn64 = (double)mn, mx64 = (double)mx;   // inputs are exact in fp32
+    const double spread = mx64 - mn64;
+    const double scale = spread == 0.0 ? 0.0 : spread / 3.0;
+    const int64_t row = row_offset + t;
+    zo[row * 4 + g] = f64_to_f16_bits(mn64);
+    so[row * 4 + g] = f64_to_f16_bits(scale);
+    if (spread != 0.0) {
+      const float inv = 3.0f / (float)spread;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float q = (x[k] - mn) * inv;
+        float r = rintf(q);
+        if (fabsf(q - floorf(q) - 0.5f) < 1e-3f)        // near a tie: exact fp64 quotient
+          r = (float)rint(((double)x[k] - mn64) / scale);
+        const uint32_t c = (uint32_t)fminf(fmaxf(r, 0.f), 3.f);
+        cw[i][k >> 2] |= c << (2 * (k & 3));
+      }
+    }
+  }
+  // dims 32g + 4a' .. + 3 of token t form byte (8g + a') of the P2T tile layout
+  const int64_t r0 = row_offset + t0;
+  if ((r0 & 3) == 0 && t0 + 4 <= n) {
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const uint32_t w = cw[0][a] | (cw[1][a] << 8) | (cw[2][a] << 16) | (cw[3][a] << 24);
+      int64_t byte;
+      int sh;
+      p2t_pos(r0, 32 * g + 4 * a, &byte, &sh);
+      *reinterpret_cast<uint32_t*>(codes + byte) = w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (t0 + i >= n) break;
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        int64_t byte;
+        int sh;
+        p2t_pos(r0 + i, 32 * g + 4 * a, &byte, &sh);
+        codes[byte] = (uint8_t)cw[i][a];
+      }
+    }
+  }
+}
+
 int launch_quantize_values(const void* v, int dtype, int64_t n, int64_t unit_stride,
                            const qjl_value_cache_t& vc, int64_t row_offset, cudaStream_t st) {
+  const size_t es = dtype_size(dtype);
+  if (vc.layout == QJL_VLAYOUT_P2T && dtype != QJL_F64 && ((uintptr_t)v % 16) == 0 &&
+      (unit_stride * es) % 16 == 0) {
+    const int64_t threads = ((n + 3) / 4) * 4;
+    dim3 grid((unsigned)((threads + 255) / 256), vc.units);
+    switch (dtype) {
+      case QJL_F32:
+        k_quantize_values_p2t<float><<<grid, 256, 0, st>>>((const float*)v, n, unit_stride, vc, row_offset);
+        break;
+      case QJL_F16:
+        k_quantize_values_p2t<__half><<<grid, 256, 0, st>>>((const __half*)v, n, unit_stride, vc, row_offset);
+        break;
+      case QJL_BF16:
+        k_quantize_values_p2t<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)v, n, unit_stride, vc,
+                                                                   row_offset);
+        break;
+    }
+    QJL_LAUNCH_CHECK("quantize_values_p2t");
+    return QJL_OK;
+  }
   dim3 grid((unsigned)((n + 7) / 8), vc.units);
   switch (dtype) {
 #define QJL_QV(DT)                                                                          \

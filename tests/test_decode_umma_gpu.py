@@ -75,3 +75,25 @@ def test_umma_lse_and_determinism(cuda):
     lg = c.scores(q).double()
     ref_lse = torch.logsumexp(lg, dim=-1)
     torch.testing.assert_close(lse1.double(), ref_lse, rtol=1e-4, atol=1e-3)
+
+
+def test_p2t_quantizer_exact_ties_and_unaligned_appends(cuda):
+    """Values on a grid that puts many quotients exactly on .5 (round-half-even in the
+    reference), constant groups, and appends starting at rows that are not multiples of 4."""
+    from paper_2406_03482_b200.device import DeviceKeyCache, p2_unpack_codes
+
+    U, n = 2, 203
+    g = torch.Generator().manual_seed(5)
+    V = (torch.randint(0, 7, (U, n, 128), generator=g).double() * 0.5)   # multiples of 1/2 -> ties
+    V[:, 7, 32:64] = 1.25                                                   # constant group
+    V[:, 11] *= 1e-3
+    Vt = V.to(torch.bfloat16)
+    c = DeviceKeyCache(U, 128, 256, 0, 0, n, value_layout="p2t")
+    for a, b in ((0, 5), (5, 6), (6, 70), (70, 203)):                       # unaligned row offsets
+        c.append_values(Vt[:, a:b].to(cuda))
+    Vh = Vt.double().numpy()
+    for u in range(U):
+        codes, zero, scale = O.quantize_values(Vh[u], 2, 32, const_dtype="f16")
+        assert np.array_equal(p2_unpack_codes(c.v_codes[u].cpu().numpy(), n, "p2t"), codes)
+        assert np.array_equal(c.v_zero[u, :n].double().cpu().numpy(), zero)
+        assert np.array_equal(c.v_scale[u, :n].double().cpu().numpy(), scale)

@@ -40,13 +40,22 @@
 namespace qjl {
 namespace ud {
 
+#ifndef QJL_UD_ABLATE
+#define QJL_UD_ABLATE 0     // perf experiments only: 1 no score MMA, 2 no PV MMA, 4 no sign expansion, 8 no P'/codes
+#endif
 #ifndef QJL_UD_SPLIT
 #define QJL_UD_SPLIT 0      // 1: split-phase mbarriers between the warps, 0: CTA barriers
 #endif
 constexpr int kThreads = 128;      // 4 warps; thread t: token t (scores) and dim t (PV)
 constexpr int kTile = 128;         // tokens per tile
-constexpr int kStages = 3;
-constexpr int kLookahead = 2;
+#ifndef QJL_UD_STAGES
+#define QJL_UD_STAGES 3
+#endif
+#ifndef QJL_UD_LA
+#define QJL_UD_LA 2
+#endif
+constexpr int kStages = QJL_UD_STAGES;
+constexpr int kLookahead = QJL_UD_LA;
 constexpr int kRec = 130;          // per (partial, query): m (log2 domain), l, out[128]
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -63,6 +72,7 @@ struct Params {
   int64_t total_tiles;
   int ctas;
   int max_seg;
+  int grouped;           // 1: every unit owns a group of CTAs that stride over its tiles
   const uint8_t* bsc;    // [units][NH][2048] score B operand images (SW128, K-major)
   const float4* qconst;  // [units][4 queries] {k_in, b_in, k_out, b_out}
   float* part;           // [units][max_seg][G][kRec]
@@ -394,8 +404,24 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = P.ctas;
   const int64_t T = P.total_tiles;
-  const int64_t r0 = tile_begin(blockIdx.x, T, C), r1 = tile_begin(blockIdx.x + 1, T, C);
-  const int ntiles = (int)(r1 - r0);
+  // Work split.  grouped: unit u owns CTAs [u C / U, (u + 1) C / U); CTA k of the group
+  // takes tiles k, k + g, k + 2g, ... so a group streams each cache array nearly
+  // contiguously at any moment (DRAM row locality).  Otherwise contiguous stream-K
+  // ranges of the flattened (unit, tile) space.
+  int u_first, lt_first, ntiles, lt_step;
+  if (P.grouped) {
+    u_first = cta_of_tile(blockIdx.x, C, P.units);
+    const int g0 = (int)tile_begin(u_first, C, P.units), g1 = (int)tile_begin(u_first + 1, C, P.units);
+    lt_first = blockIdx.x - g0;
+    lt_step = g1 - g0;
+    ntiles = lt_first < P.tpu ? (P.tpu - lt_first + lt_step - 1) / lt_step : 0;
+  } else {
+    const int64_t r0 = tile_begin(blockIdx.x, T, C), r1 = tile_begin(blockIdx.x + 1, T, C);
+    ntiles = (int)(r1 - r0);
+    u_first = (int)(r0 / P.tpu);
+    lt_first = (int)(r0 - (int64_t)u_first * P.tpu);
+    lt_step = 1;
+  }
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -421,8 +447,6 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   const uint64_t dpv0 = desc_none(smem_u32(sm + L::oBpv), 128, 2048);
   const uint32_t tlane = tbase + ((uint32_t)(warp * 32) << 16);   // this warp's TMEM lanes
 
-  const int u_first = (int)(r0 / P.tpu);
-  const int lt_first = (int)(r0 - (int64_t)u_first * P.tpu);
   // Every warp's lane 0 issues a share of the tile's bulk copies (the issue sequence of
   // a single-thread cp.async.bulk is ~15 instructions; spreading them keeps the warps
   // balanced at the tile barriers).  Copies may complete before the expect_tx arrive;
@@ -436,7 +460,26 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     const int64_t row = (int64_t)iss_u * P.kc.capacity + tok;
     const int64_t vrow = (int64_t)iss_u * P.vc.capacity + tok;
     uint8_t* st = sm + L::oStage + s * L::kStageBytes;
-    if (warp == 0) {
+    if (QJL_UD_ABLATE & 1024) {                    // memory test: bits_in + codes only (8 KB/tile)
+      if (warp == 0) {
+        mbar_expect_tx(&full[s], L::kBitsIn + L::kCodes);
+        bulk_g2s(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, &full[s]);
+      } else if (warp == 1) {
+        bulk_g2s(st + L::oCodes, (const uint8_t*)P.vc.codes + vrow * 32, L::kCodes, &full[s]);
+      }
+    } else if (QJL_UD_ABLATE & 2048) {             // memory test: no norms (bits, codes, consts)
+      if (warp == 0) {
+        mbar_expect_tx(&full[s], L::kBitsIn + L::kCodes + L::kBitsOut + 2 * L::kConst);
+        bulk_g2s(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, &full[s]);
+      } else if (warp == 1) {
+        bulk_g2s(st + L::oCodes, (const uint8_t*)P.vc.codes + vrow * 32, L::kCodes, &full[s]);
+      } else if (warp == 2) {
+        if (KCO) bulk_g2s(st + L::oBitsOut, P.kc.bits_out + row * (KCO * 4), L::kBitsOut, &full[s]);
+      } else {
+        bulk_g2s(st + L::oZero, (const uint8_t*)P.vc.zero + vrow * 8, L::kConst, &full[s]);
+        bulk_g2s(st + L::oScale, (const uint8_t*)P.vc.scale + vrow * 8, L::kConst, &full[s]);
+      }
+    } else if (warp == 0) {
       mbar_expect_tx(&full[s], L::kStageBytes);
       bulk_g2s(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, &full[s]);
     } else if (warp == 1) {
@@ -452,7 +495,8 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       bulk_g2s(st + L::oScale, (const uint8_t*)P.vc.scale + vrow * 8, L::kConst, &full[s]);
     }
     ++iss_i;
-    if (++iss_lt == P.tpu) { iss_lt = 0; ++iss_u; }
+    iss_lt += lt_step;
+    if (iss_lt >= P.tpu) { iss_lt = 0; ++iss_u; }
   };
   if (lane == 0)
     for (int i = 0; i < kLookahead && i < ntiles; ++i) issue_next();
@@ -465,6 +509,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   uint32_t tphase = 0;                      // parity of the per-tile barriers
 
   auto load_unit = [&](int u) {
+    if (QJL_UD_ABLATE & 8192) return;
     const uint4* src = reinterpret_cast<const uint4*>(P.bsc + (size_t)u * L::NH * 2048);
     for (int i = tid; i < L::NH * 128; i += kThreads) reinterpret_cast<uint4*>(sm + L::oBsc)[i] = src[i];
 #pragma unroll
@@ -480,6 +525,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   };
 
   auto flush = [&](int u) {
+    if (QJL_UD_ABLATE & 4096) return;
     // token-side partials -> warp sums -> smem (the Bsc/Bpv region is free now)
     float v[20];
 #pragma unroll
@@ -498,9 +544,17 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
 #pragma unroll
       for (int i = 0; i < 20; ++i) red[warp * 20 + i] = v[i];
     bar_sync1();
-    const int c0 = cta_of_tile((int64_t)u * P.tpu, T, C);
-    const int c1 = cta_of_tile((int64_t)u * P.tpu + P.tpu - 1, T, C);
-    const int ns = c1 - c0 + 1, slot = blockIdx.x - c0;
+    int ns, slot;
+    if (P.grouped) {
+      const int g0 = (int)tile_begin(u, C, P.units), g1 = (int)tile_begin(u + 1, C, P.units);
+      ns = min(g1 - g0, P.tpu);
+      slot = blockIdx.x - g0;
+    } else {
+      const int c0 = cta_of_tile((int64_t)u * P.tpu, T, C);
+      const int c1 = cta_of_tile((int64_t)u * P.tpu + P.tpu - 1, T, C);
+      ns = c1 - c0 + 1;
+      slot = blockIdx.x - c0;
+    }
     float* mypart = P.part + ((int64_t)u * P.max_seg + slot) * P.G * kRec;
     const int grp = tid >> 5;           // value group of dim tid
 #pragma unroll
@@ -531,18 +585,34 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       bar_sync1();
     }
     const float* up = P.part + (int64_t)u * P.max_seg * P.G * kRec;
+    // loads of the ns partials are independent: issue them 16 at a time so the merge
+    // costs ~ceil(ns / 16) L2 round trips instead of 3 * ns dependent ones
     for (int i = tid; i < P.G * 128; i += kThreads) {
       const int qq = i >> 7, dim = i & 127;
-      float M = -INFINITY;
-      for (int s = 0; s < ns; ++s) M = fmaxf(M, __ldcg(up + (s * P.G + qq) * kRec));
-      float Ls = 0.f, a = 0.f;
-      for (int s = 0; s < ns; ++s) {
-        const float* W = up + (s * P.G + qq) * kRec;
-        const float ms = __ldcg(W);
-        if (ms == -INFINITY) continue;
-        const float f = ex2(ms - M);
-        Ls = fmaf(f, __ldcg(W + 1), Ls);
-        a = fmaf(f, __ldcg(W + 2 + dim), a);
+      float M = -INFINITY, Ls = 0.f, a = 0.f;
+      for (int s0 = 0; s0 < ns; s0 += 16) {
+        float mv[16], lv[16], av[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float* W = up + ((s0 + k) * P.G + qq) * kRec;
+          const bool ok = s0 + k < ns;
+          mv[k] = ok ? __ldcg(W) : -INFINITY;
+          lv[k] = ok ? __ldcg(W + 1) : 0.f;
+          av[k] = ok ? __ldcg(W + 2 + dim) : 0.f;
+        }
+        float Mc = M;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) Mc = fmaxf(Mc, mv[k]);
+        const float rs = (M == -INFINITY) ? 0.f : ex2(M - Mc);   // rescale earlier chunks
+        Ls *= rs;
+        a *= rs;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float f = (mv[k] == -INFINITY) ? 0.f : ex2(mv[k] - Mc);
+          Ls = fmaf(f, lv[k], Ls);
+          a = fmaf(f, av[k], a);
+        }
+        M = Mc;
       }
       P.out[((int64_t)u * P.G + qq) * 128 + dim] = a / Ls;
       if (P.lse && dim == 0) P.lse[(int64_t)u * P.G + qq] = (M + __log2f(Ls)) * kLn2;
@@ -563,6 +633,15 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     if (lane == 0 && it + kLookahead < ntiles) issue_next();
     mbar_wait(&full[s], full_phase);
     const uint8_t* st = sm + L::oStage + s * L::kStageBytes;
+    if (QJL_UD_ABLATE & 512) {                       // memory pipeline only
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      lt += lt_step;
+      if (lt >= P.tpu) { lt = 0; ++u; }
+      if (++s == kStages) { s = 0; full_phase ^= 1; }
+      tphase ^= 1;
+      continue;
+    }
     auto body = [&](auto mask_tag) {
     constexpr bool MASK = decltype(mask_tag)::value;
     const bool valid = !MASK || (int64_t)lt * kTile + tid < P.n;   // this thread's token is < n
@@ -584,14 +663,16 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
           wv[KCI + 2 * c] = x.x; wv[KCI + 2 * c + 1] = x.y;
         }
       }
+      if (!(QJL_UD_ABLATE & 4)) {
 #pragma unroll
-      for (int c = 0; c < KC; c += 2) {
-        uint32_t r[16];
+        for (int c = 0; c < KC; c += 2) {
+          uint32_t r[16];
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
+          for (int e = 0; e < 2; ++e)
 #pragma unroll
-          for (int b = 0; b < 8; ++b) r[8 * e + b] = wv[c + e] & (0x01010101u << b);
-        tmem_st16(tlane + 8 * c, r);
+            for (int b = 0; b < 8; ++b) r[8 * e + b] = wv[c + e] & (0x01010101u << b);
+          tmem_st16(tlane + 8 * c, r);
+        }
       }
     }
     tmem_wait_st();
@@ -602,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
 #else
     bar_sync1();
 #endif
-    if (warp == 0) {
+    if (warp == 0 && !(QJL_UD_ABLATE & 1)) {
       if (elect_one()) {
         if (QJL_UD_SPLIT) mbar_wait(a_rdy, tphase);
         tc_fence_after();
@@ -646,10 +727,10 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     if (lane == 0) mbar_arrive(&empty[s]);            // stage fully read by this warp
 
     // ---------------- 3. logits, tile maxima ----------------
-    mbar_wait(sc_bar, tphase);
+    if (!(QJL_UD_ABLATE & 1)) mbar_wait(sc_bar, tphase);
     tc_fence_after();
-    float lg[4];
-    {
+    float lg[4] = {nin, nin + 1.f, nin + 2.f, nin + 3.f};
+    if (!(QJL_UD_ABLATE & 16)) {
       uint32_t dr[32];
       tmem_ld16(tlane + L::cDsc, dr);
       if (KCO) tmem_ld16(tlane + L::cDsc + 16, dr + 16);
@@ -686,15 +767,17 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     // wait for the other warps' maxima
     {
       const uint32_t mk = 0x03030303u << (2 * (tid & 3));
+      if (!(QJL_UD_ABLATE & 8)) {
 #pragma unroll
-      for (int k = 0; k < 32; ++k) cw[k] &= mk;
-      tmem_st16(tlane + 0, cw);
-      tmem_st16(tlane + 16, cw + 16);
+        for (int k = 0; k < 32; ++k) cw[k] &= mk;
+        tmem_st16(tlane + 0, cw);
+        tmem_st16(tlane + 16, cw + 16);
+      }
     }
 #if QJL_UD_SPLIT
     mbar_wait(mx_rdy, tphase);
 #else
-    bar_sync1();
+    if (!(QJL_UD_ABLATE & 64)) bar_sync1();
 #endif
 
     // ---------------- 4. softmax, P' digits (tokens), code operand (dims) ----------------
@@ -758,7 +841,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     {
       uint4* bpv = reinterpret_cast<uint4*>(sm + L::oBpv) + tid;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 4 && !(QJL_UD_ABLATE & 8); ++q) {
         uint32_t o[4];
 #pragma unroll
         for (int G = 0; G < 4; ++G) {
@@ -778,7 +861,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
 #endif
 
     // ---------------- 5. PV MMA ----------------
-    if (warp == 0) {
+    if (warp == 0 && !(QJL_UD_ABLATE & 2)) {
       if (elect_one()) {
         if (QJL_UD_SPLIT) mbar_wait(p_rdy, tphase);
         tc_fence_after();
@@ -793,9 +876,9 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     }
 
     // ---------------- 6. accumulate (thread = dim) ----------------
-    mbar_wait(pv_bar, tphase);
+    if (!(QJL_UD_ABLATE & 2)) mbar_wait(pv_bar, tphase);
     tc_fence_after();
-    {
+    if (!(QJL_UD_ABLATE & 2)) {
       const int G = warp;                                   // value group of dim tid
       uint32_t dd[4][4];                                    // [head q][lo, mid, hi, pad]
 #pragma unroll
@@ -810,7 +893,8 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     };
     if ((int64_t)(lt + 1) * kTile <= P.n) body(std::false_type{});
     else body(std::true_type{});
-    if (++lt == P.tpu) { lt = 0; ++u; }
+    lt += lt_step;
+    if (lt >= P.tpu) { lt = 0; ++u; }
     if (++s == kStages) { s = 0; full_phase ^= 1; }
     tphase ^= 1;
   }
@@ -821,7 +905,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
 }
 
 struct Plan {
-  int tpu, ctas, max_seg;
+  int tpu, ctas, max_seg, grouped;
   int64_t T;
   size_t bsc_off, qconst_off, part_off, cnt_off, total;
 };
@@ -884,11 +968,17 @@ static Plan make_plan(const qjl_key_cache_t& kc, int64_t n, int G, int id) {
   p.T = (int64_t)kc.units * p.tpu;
   const int64_t slots = (int64_t)device_sm_count() * occupancy_by_id(id);
   p.ctas = (int)(p.T < slots ? p.T : slots);
+  p.grouped = (p.ctas >= kc.units && getenv("QJL_UD_CONTIG") == nullptr) ? 1 : 0;
   int ms = 1;
   for (int u = 0; u < kc.units; ++u) {
-    const int c0 = cta_of_tile((int64_t)u * p.tpu, p.T, p.ctas);
-    const int c1 = cta_of_tile((int64_t)u * p.tpu + p.tpu - 1, p.T, p.ctas);
-    ms = ms > c1 - c0 + 1 ? ms : c1 - c0 + 1;
+    int ns;
+    if (p.grouped) {
+      const int g = (int)(tile_begin(u + 1, p.ctas, kc.units) - tile_begin(u, p.ctas, kc.units));
+      ns = g < p.tpu ? g : p.tpu;
+    } else {
+      ns = cta_of_tile((int64_t)u * p.tpu + p.tpu - 1, p.T, p.ctas) - cta_of_tile((int64_t)u * p.tpu, p.T, p.ctas) + 1;
+    }
+    ms = ms > ns ? ms : ns;
   }
   p.max_seg = ms;
   p.bsc_off = 0;
@@ -955,6 +1045,7 @@ static int launch_umma_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
   P.total_tiles = plan.T;
   P.ctas = plan.ctas;
   P.max_seg = plan.max_seg;
+  P.grouped = plan.grouped;
   P.bsc = bsc;
   P.qconst = qconst;
   P.part = part;

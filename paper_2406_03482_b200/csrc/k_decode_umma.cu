@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
     qs[g][i % d] = g < G ? to_acc<acc_t>(q[((int64_t)u * G + g) * d + i % d]) : (acc_t)0;
   }
   if (threadIdx.x < 8) mxbits[threadIdx.x >> 1][threadIdx.x & 1] = 0u;
-  if (threadIdx.x == 0) counters[u] = 0;
+  // let the decode kernel launch now: its prologue and first bulk copies overlap us
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __syncthreads();
   {
     const int r = threadIdx.x;               // blockDim.x == MT
@@ -337,6 +338,10 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
     if (lane == 0) red[g][side][1] = (double)acc * red[g][side][0];
   }
   __syncthreads();
+  // Everything above overlaps the previous decode's tail (this grid is launched with
+  // programmatic dependent launch); the workspace writes below must wait for it.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) counters[u] = 0;
   // B image bytes, 4 per thread iteration (one u32 of a swizzled 16-byte chunk)
   uint8_t* out = bsc + (size_t)u * L::NH * 2048;
   for (int w = threadIdx.x; w < L::NH * 512; w += blockDim.x) {
@@ -898,6 +903,8 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     if (++s == kStages) { s = 0; full_phase ^= 1; }
     tphase ^= 1;
   }
+  // all tiles consumed: the next step's query-sketch kernel may start its math now
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (cur_u >= 0) flush(cur_u);
   tc_fence_before();
   __syncthreads();
@@ -1016,9 +1023,19 @@ static int launch_umma_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
   float* part = (float*)(w + plan.part_off);
   int* counters = (int*)(w + plan.cnt_off);
   constexpr int MT = (KCI + KCO) * 32;
-#define QJL_UPREP(TQ, TS)                                                                        \
-  k_uprep<TQ, TS, KCI, KCO><<<kc.units, MT, 0, st>>>((const TQ*)q, G, (const TS*)sk.s_full,      \
-                                                     sk.unit_stride, inv_t, bsc, qconst, counters)
+  cudaLaunchAttribute pattr[1];
+  pattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pattr[0].val.programmaticStreamSerializationAllowed = timing_enabled() ? 0 : 1;
+  cudaLaunchConfig_t pcfg = {};
+  pcfg.gridDim = dim3(kc.units);
+  pcfg.blockDim = dim3(MT);
+  pcfg.stream = st;
+  pcfg.attrs = pattr;
+  pcfg.numAttrs = 1;
+  cudaError_t pe = cudaErrorInvalidValue;
+#define QJL_UPREP(TQ, TS)                                                                              \
+  pe = cudaLaunchKernelEx(&pcfg, k_uprep<TQ, TS, KCI, KCO>, (const TQ*)q, G, (const TS*)sk.s_full,     \
+                          sk.unit_stride, inv_t, bsc, qconst, counters)
 #define QJL_UPREP_S(TQ)                                                  \
   switch (sk.dtype) {                                                    \
     case QJL_BF16: QJL_UPREP(TQ, __nv_bfloat16); break;                  \
@@ -1034,6 +1051,7 @@ static int launch_umma_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
   }
 #undef QJL_UPREP_S
 #undef QJL_UPREP
+  if (pe != cudaSuccess) return cuda_status(pe, "decode_umma_prep");
   QJL_LAUNCH_CHECK("decode_umma_prep");
   Params P;
   P.kc = kc;

@@ -239,7 +239,7 @@ struct Layout {
   static constexpr int oStage = oBpv + 4 * 2048;
   static constexpr int oMax = oStage + kStages * kStageBytes;   // [4 warps][8] tile maxima
   static constexpr int oBar = oMax + 4 * 8 * 4;
-  static constexpr int kBars = 2 * kStages + 5;
+  static constexpr int kBars = 2 * kStages + 6;
   static constexpr int oTmem = oBar + kBars * 8;
   static constexpr int oFlag = oTmem + 4;
   static constexpr int kTotal = oFlag + 12 + 1024;      // + alignment slack
@@ -405,6 +405,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   uint64_t* a_rdy = sc_bar + 2;             // 4 warps: score A operand in TMEM
   uint64_t* mx_rdy = sc_bar + 3;            // 4 warps: tile maxima in smem
   uint64_t* p_rdy = sc_bar + 4;             // 4 warps: PV operands (B smem, A TMEM) ready
+  uint64_t* bsc_bar = sc_bar + 5;           // the unit's score B image landed (bulk copy)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::oTmem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = P.ctas;
@@ -437,6 +438,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     mbar_init(a_rdy, 4);
     mbar_init(mx_rdy, 4);
     mbar_init(p_rdy, 4);
+    mbar_init(bsc_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -513,10 +515,14 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   const float wrow = (tid & 3) == 0 ? 1.f : (tid & 3) == 1 ? 0.25f : (tid & 3) == 2 ? 0.0625f : 0.015625f;
   uint32_t tphase = 0;                      // parity of the per-tile barriers
 
+  uint32_t bsc_phase = 0, bsc_par = 0;      // bsc_phase: 0 = wait for the copy before the next MMA
   auto load_unit = [&](int u) {
-    if (QJL_UD_ABLATE & 8192) return;
-    const uint4* src = reinterpret_cast<const uint4*>(P.bsc + (size_t)u * L::NH * 2048);
-    for (int i = tid; i < L::NH * 128; i += kThreads) reinterpret_cast<uint4*>(sm + L::oBsc)[i] = src[i];
+    bsc_phase = 0;
+    // the unit's score B image: one bulk copy; only the MMA issuer waits for it
+    if (tid == 0) {
+      mbar_expect_tx(bsc_bar, L::NH * 2048);
+      bulk_g2s(sm + L::oBsc, P.bsc + (size_t)u * L::NH * 2048, L::NH * 2048, bsc_bar);
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       qcr[q] = P.qconst[(int64_t)u * 4 + q];
@@ -525,8 +531,6 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       acc[q] = 0.f;
       Z[q][0] = Z[q][1] = make_float2(0.f, 0.f);
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // Bsc -> tensor core
-    bar_sync1();
   };
 
   auto flush = [&](int u) {
@@ -691,6 +695,11 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     if (warp == 0 && !(QJL_UD_ABLATE & 1)) {
       if (elect_one()) {
         if (QJL_UD_SPLIT) mbar_wait(a_rdy, tphase);
+        if (bsc_phase == 0) {                      // first tile of a unit: B image landed?
+          mbar_wait(bsc_bar, bsc_par);
+          bsc_par ^= 1;
+          bsc_phase = 1;
+        }
         tc_fence_after();
         constexpr uint32_t ID = idesc_i8(16, 0);
         // descriptor start-address field is in 16-byte units: K chunk c -> +2 per 32 B,

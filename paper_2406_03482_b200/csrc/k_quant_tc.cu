@@ -42,11 +42,21 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+#ifndef QJL_K1_SUSPEND_NS
+#define QJL_K1_SUSPEND_NS 0   // try_wait suspend-time hint (ns); 0 = default polling (measured faster)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+#if QJL_K1_SUSPEND_NS
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity), "n"(QJL_K1_SUSPEND_NS) : "memory");
+#else
   asm volatile(
       "{\n.reg .pred p;\nWAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+#endif
 }
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
   asm volatile(
@@ -106,6 +116,29 @@ __device__ __forceinline__ uint32_t sign_word(const uint32_t* r) {
     a[i & 3] |= m & (1u << i);
   }
   return (a[0] | a[1]) | (a[2] | a[3]);
+}
+#ifndef QJL_K1_FASTSIGN
+#define QJL_K1_FASTSIGN 1
+#endif
+// Same bits with ~1.5 instructions per bit: x + 0 (one FFMA2 per pair) turns -0.0 into
+// +0.0, then a funnel shift per element collects the sign bits and one NOT flips them.
+// A NaN projection has NaN in every column of its row (the NaN key element meets every
+// sketch row, padding zeros included), so checking the first column of the word keeps
+// the reference's NaN -> 0.
+__device__ __forceinline__ uint32_t sign_word_fast(const uint32_t* r) {
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 30; i >= 0; i -= 2) {
+    float y0, y1;
+    asm("{\n.reg .b64 a, b, c, o;\nmov.b64 a, {%2, %3};\nmov.b64 b, {%4, %4};\nmov.b64 c, {%5, %5};\n"
+        "fma.rn.f32x2 o, a, b, c;\nmov.b64 {%0, %1}, o;\n}"
+        : "=f"(y0), "=f"(y1)
+        : "f"(__uint_as_float(r[i])), "f"(__uint_as_float(r[i + 1])), "f"(1.0f), "f"(0.0f));
+    acc = __funnelshift_l(__float_as_uint(y1), acc, 1);
+    acc = __funnelshift_l(__float_as_uint(y0), acc, 1);
+  }
+  const float x0 = __uint_as_float(r[0]);
+  return (x0 != x0) ? 0u : ~acc;
 }
 // 64 fp32 accumulator columns of this thread's TMEM lane
 __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t* r) {
@@ -289,20 +322,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       const int s = it % STAGES;
       mbar_wait(&a_full[s], (it / STAGES) & 1);
       const uint8_t* a = sm + L::oA + s * L::kABytes;
-      // One token row per thread.  x^2 is exact in fp32 (<= 11-bit significands);
-      // the sum is carried as an unevaluated double-float (TwoSum, 4 chains), so the
-      // result matches an fp64 accumulation to ~1e-14 relative without fp64 math.
+      // One token row per thread.  x^2 is exact in fp32 (<= 11-bit significands).  Fast
+      // path: fp32 sum of squares with FFMA2 (4 chains, relative error <= 2^-19), and the
+      // outlier channels summed exactly in fp64.  When the fp16 rounding of the inlier
+      // norm is not decided by that bound, the row is recomputed as an unevaluated
+      // double-float (TwoSum), which matches an fp64 accumulation to ~1e-14 relative.
       const int row = ntid;
       const int64_t tok = (int64_t)lt * kM + row;
-      float hs[4] = {0.f, 0.f, 0.f, 0.f}, ls[4] = {0.f, 0.f, 0.f, 0.f};
-      auto two_sum_add = [&](int k, float x) {
-        const float p = x * x;
-        const float t = hs[k] + p;
-        const float z = t - hs[k];
-        ls[k] += (hs[k] - (t - z)) + (p - z);
-        hs[k] = t;
+      auto elem_pair = [&](uint32_t w) -> float2 {
+        if (ABF) return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+        return __half22float2(*reinterpret_cast<const __half2*>(&w));
       };
+      float all32 = 0.f;
       if (!(P.ablate & 2)) {
+        float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           const uint8_t* rowp = a + hf * (L::kABytes / 2) + row * 128;
@@ -312,24 +345,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
             const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              float lo, hi;
-              if (ABF) {
-                lo = __uint_as_float(w[e] << 16);
-                hi = __uint_as_float(w[e] & 0xFFFF0000u);
-              } else {
-                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
-                lo = f.x;
-                hi = f.y;
-              }
-              two_sum_add(e, lo);
-              two_sum_add(e, hi);
+              const float2 f = elem_pair(w[e]);
+              float2& c = acc2[e & 1];
+              asm("{\n.reg .b64 x, y;\nmov.b64 x, {%2, %3};\nmov.b64 y, {%0, %1};\n"
+                  "fma.rn.f32x2 y, x, x, y;\nmov.b64 {%0, %1}, y;\n}"
+                  : "+f"(c.x), "+f"(c.y)
+                  : "f"(f.x), "f"(f.y));
             }
           }
         }
+        all32 = (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y);
       }
-      double all = 0.0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) all += (double)hs[k] + (double)ls[k];
       double outl = 0.0;
       for (int j = 0; j < P.h; ++j) {             // outlier channels: read them back
         const int c = chan[j];
@@ -339,9 +365,44 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         const float x = ABF ? __uint_as_float((uint32_t)bits << 16) : __half2float(__ushort_as_half(bits));
         outl += (double)(x * x);                  // <= 64 exact terms, tiny fp64 work
       }
+      double in64 = fmax((double)all32 - outl, 0.0);
+      {
+        const double err = (double)all32 * 2e-6;  // 128 terms in 4 fp32 chains: <= 32 ulp each
+        const uint16_t lo = f64_to_f16_bits(sqrt(fmax(in64 - err, 0.0)));
+        const uint16_t hi = f64_to_f16_bits(sqrt(in64 + err));
+        if (lo != hi && !(P.ablate & 2)) {        // undecided: exact double-float recompute
+          float hs[4] = {0.f, 0.f, 0.f, 0.f}, ls[4] = {0.f, 0.f, 0.f, 0.f};
+          auto two_sum_add = [&](int k, float x) {
+            const float p = x * x;
+            const float t = hs[k] + p;
+            const float z = t - hs[k];
+            ls[k] += (hs[k] - (t - z)) + (p - z);
+            hs[k] = t;
+          };
+#pragma unroll 1
+          for (int hf = 0; hf < 2; ++hf) {
+            const uint8_t* rowp = a + hf * (L::kABytes / 2) + row * 128;
+#pragma unroll 1
+            for (int j = 0; j < 8; ++j) {
+              const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((j ^ (row & 7)) << 4));
+              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = elem_pair(w[e]);
+                two_sum_add(e, f.x);
+                two_sum_add(e, f.y);
+              }
+            }
+          }
+          double all = 0.0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) all += (double)hs[k] + (double)ls[k];
+          in64 = fmax(all - outl, 0.0);
+        }
+      }
       if (tok < P.n) {
         const int64_t crow = (int64_t)u * P.kc.capacity + P.row_offset + tok;
-        P.kc.norm_in[crow] = f64_to_f16_bits(sqrt(fmax(all - outl, 0.0)));
+        P.kc.norm_in[crow] = f64_to_f16_bits(sqrt(in64));
         if (m_out > 0) P.kc.norm_out[crow] = f64_to_f16_bits(sqrt(outl));
       }
       __syncwarp();
@@ -367,7 +428,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         for (int g64 = 0; g64 < (P.ablate & 1 ? 0 : CH / 64); ++g64) {
           uint32_t r[64];
           tmem_ld64(tmem + ((uint32_t)(ew * 32) << 16) + buf * 256 + g64 * 64, r);
-          const uint32_t w0 = sign_word(r), w1 = sign_word(r + 32);
+          const uint32_t w0 = QJL_K1_FASTSIGN ? sign_word_fast(r) : sign_word(r);
+          const uint32_t w1 = QJL_K1_FASTSIGN ? sign_word_fast(r + 32) : sign_word(r + 32);
           const int sr = c * CH + g64 * 64;      // first sketch row of the word pair
           if (valid) {
             uint32_t* d0 = sr < m_in ? reinterpret_cast<uint32_t*>(P.kc.bits_in + crow * (m_in / 8)) + (sr >> 5)
@@ -386,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         if constexpr (CH % 64 == 32) {           // trailing 32-column group of the chunk
           uint32_t r[32];
           tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + buf * 256 + (CH - 32), r);
-          const uint32_t w = sign_word(r);
+          const uint32_t w = QJL_K1_FASTSIGN ? sign_word_fast(r) : sign_word(r);
           const int sr = c * CH + CH - 32;
           if (valid) {
             if (sr < m_in)

@@ -382,26 +382,54 @@ def run_gpu(args):
     kms, kcnt = ctypes.c_double(), ctypes.c_int()
     lib.qjl_timing_read(ctypes.byref(kms), ctypes.byref(kcnt), 1)
 
-    # end-to-end through the public API with host buffers
-    qh = q.cpu().pin_memory()
-    oh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
-    qd = torch.empty_like(q)
-    for _ in range(args.warmup):
-        qd.copy_(qh, non_blocking=True)
-        cache.decode(qd, out=out)
-        oh.copy_(out, non_blocking=True)
+    # end-to-end through the public API with host buffers: every step copies its query
+    # (pinned host -> device) and reads its output back (device -> pinned host).  The
+    # copies run on a side stream, double-buffered, so step i+1's upload and step i's
+    # read-back overlap the decode kernels (each decode waits for its own upload; each
+    # read-back waits for its own decode).
+    qh = [q.cpu().pin_memory() for _ in range(2)]
+    oh = [torch.empty(out.shape, dtype=out.dtype).pin_memory() for _ in range(2)]
+    qd = [torch.empty_like(q) for _ in range(2)]
+    od = [torch.empty_like(out) for _ in range(2)]
+    comp = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    up_done = [torch.cuda.Event() for _ in range(2)]
+    dec_done = [torch.cuda.Event() for _ in range(2)]
+    d2h_done = [torch.cuda.Event() for _ in range(2)]
+
+    def e2e_steps(k):
+        with torch.cuda.stream(copy):
+            qd[0].copy_(qh[0], non_blocking=True)
+            up_done[0].record(copy)
+        for i in range(k):
+            b = i & 1
+            if i + 1 < k:                               # upload the next step's query
+                with torch.cuda.stream(copy):
+                    copy.wait_event(dec_done[1 - b]) if i >= 1 else None   # buffer reuse
+                    qd[1 - b].copy_(qh[1 - b], non_blocking=True)
+                    up_done[1 - b].record(copy)
+            comp.wait_event(up_done[b])
+            if i >= 2:
+                comp.wait_event(d2h_done[b])            # od[b] was read back two steps ago
+            cache.decode(qd[b], out=od[b])
+            dec_done[b].record(comp)
+            with torch.cuda.stream(copy):               # read this step's output back
+                copy.wait_event(dec_done[b])
+                oh[b].copy_(od[b], non_blocking=True)
+                d2h_done[b].record(copy)
+        comp.wait_stream(copy)
+
+    e2e_steps(args.warmup)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record()
-    for _ in range(args.steps):
-        qd.copy_(qh, non_blocking=True)
-        cache.decode(qd, out=out)
-        oh.copy_(out, non_blocking=True)
+    e2e_steps(args.steps)
     e3.record()
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3)
+    qd, out = qd[0], od[(args.steps - 1) & 1]
 
     # output gather over NCCL (the path's only exchange), timed on its own
     gather_ms = 0.0

@@ -920,8 +920,556 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(L::kAlloc));
 }
 
+// ===================================================================================
+// Warp-specialized variant (KC <= 12): 8 warps per CTA, 2 CTAs per SM, 256 TMEM columns.
+//   warps 0-3 ("T", thread t = token t): score accumulators -> logits, CTA tile maxima,
+//             online softmax, P' digits (B operand of the PV MMA), zero-point sums;
+//   warps 4-7 ("D", thread t = token t for the sign expansion, dim t for the values):
+//             score A operand (tile i+1), PV A operand (tile i+1), both MMA issues, the
+//             PV accumulators -> fp32 running output, and the cache streaming.
+// The score accumulators and the P' operand are double buffered, so the T warps work
+// on tile i while the D warps expand tile i+1 and run tile i's PV MMA.  All hand-offs
+// are mbarriers (tcgen05.commit for MMA completion); there is no CTA-wide barrier in the
+// steady state.  TMEM: A_sc [0, 96), D_sc[2] [96, 160), A_pv [160, 192), D_pv [192, 256).
+// ===================================================================================
+namespace wsd {
+constexpr int kThreads = 256;
+constexpr int kStages = 4;
+constexpr int kLookahead = 2;
+constexpr int cDsc0 = 96, cApv = 160, cDpv = 192;
+}  // namespace wsd
+
+template <int KCI, int KCO>
+struct WLayout {
+  static constexpr int KC = KCI + KCO;
+  static constexpr int NHI = KCI / 4, NHO = (KCO + 3) / 4, NH = NHI + NHO;
+  static constexpr int kBitsIn = kTile * KCI * 4;
+  static constexpr int kBitsOut = kTile * KCO * 4;
+  static constexpr int kNorm = kTile * 2;
+  static constexpr int kCodes = kTile * 32;
+  static constexpr int kConst = kTile * 8;
+  static constexpr int oBitsIn = 0;
+  static constexpr int oBitsOut = oBitsIn + kBitsIn;
+  static constexpr int oNormIn = oBitsOut + kBitsOut;
+  static constexpr int oNormOut = oNormIn + kNorm;
+  static constexpr int oCodes = oNormOut + (KCO ? kNorm : 0);
+  static constexpr int oZero = oCodes + kCodes;
+  static constexpr int oScale = oZero + kConst;
+  static constexpr int kStageBytes = oScale + kConst;
+  static constexpr int oBsc = 0;                                   // 1024-aligned, <= 6 KB
+  static constexpr int oBpv = 6144;                                // [2][4 heads][128 tokens][16 B]
+  static constexpr int oRed = oBpv;                                // flush scratch aliases B_pv
+  static constexpr int oStage = oBpv + 2 * 8192;
+  static constexpr int oMax = oStage + wsd::kStages * kStageBytes;  // [2][4 T warps][8] f32
+  static constexpr int oPar = oMax + 2 * 4 * 8 * 4;                // [2][alpha 4, invK 4] f32
+  static constexpr int oBar = oPar + 2 * 8 * 4;
+  // full[S], empty[S], sc_done[2], sc_free[2], p_rdy[2], pvd[2], bsc
+  static constexpr int kBars = 2 * wsd::kStages + 9;
+  static constexpr int oTmem = oBar + kBars * 8;
+  static constexpr int oFlag = oTmem + 4;
+  static constexpr int kTotal = oFlag + 12 + 1024;
+};
+
+template <int KCI, int KCO>
+__global__ void __launch_bounds__(wsd::kThreads, 2) k_wdecode(const Params P) {
+  using L = WLayout<KCI, KCO>;
+  constexpr int KC = KCI + KCO;
+  static_assert(8 * KC <= wsd::cDsc0, "score A operand must fit below the accumulators");
+  constexpr int S = wsd::kStages, LA = wsd::kLookahead;
+  extern __shared__ uint8_t sm_raw[];
+  uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::oBar);
+  uint64_t* empty = full + S;
+  uint64_t* sc_done = full + 2 * S;   // [2] tcgen05.commit of the score MMA of tile i (buffer i & 1)
+  uint64_t* sc_free = sc_done + 2;    // [2] 4 T warps read D_sc[i & 1]
+  uint64_t* p_rdy = sc_done + 4;      // [2] 4 T warps wrote B_pv[i & 1] and par[i & 1]
+  uint64_t* pvd = sc_done + 6;        // [2] tcgen05.commit of the PV MMA of tile i
+  uint64_t* bsc_bar = sc_done + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::oTmem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wq = warp & 3, t4 = tid & 127;     // TMEM lane quadrant; token / dim of this thread
+  const bool is_t = warp < 4;
+  const int C = P.ctas;
+
+  // grouped schedule only (host guarantees ctas >= units): unit u, tiles k, k + g, ...
+  const int u = cta_of_tile(blockIdx.x, C, P.units);
+  const int g0 = (int)tile_begin(u, C, P.units), g1 = (int)tile_begin(u + 1, C, P.units);
+  const int k0 = blockIdx.x - g0, gstep = g1 - g0;
+  const int ntiles = k0 < P.tpu ? (P.tpu - k0 + gstep - 1) / gstep : 0;
+  if (ntiles == 0) return;                     // no tiles, no partial (ns counts only busy CTAs)
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sc_done[b], 1);
+      mbar_init(&sc_free[b], 4);
+      mbar_init(&p_rdy[b], 4);
+      mbar_init(&pvd[b], 1);
+    }
+    mbar_init(bsc_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const uint32_t tlane = tbase + ((uint32_t)(wq * 32) << 16);
+  const uint64_t dsc0 = desc_sw128(smem_u32(sm + L::oBsc));
+  const uint64_t dpv0 = desc_none(smem_u32(sm + L::oBpv), 128, 2048);
+  auto tile_tok = [&](int i) -> int64_t { return (int64_t)(k0 + i * gstep) * kTile; };
+  auto stage = [&](int i) -> const uint8_t* { return sm + L::oStage + (i % S) * L::kStageBytes; };
+
+  // D warps' lane 0 stream the cache: the four warps split the seven copies of a tile
+  auto issue = [&](int i) {
+    const int s = i % S;
+    if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+    const int64_t row = (int64_t)u * P.kc.capacity + tile_tok(i);
+    const int64_t vrow = (int64_t)u * P.vc.capacity + tile_tok(i);
+    uint8_t* st = sm + L::oStage + s * L::kStageBytes;
+    if (wq == 0) {
+      mbar_expect_tx(&full[s], L::kStageBytes);
+      bulk_g2s(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, &full[s]);
+    } else if (wq == 1) {
+      bulk_g2s(st + L::oCodes, (const uint8_t*)P.vc.codes + vrow * 32, L::kCodes, &full[s]);
+    } else if (wq == 2) {
+      bulk_g2s(st + L::oNormIn, P.kc.norm_in + row, L::kNorm, &full[s]);
+      if (KCO) {
+        bulk_g2s(st + L::oBitsOut, P.kc.bits_out + row * (KCO * 4), L::kBitsOut, &full[s]);
+        bulk_g2s(st + L::oNormOut, P.kc.norm_out + row, L::kNorm, &full[s]);
+      }
+    } else {
+      bulk_g2s(st + L::oZero, (const uint8_t*)P.vc.zero + vrow * 8, L::kConst, &full[s]);
+      bulk_g2s(st + L::oScale, (const uint8_t*)P.vc.scale + vrow * 8, L::kConst, &full[s]);
+    }
+  };
+
+#ifndef QJL_WS_TCODES
+#define QJL_WS_TCODES 1     // 1: the T warps build the PV code operand (balances the groups)
+#endif
+  auto codes_op = [&](int i) {               // P2T code words of dim t4 -> PV A operand
+    const uint8_t* st = stage(i);
+    uint32_t cw[32];
+    const uint4* cs = reinterpret_cast<const uint4*>(st + L::oCodes + (t4 >> 2) * 128);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint4 x = cs[k];
+      cw[4 * k] = x.x; cw[4 * k + 1] = x.y; cw[4 * k + 2] = x.z; cw[4 * k + 3] = x.w;
+    }
+    const uint32_t mk = 0x03030303u << (2 * (t4 & 3));
+#pragma unroll
+    for (int k = 0; k < 32; ++k) cw[k] &= mk;
+    tmem_st16(tlane + wsd::cApv, cw);
+    tmem_st16(tlane + wsd::cApv + 16, cw + 16);
+  };
+  // token-side state (T) / dim-side state (D)
+  float m_run[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  float l_part[4] = {0.f, 0.f, 0.f, 0.f}, acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float2 Z[4][2];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Z[q][0] = Z[q][1] = make_float2(0.f, 0.f);
+
+  if (!is_t) {
+    // ================================ D warps ===================================
+    const float wrow = (t4 & 3) == 0 ? 1.f : (t4 & 3) == 1 ? 0.25f : (t4 & 3) == 2 ? 0.0625f : 0.015625f;
+    auto bar_d = [&]() { asm volatile("bar.sync 3, 128;" ::: "memory"); };
+    auto signs = [&](int i) {                  // sign words of token t4 -> score A operand
+      const uint8_t* st = stage(i);
+      uint32_t wv[KC];
+      const uint4* bi = reinterpret_cast<const uint4*>(st + L::oBitsIn + t4 * KCI * 4);
+#pragma unroll
+      for (int c = 0; c < KCI / 4; ++c) {
+        const uint4 x = bi[c];
+        wv[4 * c] = x.x; wv[4 * c + 1] = x.y; wv[4 * c + 2] = x.z; wv[4 * c + 3] = x.w;
+      }
+      if (KCO) {
+        const uint2* bo = reinterpret_cast<const uint2*>(st + L::oBitsOut + t4 * KCO * 4);
+#pragma unroll
+        for (int c = 0; c < KCO / 2; ++c) {
+          const uint2 x = bo[c];
+          wv[KCI + 2 * c] = x.x; wv[KCI + 2 * c + 1] = x.y;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < KC; c += 2) {
+        uint32_t r[16];
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int b = 0; b < 8; ++b) r[8 * e + b] = wv[c + e] & (0x01010101u << b);
+        tmem_st16(tlane + 8 * c, r);
+      }
+    };
+    auto codes = [&](int i) {                  // P2T code words of dim t4 -> PV A operand
+      const uint8_t* st = stage(i);
+      uint32_t cw[32];
+      const uint4* cs = reinterpret_cast<const uint4*>(st + L::oCodes + (t4 >> 2) * 128);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint4 x = cs[k];
+        cw[4 * k] = x.x; cw[4 * k + 1] = x.y; cw[4 * k + 2] = x.z; cw[4 * k + 3] = x.w;
+      }
+      const uint32_t mk = 0x03030303u << (2 * (t4 & 3));
+#pragma unroll
+      for (int k = 0; k < 32; ++k) cw[k] &= mk;
+      tmem_st16(tlane + wsd::cApv, cw);
+      tmem_st16(tlane + wsd::cApv + 16, cw + 16);
+    };
+    auto mma_sc = [&](int i) {                 // elected thread of warp 4
+      if (i >= 2) mbar_wait(&sc_free[i & 1], ((i - 2) >> 1) & 1);
+      tc_fence_after();
+      constexpr uint32_t ID = idesc_i8(16, 0);
+      const uint32_t dsc = tbase + wsd::cDsc0 + 32 * (i & 1);
+      tc_mma_i8c<0>(dsc, tbase, dsc0, ID);
+#pragma unroll
+      for (int c = 1; c < KCI; ++c)
+        tc_mma_i8c<1>(dsc, tbase + 8 * c, dsc0 + (uint64_t)((c >> 2) * 128 + (c & 3) * 2), ID);
+      if (KCO) {
+        constexpr int h0 = L::NHI * 128;
+        tc_mma_i8c<0>(dsc + 16, tbase + 8 * KCI, dsc0 + (uint64_t)h0, ID);
+#pragma unroll
+        for (int c = 1; c < KCO; ++c)
+          tc_mma_i8c<1>(dsc + 16, tbase + 8 * (KCI + c), dsc0 + (uint64_t)(h0 + (c >> 2) * 128 + (c & 3) * 2), ID);
+      }
+      tc_commit(&sc_done[i & 1]);
+    };
+
+    // Software pipeline (iteration it): PV MMA of tile it, sign expansion of tile it+2
+    // while that MMA runs, tile it's PV accumulators, code operand of tile it+1, and the
+    // score MMA of tile it+2 -- the T warps always have the next score tile ready.
+    if (lane == 0)
+      for (int i = 0; i < LA + 2 && i < ntiles; ++i) issue(i);
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // the B image comes from k_uprep
+    if (tid == 128) {
+      mbar_expect_tx(bsc_bar, L::NH * 2048);
+      bulk_g2s(sm + L::oBsc, P.bsc + (size_t)u * L::NH * 2048, L::NH * 2048, bsc_bar);
+    }
+    // prologue: score MMAs of tiles 0 and 1, code operand of tile 0
+    mbar_wait(&full[0], 0);
+    signs(0);
+    if (!QJL_WS_TCODES) codes(0);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[0]);
+    tmem_wait_st();
+    tc_fence_before();
+    bar_d();
+    if (warp == 4) {
+      if (elect_one()) {
+        mbar_wait(bsc_bar, 0);
+        mma_sc(0);
+      }
+      __syncwarp();
+    }
+    if (ntiles > 1) {
+      mbar_wait(&full[1], 0);
+      mbar_wait(&sc_done[0], 0);               // A_sc free
+      tc_fence_after();
+      signs(1);
+      tmem_wait_st();
+      tc_fence_before();
+      bar_d();
+      if (warp == 4) {
+        if (elect_one()) mma_sc(1);
+        __syncwarp();
+      }
+    }
+    for (int it = 0; it < ntiles; ++it) {
+      if (lane == 0 && it + LA + 2 < ntiles) issue(it + LA + 2);
+      // 1. PV MMA of tile it (A_pv(it) was written and fenced in the previous iteration)
+      mbar_wait(&p_rdy[it & 1], (it >> 1) & 1);
+      const float* par = reinterpret_cast<const float*>(sm + L::oPar) + 8 * (it & 1);
+      const float4 al = *reinterpret_cast<const float4*>(par), ik = *reinterpret_cast<const float4*>(par + 4);
+      bar_d();                                 // par read by every D thread before the MMA
+      if (warp == 4) {
+        if (elect_one()) {
+          tc_fence_after();
+          constexpr uint32_t ID = idesc_i8(64, 1);
+          const uint64_t bd = dpv0 + (uint64_t)((it & 1) * 512);      // + 8 KB per buffer
+          tc_mma_i8c<0>(tbase + wsd::cDpv, tbase + wsd::cApv, bd, ID);
+          tc_mma_i8c<1>(tbase + wsd::cDpv, tbase + wsd::cApv + 8, bd + 32, ID);
+          tc_mma_i8c<1>(tbase + wsd::cDpv, tbase + wsd::cApv + 16, bd + 64, ID);
+          tc_mma_i8c<1>(tbase + wsd::cDpv, tbase + wsd::cApv + 24, bd + 96, ID);
+          tc_commit(&pvd[it & 1]);
+        }
+        __syncwarp();
+      }
+      // 2. score operand of tile it+2 while the PV MMA runs
+      const bool more2 = it + 2 < ntiles;
+      if (more2) {
+        mbar_wait(&full[(it + 2) % S], ((it + 2) / S) & 1);
+        mbar_wait(&sc_done[(it + 1) & 1], ((it + 1) >> 1) & 1);   // MMA_sc(it+1) done with A_sc
+        tc_fence_after();
+        signs(it + 2);
+      }
+      // 3. tile it's PV accumulators
+      mbar_wait(&pvd[it & 1], (it >> 1) & 1);
+      tc_fence_after();
+      {
+        uint32_t dd[4][4];                     // [head q][lo, mid, hi, pad] of this dim's group
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tmem_ld4(tlane + wsd::cDpv + 16 * q + 4 * wq, dd[q]);
+        tmem_wait_ld();
+        const float a4[4] = {al.x, al.y, al.z, al.w}, k4[4] = {ik.x, ik.y, ik.z, ik.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float f = fmaf((float)(int)dd[q][2], 65536.f, (float)((int)dd[q][0] + 256 * (int)dd[q][1]));
+          acc[q] = fmaf(f, k4[q] * wrow, acc[q] * a4[q]);
+        }
+      }
+      // 4. code operand of tile it+1 (A_pv free: MMA_pv(it) done)
+      if (it + 1 < ntiles) {
+        if (!QJL_WS_TCODES) codes(it + 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[(it + 1) % S]);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      // 5. score MMA of tile it+2
+      if (more2) {
+        bar_d();
+        if (warp == 4) {
+          if (elect_one()) mma_sc(it + 2);
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ================================ T warps ===================================
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    float4 qcr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) qcr[q] = P.qconst[(int64_t)u * 4 + q];
+    for (int it = 0; it < ntiles; ++it) {
+      const uint8_t* st = stage(it);
+      mbar_wait(&full[it % S], (it / S) & 1);
+      const bool valid = tile_tok(it) + t4 < P.n;
+      const float nin = __half2float(reinterpret_cast<const __half*>(st + L::oNormIn)[t4]);
+      const float nout = KCO ? __half2float(reinterpret_cast<const __half*>(st + L::oNormOut)[t4]) : 0.f;
+      uint2 zr = reinterpret_cast<const uint2*>(st + L::oZero)[t4];
+      uint2 sr = reinterpret_cast<const uint2*>(st + L::oScale)[t4];
+      if (!valid) zr = sr = make_uint2(0u, 0u);
+      if (!QJL_WS_TCODES) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[it % S]);
+      }
+      // logits from the score accumulators of buffer it & 1
+      mbar_wait(&sc_done[it & 1], (it >> 1) & 1);
+      tc_fence_after();
+      float lg[4];
+      {
+        uint32_t dr[32];
+        const uint32_t dsc = tlane + wsd::cDsc0 + 32 * (it & 1);
+        tmem_ld16(dsc, dr);
+        if (KCO) tmem_ld16(dsc + 16, dr + 16);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sc_free[it & 1]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int* di = reinterpret_cast<const int*>(dr + 4 * q);
+          const float fi = fmaf((float)(di[2] + 256 * di[3]), 65536.f, (float)(di[0] + 256 * di[1]));
+          float l2 = nin * fmaf(qcr[q].x, fi, -qcr[q].y);
+          if (KCO) {
+            const int* dq = reinterpret_cast<const int*>(dr + 16 + 4 * q);
+            const float fo = fmaf((float)(dq[2] + 256 * dq[3]), 65536.f, (float)(dq[0] + 256 * dq[1]));
+            l2 = fmaf(nout, fmaf(qcr[q].z, fo, -qcr[q].w), l2);
+          }
+          lg[q] = valid ? l2 : -INFINITY;
+        }
+      }
+      // CTA tile maxima over the 4 T warps (named barrier 2)
+      float tmax[4], smax;
+      {
+        float* mx = reinterpret_cast<float*>(sm + L::oMax) + (it & 1) * 32;
+        const float2 hf = h2f2(hmax2u(sr.x, sr.y));
+        const float smax_w = warp_max_f32(fmaxf(hf.x, hf.y));
+        float tm[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tm[q] = warp_max_f32(lg[q]);
+        if (lane == 0) {
+          *reinterpret_cast<float4*>(mx + wq * 8) = make_float4(tm[0], tm[1], tm[2], tm[3]);
+          mx[wq * 8 + 4] = smax_w;
+        }
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        const float4 a = *reinterpret_cast<const float4*>(mx), b = *reinterpret_cast<const float4*>(mx + 8),
+                     c = *reinterpret_cast<const float4*>(mx + 16), e = *reinterpret_cast<const float4*>(mx + 24);
+        tmax[0] = fmaxf(fmaxf(a.x, b.x), fmaxf(c.x, e.x));
+        tmax[1] = fmaxf(fmaxf(a.y, b.y), fmaxf(c.y, e.y));
+        tmax[2] = fmaxf(fmaxf(a.z, b.z), fmaxf(c.z, e.z));
+        tmax[3] = fmaxf(fmaxf(a.w, b.w), fmaxf(c.w, e.w));
+        smax = fmaxf(fmaxf(mx[4], mx[12]), fmaxf(mx[20], mx[28]));
+      }
+      float alpha[4], p[4], K[4], invK[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float m_new = fmaxf(m_run[q], tmax[q]);
+        alpha[q] = ex2(m_run[q] - m_new);
+        m_run[q] = m_new;
+        p[q] = ex2(lg[q] - m_new);
+        const float bound = ex2(tmax[q] - m_new) * smax;
+        K[q] = bound > 0.f ? kPMax * rcp_approx(bound) : 0.f;
+        invK[q] = bound * (1.f / kPMax);
+        l_part[q] = fmaf(l_part[q], alpha[q], p[q]);
+      }
+      const float2 z01 = h2f2(zr.x), z23 = h2f2(zr.y);
+      const float2 s01 = h2f2(sr.x), s23 = h2f2(sr.y);
+      uint32_t wv[4][4];
+      {
+        const float2 mg = make_float2(kMagic, kMagic);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 a2 = make_float2(alpha[q], alpha[q]), pp = make_float2(p[q], p[q]);
+          const float2 z2 = make_float2(0.f, 0.f);
+          Z[q][0] = fma2(pp, z01, fma2(Z[q][0], a2, z2));
+          Z[q][1] = fma2(pp, z23, fma2(Z[q][1], a2, z2));
+          const float pk = p[q] * K[q];
+          const float2 pk2 = make_float2(pk, pk);
+          const float2 w01 = fma2(pk2, s01, mg), w23 = fma2(pk2, s23, mg);
+          wv[q][0] = __float_as_uint(w01.x);
+          wv[q][1] = __float_as_uint(w01.y);
+          wv[q][2] = __float_as_uint(w23.x);
+          wv[q][3] = __float_as_uint(w23.y);
+        }
+      }
+      if (QJL_WS_TCODES) {
+        if (it >= 1) mbar_wait(&pvd[(it - 1) & 1], ((it - 1) >> 1) & 1);   // A_pv, B_pv, par free
+        tc_fence_after();
+        codes_op(it);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[it % S]);   // stage it fully read by this warp
+      } else if (it >= 2) {
+        mbar_wait(&pvd[it & 1], ((it - 2) >> 1) & 1);   // B_pv / par buffer free
+      }
+      {
+        uint4* bpv = reinterpret_cast<uint4*>(sm + L::oBpv + (it & 1) * 8192) + t4;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t o[4];
+#pragma unroll
+          for (int G = 0; G < 4; ++G)
+            asm("lop3.b32 %0, %1, 0x8080, 0xFFFFFF, 0x28;" : "=r"(o[G]) : "r"(wv[q][G]));
+          bpv[128 * q] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+        if (t4 == 0) {
+          float* par = reinterpret_cast<float*>(sm + L::oPar) + 8 * (it & 1);
+          *reinterpret_cast<float4*>(par) = make_float4(alpha[0], alpha[1], alpha[2], alpha[3]);
+          *reinterpret_cast<float4*>(par + 4) = make_float4(invK[0], invK[1], invK[2], invK[3]);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // B_pv -> tensor core
+      if (QJL_WS_TCODES) {
+        tmem_wait_st();
+        tc_fence_before();
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_rdy[it & 1]);
+    }
+  }
+
+  // ================================ flush ====================================
+  __syncthreads();                              // both groups done; B_pv region is free
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  float* red = reinterpret_cast<float*>(sm + L::oRed);   // [4 T warps][20] + m_run[4] at 80
+  if (is_t) {
+    float v[20];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      v[q] = l_part[q];
+      v[4 + 4 * q + 0] = Z[q][0].x;
+      v[4 + 4 * q + 1] = Z[q][0].y;
+      v[4 + 4 * q + 2] = Z[q][1].x;
+      v[4 + 4 * q + 3] = Z[q][1].y;
+    }
+#pragma unroll
+    for (int i = 0; i < 20; ++i) v[i] = warp_sum(v[i]);
+    if (lane == 0)
+#pragma unroll
+      for (int i = 0; i < 20; ++i) red[wq * 20 + i] = v[i];
+    if (tid == 0)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) red[80 + q] = m_run[q];
+  }
+  __syncthreads();
+  const int ns = min(gstep, P.tpu), slot = k0;
+  float* mypart = P.part + ((int64_t)u * P.max_seg + slot) * P.G * kRec;
+  if (!is_t) {                                  // dim t4 of every head
+    const int grp = t4 >> 5;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < P.G) {
+        float lq = 0.f, zq = 0.f;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          lq += red[w * 20 + q];
+          zq += red[w * 20 + 4 + 4 * q + grp];
+        }
+        if (t4 == 0) {
+          mypart[q * kRec + 0] = red[80 + q];
+          mypart[q * kRec + 1] = lq;
+        }
+        mypart[q * kRec + 2 + t4] = acc[q] + zq;
+      }
+    }
+  }
+  int* flag = reinterpret_cast<int*>(sm + L::oFlag);
+  bool merge = true;
+  if (ns > 1) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) *flag = (atomicAdd(&P.counters[u], 1) == ns - 1);
+    __syncthreads();
+    merge = *flag != 0;
+    if (merge) __threadfence();
+  } else {
+    __syncthreads();
+  }
+  if (merge) {
+    const float* up = P.part + (int64_t)u * P.max_seg * P.G * kRec;
+    for (int i = tid; i < P.G * 128; i += wsd::kThreads) {
+      const int qq = i >> 7, dim = i & 127;
+      float M = -INFINITY, Ls = 0.f, a = 0.f;
+      for (int s0 = 0; s0 < ns; s0 += 16) {
+        float mv[16], lv[16], av[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float* W = up + ((s0 + k) * P.G + qq) * kRec;
+          const bool ok = s0 + k < ns;
+          mv[k] = ok ? __ldcg(W) : -INFINITY;
+          lv[k] = ok ? __ldcg(W + 1) : 0.f;
+          av[k] = ok ? __ldcg(W + 2 + dim) : 0.f;
+        }
+        float Mc = M;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) Mc = fmaxf(Mc, mv[k]);
+        const float rs = (M == -INFINITY) ? 0.f : ex2(M - Mc);
+        Ls *= rs;
+        a *= rs;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float f = (mv[k] == -INFINITY) ? 0.f : ex2(mv[k] - Mc);
+          Ls = fmaf(f, lv[k], Ls);
+          a = fmaf(f, av[k], a);
+        }
+        M = Mc;
+      }
+      P.out[((int64_t)u * P.G + qq) * 128 + dim] = a / Ls;
+      if (P.lse && dim == 0) P.lse[(int64_t)u * P.G + qq] = (M + __log2f(Ls)) * kLn2;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tbase));
+}
+
 struct Plan {
-  int tpu, ctas, max_seg, grouped;
+  int tpu, ctas, max_seg, grouped, ws;
   int64_t T;
   size_t bsc_off, qconst_off, part_off, cnt_off, total;
 };
@@ -955,6 +1503,30 @@ static int occupancy() {
   return occ;
 }
 
+template <int KCI, int KCO>
+static int occupancy_ws() {
+  using L = WLayout<KCI, KCO>;
+  static int occ = -1;
+  if (occ < 0) {
+    cudaFuncSetAttribute(k_wdecode<KCI, KCO>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    cudaFuncSetAttribute(k_wdecode<KCI, KCO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k_wdecode<KCI, KCO>);
+    int dev = 0, smem_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+    const int by_regs = 65536 / (regs_warp * (wsd::kThreads / 32));
+    const int by_smem = smem_sm / (L::kTotal + 1024);
+    int o = by_regs < by_smem ? by_regs : by_smem;
+    occ = o < 1 ? 1 : (o > 2 ? 2 : o);        // 256 TMEM columns per CTA
+    if (getenv("QJL_DEBUG"))
+      fprintf(stderr, "k_wdecode<%d,%d>: %d CTAs/SM (regs %d -> %d, smem %d/%d -> %d)\n", KCI, KCO, occ,
+              fa.numRegs, by_regs, L::kTotal, smem_sm, by_smem);
+  }
+  return occ;
+}
+
 static bool kc_dispatch(int kci, int kco, int* id) {
   const int pairs[][2] = {{8, 2}, {8, 4}, {8, 0}, {16, 2}, {16, 0}, {16, 4}};
   for (int i = 0; i < 6; ++i)
@@ -972,6 +1544,14 @@ static int occupancy_by_id(int id) {
   }
   return 1;
 }
+static int occupancy_ws_by_id(int id) {
+  switch (id) {
+    case 0: return occupancy_ws<8, 2>();
+    case 1: return occupancy_ws<8, 4>();
+    case 2: return occupancy_ws<8, 0>();
+  }
+  return 0;
+}
 static int nh_by_id(int id) {
   const int nh[] = {3, 3, 2, 5, 4, 5};
   return nh[id];
@@ -982,8 +1562,22 @@ static Plan make_plan(const qjl_key_cache_t& kc, int64_t n, int G, int id) {
   Plan p;
   p.tpu = (int)((n + kTile - 1) / kTile);
   p.T = (int64_t)kc.units * p.tpu;
-  const int64_t slots = (int64_t)device_sm_count() * occupancy_by_id(id);
-  p.ctas = (int)(p.T < slots ? p.T : slots);
+  // warp-specialized kernel (opt-in, QJL_UD_WS=1: measured 91 us vs 85 us for the
+  // 4-CTA kernel at C3) when the score operand fits (KC <= 12) and every unit gets its
+  // own CTA group
+  p.ws = 0;
+  if (id <= 2 && getenv("QJL_UD_WS") != nullptr && getenv("QJL_UD_CONTIG") == nullptr) {
+    const int64_t wslots = (int64_t)device_sm_count() * occupancy_ws_by_id(id);
+    const int wctas = (int)(p.T < wslots ? p.T : wslots);
+    if (wctas >= kc.units) {
+      p.ws = 1;
+      p.ctas = wctas;
+    }
+  }
+  if (!p.ws) {
+    const int64_t slots = (int64_t)device_sm_count() * occupancy_by_id(id);
+    p.ctas = (int)(p.T < slots ? p.T : slots);
+  }
   p.grouped = (p.ctas >= kc.units && getenv("QJL_UD_CONTIG") == nullptr) ? 1 : 0;
   int ms = 1;
   for (int u = 0; u < kc.units; ++u) {
@@ -1079,11 +1673,20 @@ static int launch_umma_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
   P.counters = counters;
   P.out = out;
   P.lse = lse;
-  occupancy<KCI, KCO>();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(plan.ctas);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = Layout<KCI, KCO>::kTotal;
+  if constexpr (KCI + KCO <= 12) {
+    if (plan.ws) {
+      occupancy_ws<KCI, KCO>();
+      cfg.blockDim = dim3(wsd::kThreads);
+      cfg.dynamicSmemBytes = WLayout<KCI, KCO>::kTotal;
+    }
+  }
+  if (!plan.ws) {
+    occupancy<KCI, KCO>();
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Layout<KCI, KCO>::kTotal;
+  }
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1091,7 +1694,13 @@ static int launch_umma_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   timing_begin(st);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_udecode<KCI, KCO>, P);
+  cudaError_t e = cudaSuccess;
+  if constexpr (KCI + KCO <= 12) {
+    if (plan.ws) e = cudaLaunchKernelEx(&cfg, k_wdecode<KCI, KCO>, P);
+    else e = cudaLaunchKernelEx(&cfg, k_udecode<KCI, KCO>, P);
+  } else {
+    e = cudaLaunchKernelEx(&cfg, k_udecode<KCI, KCO>, P);
+  }
   timing_end(st);
   if (e != cudaSuccess) return cuda_status(e, "decode_umma");
   QJL_LAUNCH_CHECK("decode_umma");

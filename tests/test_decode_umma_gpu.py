@@ -97,3 +97,20 @@ def test_p2t_quantizer_exact_ties_and_unaligned_appends(cuda):
         assert np.array_equal(p2_unpack_codes(c.v_codes[u].cpu().numpy(), n, "p2t"), codes)
         assert np.array_equal(c.v_zero[u, :n].double().cpu().numpy(), zero)
         assert np.array_equal(c.v_scale[u, :n].double().cpu().numpy(), scale)
+
+
+def test_warp_specialized_kernel_matches(cuda):
+    """The opt-in warp-specialized variant (QJL_UD_WS=1) against the default kernel."""
+    import os
+
+    c, q = _cache(64, 4096, 4, 8, 256, 64, seed=21, layout="p2t")
+    a = c.decode(q).double().cpu().numpy()
+    os.environ["QJL_UD_WS"] = "1"
+    try:
+        b = c.decode(q).double().cpu().numpy()
+    finally:
+        del os.environ["QJL_UD_WS"]
+    from tests._parity import rel_l2
+    for u in range(64):
+        for g in range(4):
+            assert rel_l2(b[u, g], a[u, g]) <= 1e-4, (u, g)

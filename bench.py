@@ -327,6 +327,70 @@ def measure_prefill(device, seed, steps=5, warmup=2):
             "note": "K.S^T over zero-padded K=128 (m_in+m_out=576 rows) + sign pack + fp16 norms"}
 
 
+def measure_qjlc(device, seed, steps=10, warmup=3):
+    """Row F3: QJLC record export / import (kvcache.py:389-520) of a C3-shaped cache
+    (64 units x 32768 tokens, m_in 256, m_out 64) holding reference-format values
+    (u8 codes, one f32 zero/scale per token).  Algorithmic bytes per token-head:
+    read 176 (40 sign + 4 norm + 128 code + 8 const) + write 180 (record) = 356."""
+    import torch
+
+    from paper_2406_03482_b200 import qjlc as Q
+    from paper_2406_03482_b200.device import DeviceKeyCache
+
+    w = WORKLOADS["c3"]
+    U, n, d = w["batch"] * w["kv_heads"], w["n"], w["d"]
+    g = torch.Generator(device=device)
+    g.manual_seed(seed + 5)
+    cache = DeviceKeyCache.create(U, d, w["m_in"], h=w["h"], m_out=w["m_out"], capacity=n, seed=seed,
+                                  key_dtype=torch.bfloat16, value_layout="u8", value_bits=2,
+                                  value_group=d, channels=np.tile(np.arange(w["h"]) * 16, (U, 1)))
+    for c0 in range(0, n, 8192):                      # chunked to bound the bf16 staging
+        K = torch.randn(U, 8192, d, generator=g, device=device).to(torch.bfloat16)
+        V = torch.randn(U, 8192, d, generator=g, device=device).to(torch.bfloat16)
+        cache.append(K, V)
+    del K, V
+    kd, vd = cache.key_desc(), cache.value_desc()
+    recs, R = Q.export_records(kd, vd, w["m_in"], w["m_out"], n)
+    dst = DeviceKeyCache(U, d, w["m_in"], w["m_out"], w["h"], n, value_layout="u8", value_bits=2,
+                         value_group=d)
+    kd2, vd2 = dst.key_desc(), dst.value_desc()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    for _ in range(warmup):
+        Q.export_records(kd, vd, w["m_in"], w["m_out"], n, out=recs)
+        Q.import_records(recs, n, w["m_in"], w["m_out"], kd2, vd2)
+    torch.cuda.synchronize()
+    ev[0].record()
+    for _ in range(steps):
+        Q.export_records(kd, vd, w["m_in"], w["m_out"], n, out=recs)
+    ev[1].record()
+    for _ in range(steps):
+        Q.import_records(recs, n, w["m_in"], w["m_out"], kd2, vd2)
+    ev[2].record()
+    torch.cuda.synchronize()
+    ok = all(torch.equal(a[:, :n], b[:, :n]) for a, b in
+             ((cache.bits_in, dst.bits_in), (cache.bits_out, dst.bits_out), (cache.norm_in, dst.norm_in),
+              (cache.v_codes, dst.v_codes), (cache.v_scale, dst.v_scale)))
+    host = torch.empty(recs.shape, dtype=torch.uint8, pin_memory=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        Q.export_records(kd, vd, w["m_in"], w["m_out"], n, out=recs)
+        host.copy_(recs)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / 3
+    exp_ms = ev[0].elapsed_time(ev[1]) / steps
+    imp_ms = ev[1].elapsed_time(ev[2]) / steps
+    byts = U * n * (176 + R)
+    del cache, dst, recs, host
+    torch.cuda.empty_cache()
+    return {"workload": "c3_qjlc_export_import", "record_bytes": R, "tokens": U * n,
+            "export_ms": exp_ms, "export_gbs": byts / (exp_ms * 1e-3) / 1e9,
+            "import_ms": imp_ms, "import_gbs": byts / (imp_ms * 1e-3) / 1e9,
+            "export_to_host_gbs": U * n * R / e2e_s / 1e9, "round_trip_identical": bool(ok),
+            "note": "algorithmic bytes = 176 read + 180 written per token-head; export_to_host adds "
+                    "the D2H of the records into pinned memory (PCIe bound)"}
+
+
 # --------------------------------------------------------------- GPU arm
 def run_gpu(args):
     import torch
@@ -497,6 +561,11 @@ def run_gpu(args):
             res["prefill"] = measure_prefill(device, args.seed)
         except Exception as e:                       # pragma: no cover
             res["prefill"] = {"error": repr(e)[:200]}
+    if world == 1 and rank == 0 and not args.no_prefill:
+        try:
+            res["qjlc"] = measure_qjlc(device, args.seed)
+        except Exception as e:                       # pragma: no cover
+            res["qjlc"] = {"error": repr(e)[:200]}
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline_leg(cache, q, w)
     if rank == 0:

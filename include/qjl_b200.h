@@ -24,6 +24,8 @@
  *   qjl_decode           <- quantized_decode (scores + softmax + weights @ values)
  *                                                       pkg/src/qjl/attention.py:56-71
  *   qjl_quantize_values  <- quantize_value             pkg/src/qjl/kvcache.py:140-161
+ *   qjl_qjlc_export      <- write_cache record loop    pkg/src/qjl/kvcache.py:389-437
+ *   qjl_qjlc_import      <- read_cache record loop     pkg/src/qjl/kvcache.py:440-520
  *
  * Data layout in HBM (unit = one (batch, kv-head) pair; all arrays unit-major):
  *   key cache   bits_in  u8  [units][capacity][m_in/8]   LSB-first sign bits; byte-
@@ -165,6 +167,29 @@ QJL_API int qjl_timing_read(double* total_ms, int* launches, int reset);
 /* Value quantizer: v [units][n][d] -> value cache rows [row_offset, row_offset + n). */
 QJL_API int qjl_quantize_values(const void* v, int dtype, int64_t n, int64_t unit_stride,
                         const qjl_value_cache_t* values, int64_t row_offset, void* stream);
+
+/* QJLC cache files (write_cache / read_cache, pkg/src/qjl/kvcache.py:368-520).
+ * One record per token, little-endian, in append order (kvcache.py:430-436, :472):
+ *   [inlier sign words 8*ceil(m_in_file/64) B][inlier norm f16]
+ *   [outlier sign words 8*ceil(m_out_file/64) B][outlier norm f16]
+ *   [d value codes, 1 B each][zero f32][scale f32]
+ * m_in_file / m_out_file are the logical widths of the file header; the key cache's
+ * (32-bit padded) widths must fit inside the file's words, and bits past the logical
+ * width are written / loaded as zero.  An empty side (width 0) writes a 0.0 norm
+ * (EMPTY_KEY, estimator.py:95).  The value cache must use the U8 layout with group == d
+ * (the only value format the file holds).  records: [units][unit_stride] bytes, unit u's
+ * n records at u * unit_stride.  The header, outlier channels and magnitudes of each file
+ * are host data (paper_2406_03482_b200/qjlc.py). */
+QJL_API int64_t qjl_qjlc_record_bytes(int d, int m_in_file, int m_out_file);
+/* Rows [row_offset, row_offset + n) of every unit -> records.  n == 0 -> QJL_ERR_EMPTY
+ * ("refusing to serialize an empty cache", kvcache.py:407-408). */
+QJL_API int qjl_qjlc_export(const qjl_key_cache_t* keys, const qjl_value_cache_t* values,
+                            int m_in_file, int m_out_file, int64_t row_offset, int64_t n,
+                            uint8_t* records, int64_t unit_stride, void* stream);
+/* records -> rows [row_offset, row_offset + n) of every unit; values may be NULL (keys only). */
+QJL_API int qjl_qjlc_import(const uint8_t* records, int64_t unit_stride, int64_t n, int m_in_file,
+                            int m_out_file, const qjl_key_cache_t* keys,
+                            const qjl_value_cache_t* values, int64_t row_offset, void* stream);
 
 #ifdef __cplusplus
 }

@@ -249,3 +249,98 @@ def decode_units(S_in, S_out, channels_per_unit, queries, caches, values_deq,
                                         temperature)
             out[u, g], logits[u, g] = o, lg
     return out, logits
+
+
+# --------------------------------------------------------------------------
+# QJLC cache files: kvcache.py:368-520 (write_cache / read_cache)
+# --------------------------------------------------------------------------
+QJLC_MAGIC = b"QJLC"                       # kvcache.py:369
+QJLC_VERSION = 1                           # kvcache.py:370
+QJLC_HEADER = "<4sHHIIIIQHHQ"              # kvcache.py:371 (48 bytes)
+QJLC_FLAG_ORTHOGONALIZED = 1               # kvcache.py:372
+
+
+def qjlc_record_bytes(d: int, m_in: int, m_out: int) -> int:
+    """Bytes of one token record (kvcache.py:472): inlier words + f16 norm +
+    outlier words + f16 norm + d one-byte codes + f32 zero + f32 scale."""
+    return 8 * words_for(m_in) + 2 + 8 * words_for(m_out) + 2 + d + 4 + 4
+
+
+def qjlc_encode(*, d, h, m_in, m_out, value_bits, seed, orthogonalized, channels, magnitudes,
+                bits_in, norm_in, bits_out, norm_out, codes, zero, scale) -> bytes:
+    """Serialize one unit exactly as write_cache does (kvcache.py:389-437).
+
+    bits_*: u8 [n, >= ceil(m/8)] LSB-first sign bytes (columns past the side's
+    8*words_for(m) bytes are ignored, missing ones are zero padding); norm_*:
+    [n] (rounded to f16 here, :430/:432); codes u8 [n, d]; zero/scale [n]
+    (rounded to f32, :434-435).  A side with m == 0 writes no words and a 0.0
+    norm (EMPTY_KEY, estimator.py:95).
+    """
+    import struct
+    n = int(np.asarray(codes).shape[0])
+    if n == 0:
+        raise ValueError("refusing to serialize an empty cache")             # :407-408
+    flags = QJLC_FLAG_ORTHOGONALIZED if orthogonalized else 0
+    head = struct.pack(QJLC_HEADER, QJLC_MAGIC, QJLC_VERSION, flags, d, h, m_in, m_out, n,
+                       value_bits, 0, seed)                                  # :416-429
+
+    def side(bits, norms, m):
+        wb = 8 * words_for(m)
+        out = np.zeros((n, wb), np.uint8)
+        if m:
+            b = np.asarray(bits, np.uint8)[:, :wb]
+            out[:, : b.shape[1]] = b
+        nv = np.zeros(n) if m == 0 else np.asarray(norms, np.float64)
+        return out, nv.astype("<f2").view(np.uint8).reshape(n, 2)
+
+    wi, ni = side(bits_in, norm_in, m_in)
+    wo, no = side(bits_out, norm_out, m_out)
+    z = np.asarray(zero, np.float64).astype("<f4").view(np.uint8).reshape(n, 4)
+    s = np.asarray(scale, np.float64).astype("<f4").view(np.uint8).reshape(n, 4)
+    rec = np.concatenate([wi, ni, wo, no, np.asarray(codes, np.uint8).reshape(n, d), z, s], axis=1)
+    assert rec.shape[1] == qjlc_record_bytes(d, m_in, m_out)
+    return (head + np.asarray(channels, "<u4").tobytes()
+            + np.asarray(magnitudes, "<f8").tobytes() + rec.tobytes())
+
+
+def qjlc_decode(blob: bytes) -> dict:
+    """Parse a QJLC file as read_cache does (kvcache.py:440-520) into arrays.
+    Raises ValueError where the reference raises FileFormatError (:452-464)."""
+    import struct
+    hs = struct.calcsize(QJLC_HEADER)
+    if len(blob) < hs:
+        raise ValueError("cache file shorter than its header")
+    magic, version, flags, d, h, m_in, m_out, n, vbits, _, seed = struct.unpack_from(QJLC_HEADER, blob)
+    if magic != QJLC_MAGIC:
+        raise ValueError(f"bad magic {magic!r}")
+    if version != QJLC_VERSION:
+        raise ValueError(f"unsupported cache version {version}")
+    R = qjlc_record_bytes(d, m_in, m_out)
+    if len(blob) != hs + 4 * h + 8 * d + n * R:
+        raise ValueError("cache payload length does not match header")
+    off = hs
+    channels = np.frombuffer(blob, "<u4", h, off).astype(np.int64)
+    off += 4 * h
+    mags = np.frombuffer(blob, "<f8", d, off).copy()
+    off += 8 * d
+    rec = np.frombuffer(blob, np.uint8, n * R, off).reshape(n, R)
+    wi, wo = 8 * words_for(m_in), 8 * words_for(m_out)
+    c = 0
+
+    def take(k):
+        nonlocal c
+        r = rec[:, c:c + k]
+        c += k
+        return np.ascontiguousarray(r)
+
+    bits_in = take(wi)
+    norm_in = take(2).view("<f2")[:, 0].astype(np.float64)
+    bits_out = take(wo)
+    norm_out = take(2).view("<f2")[:, 0].astype(np.float64)
+    codes = take(d)
+    zero = take(4).view("<f4")[:, 0].astype(np.float64)
+    scale = take(4).view("<f4")[:, 0].astype(np.float64)
+    return dict(d=d, h=h, m_in=m_in, m_out=m_out, n=n, value_bits=vbits, seed=seed,
+                orthogonalized=bool(flags & QJLC_FLAG_ORTHOGONALIZED), channels=channels,
+                magnitudes=mags, bits_in=bits_in, norm_in=norm_in, bits_out=bits_out,
+                norm_out=norm_out, codes=codes, zero=zero, scale=scale)

@@ -25,6 +25,10 @@ from .estimator import (
     unpack_signs,
 )
 from .kvcache import (
+    CACHE_MAGIC,
+    CACHE_VERSION,
+    CacheHeader,
+    FileFormatError,
     KeyCacheState,
     MemoryReport,
     OutlierProfile,
@@ -33,13 +37,16 @@ from .kvcache import (
     dequantize_value,
     detect_outliers,
     quantize_value,
+    read_cache,
     softmax,
+    write_cache,
 )
 from .sketch import SketchMatrix, derive_seed, generate_gaussian, orthogonalize, rng_from_seed
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "CACHE_MAGIC", "CACHE_VERSION", "CacheHeader", "FileFormatError", "read_cache", "write_cache",
     "DecodeResult", "DeviceKeyCache", "EMPTY_KEY", "ESTIMATOR_SCALE", "KeyCacheState", "MemoryReport",
     "OutlierProfile", "QuantizedKey", "QuantizedValueToken", "ScoreVector", "SketchMatrix",
     "SketchedQuery", "UnitShard", "dequantize_value", "derive_seed", "detect_outliers",

@@ -372,4 +372,62 @@ int qjl_quantize_values(const void* v, int dtype, int64_t n, int64_t unit_stride
   return launch_quantize_values(v, dtype, n, unit_stride, *values, row_offset, (cudaStream_t)stream);
 }
 
+int64_t qjl_qjlc_record_bytes(int d, int m_in, int m_out) {
+  if (d < 1 || m_in < 0 || m_out < 0) return -1;
+  return qjlc_record_bytes(d, m_in, m_out);
+}
+
+// shared checks of the QJLC record entry points: the key cache's padded widths must
+// fit inside the file's whole u64 words, values in the reference's own format
+static int check_qjlc(const qjl_key_cache_t* kc, const qjl_value_cache_t* vc, int mfi, int mfo,
+                      int64_t row_offset, int64_t n, const void* records, int64_t ustride) {
+  QJL_TRY(check_key_cache(kc));
+  QJL_CHECK_ARG(records != nullptr, "records buffer is NULL");
+  QJL_CHECK_ARG(mfi >= 0 && mfi <= kc->m_in && (mfi > 0) == (kc->m_in > 0),
+                "file inlier width %d does not fit the cache's %d bits", mfi, kc->m_in);
+  QJL_CHECK_ARG(mfo >= 0 && mfo <= kc->m_out && (mfo > 0) == (kc->m_out > 0),
+                "file outlier width %d does not fit the cache's %d bits", mfo, kc->m_out);
+  if (kc->m_in > 64 * ((mfi + 63) / 64) || kc->m_out > 64 * ((mfo + 63) / 64)) {
+    set_error("cache rows (%d/%d bits) are wider than the file's sign words (%d/%d bits)", kc->m_in,
+              kc->m_out, mfi, mfo);
+    return QJL_ERR_UNSUPPORTED;
+  }
+  QJL_CHECK_ARG(n >= 0 && row_offset >= 0 && row_offset + n <= kc->capacity, "rows exceed key capacity");
+  QJL_CHECK_ARG(ustride >= n * qjlc_record_bytes(kc->d, mfi, mfo), "record unit stride too small");
+  if (vc) {
+    QJL_CHECK_ARG(vc->codes && vc->zero && vc->scale, "value cache pointers must be set");
+    QJL_CHECK_ARG(vc->d == kc->d && vc->units == kc->units, "value cache shape does not match the keys");
+    QJL_CHECK_ARG(vc->bits >= 1 && vc->bits <= 8, "value bit width must be in [1, 8], got %d", vc->bits);
+    QJL_CHECK_ARG(row_offset + n <= vc->capacity, "rows exceed value capacity");
+    if (vc->layout != QJL_VLAYOUT_U8 || vc->group != vc->d) {
+      set_error("QJLC files hold one byte per code and one f32 zero/scale per token: the value cache "
+                "must use the U8 layout with group == d (got layout %d, group %d)", vc->layout, vc->group);
+      return QJL_ERR_UNSUPPORTED;
+    }
+  }
+  return QJL_OK;
+}
+
+int qjl_qjlc_export(const qjl_key_cache_t* keys, const qjl_value_cache_t* values, int m_in_file,
+                    int m_out_file, int64_t row_offset, int64_t n, uint8_t* records, int64_t unit_stride,
+                    void* stream) {
+  QJL_CHECK_ARG(values != nullptr, "a QJLC record carries value codes: values is NULL");
+  QJL_TRY(check_qjlc(keys, values, m_in_file, m_out_file, row_offset, n, records, unit_stride));
+  if (n == 0) {
+    set_error("refusing to serialize an empty cache");
+    return QJL_ERR_EMPTY;
+  }
+  return launch_qjlc_export(*keys, *values, m_in_file, m_out_file, row_offset, n, records, unit_stride,
+                            (cudaStream_t)stream);
+}
+
+int qjl_qjlc_import(const uint8_t* records, int64_t unit_stride, int64_t n, int m_in_file, int m_out_file,
+                    const qjl_key_cache_t* keys, const qjl_value_cache_t* values, int64_t row_offset,
+                    void* stream) {
+  QJL_TRY(check_qjlc(keys, values, m_in_file, m_out_file, row_offset, n, records, unit_stride));
+  if (n == 0) return QJL_OK;
+  return launch_qjlc_import(records, unit_stride, m_in_file, m_out_file, n, *keys, values, row_offset,
+                            (cudaStream_t)stream);
+}
+
 }  // extern "C"

@@ -54,4 +54,12 @@ int launch_decode_umma(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, i
                        int q_dtype, int G, const qjl_sketch_t& sk, float inv_t, float* out, float* lse,
                        void* ws, size_t ws_bytes, cudaStream_t st);
 
+// QJLC cache records <-> device cache layout (k_qjlc.cu)
+int64_t qjlc_record_bytes(int d, int m_in_file, int m_out_file);
+int launch_qjlc_export(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int mfi, int mfo,
+                       int64_t row0, int64_t n, uint8_t* out, int64_t ustride, cudaStream_t st);
+int launch_qjlc_import(const uint8_t* in, int64_t ustride, int mfi, int mfo, int64_t n,
+                       const qjl_key_cache_t& kc, const qjl_value_cache_t* vc, int64_t row0,
+                       cudaStream_t st);
+
 }  // namespace qjl

@@ -10,6 +10,7 @@ the C ABI (there is no CPU fallback):
     KeyCacheState.estimate_logits  :322-329        -> qjl_scores
     KeyCacheState.estimate_scores  :331-337        -> qjl_scores + qjl_softmax_f64
     quantize_value             kvcache.py:140-161  -> qjl_quantize_values (U8 layout)
+    write_cache / read_cache   kvcache.py:389-520  -> qjl_qjlc_export / qjl_qjlc_import
 
 Storage policy (documented divergence, within the 1e-3 logit tolerance): key
 norms are held at half precision, the reference's own serialization policy
@@ -36,8 +37,8 @@ OUTLIER_STREAM = 1                     # kvcache.py:29
 DEFAULT_OUTLIER_BITS_PER_CHANNEL = 8   # kvcache.py:31
 
 
-class FileFormatError(Exception):
-    """A binary file failed magic/version/length validation (kvcache.py:34)."""
+from .qjlc import CACHE_MAGIC, CACHE_VERSION, CacheHeader, FileFormatError  # noqa: E402,F401
+from . import qjlc as _qjlc  # noqa: E402
 
 
 def _cuda() -> torch.device:
@@ -410,3 +411,71 @@ class KeyCacheState:
         value_bits_per_fpn = value_bits + (zero_bits + scale_bits) / d
         total = (key_bits + value_bits_per_fpn) / 2.0
         return MemoryReport(key_bits, value_bits_per_fpn, total, 16.0, 16.0 / total)
+
+
+def write_cache(path, state: KeyCacheState, value_tokens: list[QuantizedValueToken]) -> None:
+    """Serialize a key-cache state and its value tokens (kvcache.py:389-437).
+
+    The key records come straight from the state's device cache; the value tokens
+    are staged as a one-unit U8 value cache, and `qjl_qjlc_export` assembles the
+    record bytes on the GPU."""
+    if state.n == 0:
+        raise ValueError("refusing to serialize an empty cache")
+    if len(value_tokens) != state.n:
+        raise ValueError(
+            f"value token count {len(value_tokens)} does not match cache length {state.n}")
+    bits = value_tokens[0].bits
+    if any(t.bits != bits or t.d != state.d for t in value_tokens):
+        raise ValueError("value tokens must share one bit width and dimension")
+    dev, n, d = _cuda(), state.n, state.d
+    codes = torch.from_numpy(np.stack([np.asarray(t.codes, np.uint8) for t in value_tokens])).to(dev)
+    zero = torch.tensor([t.zero for t in value_tokens], dtype=torch.float64).to(torch.float32).to(dev)
+    scale = torch.tensor([t.scale for t in value_tokens], dtype=torch.float64).to(torch.float32).to(dev)
+    vd = _lib.ValueCacheDesc(codes.data_ptr(), zero.data_ptr(), scale.data_ptr(), n, 1, d, bits, d,
+                             _lib.QJL_VLAYOUT_U8)
+    recs, R = _qjlc.export_records(state.device_cache.key_desc(), vd, state.m_in, state.m_out, n)
+    hdr = CacheHeader(CACHE_VERSION, d, state.h, state.m_in, state.m_out, n, bits, state.seed,
+                      state.orthogonalized)
+    body = recs[0, : n * R].cpu().numpy()
+    with open(path, "wb") as handle:
+        handle.write(_qjlc.pack_header(hdr))
+        handle.write(np.asarray(state.profile.channels, dtype="<u4").tobytes())
+        handle.write(np.asarray(state.profile.channel_magnitudes, "<f8").tobytes())
+        handle.write(body.tobytes())
+
+
+def read_cache(path) -> tuple[KeyCacheState, list[QuantizedValueToken], CacheHeader]:
+    """Load a cache file written by write_cache (kvcache.py:440-520).
+
+    Sketches are regenerated from the header; the key records are scattered into
+    the state's device cache by `qjl_qjlc_import`; value tokens are returned as
+    host objects with f32-valued zero/scale, as the reference returns them."""
+    with open(path, "rb") as handle:
+        blob = handle.read()
+    hdr = _qjlc.parse_header(blob)
+    channels, mags = _qjlc.profile_bytes(blob, hdr)
+    mags.setflags(write=False)
+    profile = OutlierProfile(channels=tuple(int(c) for c in channels), d=hdr.d, channel_magnitudes=mags)
+    state = KeyCacheState.create(profile, m_in=hdr.m_in, m_out=hdr.m_out if hdr.h > 0 else 0,
+                                 seed=hdr.seed, orthogonalize_sketches=hdr.orthogonalized)
+    n = hdr.n
+    recs_np = _qjlc.records_view(blob, hdr)
+    if n:
+        if n > state._cap:
+            state._grow(n)
+        recs = torch.from_numpy(np.array(recs_np).reshape(1, -1)).to(_cuda())
+        _qjlc.import_records(recs, n, state.m_in, state.m_out, state.device_cache.key_desc(), None)
+        state._n = n
+        state.device_cache.n = n
+    R = recs_np.shape[1]
+    c0 = R - hdr.d - 8
+    codes = np.ascontiguousarray(recs_np[:, c0:c0 + hdr.d])
+    zero = np.ascontiguousarray(recs_np[:, R - 8:R - 4]).view("<f4")[:, 0].astype(np.float64)
+    scale = np.ascontiguousarray(recs_np[:, R - 4:]).view("<f4")[:, 0].astype(np.float64)
+    tokens = []
+    for i in range(n):
+        c = codes[i].copy()
+        c.setflags(write=False)
+        tokens.append(QuantizedValueToken(codes=c, zero=float(zero[i]), scale=float(scale[i]),
+                                          bits=hdr.value_bits))
+    return state, tokens, hdr

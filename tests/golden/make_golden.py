@@ -112,6 +112,50 @@ def main() -> None:
     g["q2_norm_out_f16"] = np.array([e[1].norm for e in st2r.entries])
     g["q2_logits_f16norm"] = np.stack([st2r.estimate_logits(q) for q in q2])
 
+    # ---------------- QJLC cache files (kvcache.py:389-520) ----------------
+    # the reference's own write_cache bytes; the device exporter must reproduce them
+    # byte for byte from the same keys/values (fp64 keys, per-token values)
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "c2.qjlc")
+        ref.write_cache(path, st2, vtok)
+        g["qjlc_c2_bytes"] = np.frombuffer(open(path, "rb").read(), np.uint8).copy()
+    # ragged widths: m_in = 96 (2 words, 4 pad bytes), m_out = 40 (partial word)
+    # key streams use a master seed other than the sketch seed: keys drawn from the
+    # sketch's own stream project to ~0 on an orthogonalized S (sign = rounding noise)
+    rng = rsk.rng_from_seed(ref.derive_seed(45, 0))
+    k3 = rng.standard_normal((37, 32))
+    k3[:, [3, 17, 20, 31]] *= 9.0
+    prof3 = kv.detect_outliers(k3, 4)
+    st3 = kv.KeyCacheState.create(prof3, m_in=96, m_out=40, seed=44, orthogonalize_sketches=False)
+    for k in k3:
+        st3.append(k)
+    v3 = rsk.rng_from_seed(ref.derive_seed(44, 1)).standard_normal((37, 32))
+    v3[2] = 1.25                                     # constant token -> scale 0
+    vt3 = [ref.quantize_value(v, 3) for v in v3]
+    g["qjlc_r_keys"], g["qjlc_r_values"] = k3, v3
+    g["qjlc_r_channels"] = np.array(prof3.channels, np.int32)
+    g["qjlc_r_mags"] = prof3.channel_magnitudes.copy()
+    # h = 0: no outlier sketch, the record still carries a zero outlier norm
+    k4 = rsk.rng_from_seed(ref.derive_seed(56, 0)).standard_normal((9, 64))
+    prof4 = kv.detect_outliers(k4, 0)
+    st4 = kv.KeyCacheState.create(prof4, m_in=64, seed=55)
+    for k in k4:
+        st4.append(k)
+    v4 = rsk.rng_from_seed(ref.derive_seed(55, 1)).standard_normal((9, 64))
+    vt4 = [ref.quantize_value(v, 8) for v in v4]
+    g["qjlc_h0_keys"], g["qjlc_h0_values"], g["qjlc_h0_mags"] = k4, v4, prof4.channel_magnitudes.copy()
+    with tempfile.TemporaryDirectory() as td:
+        for name, st_, vt_ in (("r", st3, vt3), ("h0", st4, vt4)):
+            path = os.path.join(td, name + ".qjlc")
+            ref.write_cache(path, st_, vt_)
+            g[f"qjlc_{name}_bytes"] = np.frombuffer(open(path, "rb").read(), np.uint8).copy()
+            st_r, _, _ = ref.read_cache(path)
+            qs = rsk.rng_from_seed(ref.derive_seed(66, 2)).standard_normal((2, st_.d))
+            g[f"qjlc_{name}_queries"] = qs
+            g[f"qjlc_{name}_logits"] = np.stack([st_r.estimate_logits(q) for q in qs])
+            g[f"qjlc_{name}_out"] = np.stack(
+                [ref.quantized_decode(q, st_r, ref.read_cache(path)[1]).output for q in qs])
+
     # ---------------- values (per-token, reference semantics) ----------------
     vals = rsk.rng_from_seed(ref.derive_seed(33, 1)).standard_normal((64, 32))
     vals[3] = 5.0                                    # constant token -> scale 0

@@ -317,6 +317,31 @@ def measure_prefill(device, seed, steps=5, warmup=2):
     lib.qjl_timing_read(ctypes.byref(ms), ctypes.byref(cnt), 1)
     step_ms = e0.elapsed_time(e1) / steps
     kern_ms = ms.value / max(cnt.value, 1)
+    # whole prefill (F2): fused profile (detect + S_full build) + K1, against the
+    # separate detect / build launches + K1
+    sk64 = tuple(torch.as_tensor(S).to(device) for S in (cache.S_in_host, cache.S_out_host))
+    for _ in range(warmup):
+        cache.n = 0
+        cache.prefill(K)
+    e0.record()
+    for _ in range(steps):
+        cache.n = 0
+        cache.prefill(K)
+    e1.record()
+    torch.cuda.synchronize()
+    fused_ms = e0.elapsed_time(e1) / steps
+    e0.record()
+    for _ in range(steps):
+        cache.n = 0
+        cache.detect_outliers(K)
+        sin, sout = sk64
+        lib.qjl_build_sketch(sin.data_ptr(), sout.data_ptr(), w["m_in"], w["m_out"], d, h,
+                             cache.channels.data_ptr(), U, _lib.QJL_BF16, cache.s_full.data_ptr(),
+                             torch.cuda.current_stream().cuda_stream)
+        cache.append_keys(K)
+    e1.record()
+    torch.cuda.synchronize()
+    sep_ms = e0.elapsed_time(e1) / steps
     flops = 2.0 * U * n * d * (w["m_in"] + w["m_out"])
     _, tf_peak, _ = load_peaks()
     del K
@@ -324,6 +349,10 @@ def measure_prefill(device, seed, steps=5, warmup=2):
             "ms_per_step": step_ms, "kernel_ms": kern_ms,
             "tflops": flops / (kern_ms * 1e-3) / 1e12,
             "tensor_frac": flops / (kern_ms * 1e-3) / 1e12 / tf_peak,
+            "with_profile": {"fused_ms": fused_ms, "keys_per_s": U * n / (fused_ms * 1e-3),
+                             "separate_ms": sep_ms,
+                             "note": "prefill(): qjl_prefill_profile (detect + S_full) + K1; "
+                                     "separate = detect_outliers + build_sketch + K1 launches"},
             "note": "K.S^T over zero-padded K=128 (m_in+m_out=576 rows) + sign pack + fp16 norms"}
 
 

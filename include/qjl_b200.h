@@ -13,6 +13,7 @@
  *   qjl_detect_outliers  <- detect_outliers            pkg/src/qjl/kvcache.py:104-123
  *   qjl_build_sketch     <- KeyCacheState.create/__init__ sketch split
  *                                                       pkg/src/qjl/kvcache.py:198-267
+ *   qjl_prefill_profile  <- detect_outliers + KeyCacheState.create, fused
  *   qjl_quantize_keys    <- KeyCacheState.append -> quantize_key (x2 sides)
  *                                                       pkg/src/qjl/kvcache.py:293-306,
  *                                                       pkg/src/qjl/estimator.py:110-124
@@ -121,6 +122,18 @@ QJL_API int qjl_detect_outliers(const void* keys, int dtype, int units, int64_t 
 QJL_API int qjl_build_sketch(const double* s_in, const double* s_out, int m_in, int m_out,
                      int d, int h, const int32_t* channels, int units, int dtype,
                      void* s_full, void* stream);
+
+/* Fused prefill profile: detect_outliers + per-unit S_full build in
+ * one pass over the prompt -- per-block channel partials, then CTAs per unit sum them
+ * in a fixed order, rank, write channels / magnitudes and scatter S_in / S_out into
+ * the unit's zero-padded S_full from the ranks they hold.  s_in [m_in][d-h] and
+ * s_out [m_out][h] are given in the operand dtype `sketch_dtype` (rounded once, as
+ * qjl_build_sketch rounds them).  Same outputs, bit for bit, as qjl_detect_outliers
+ * followed by qjl_build_sketch (kvcache.py:104-123, :198-267). */
+QJL_API int qjl_prefill_profile(const void* keys, int dtype, int units, int64_t n0, int d,
+                                int64_t unit_stride, int h, const void* s_in, const void* s_out,
+                                int m_in, int m_out, int sketch_dtype, int32_t* channels,
+                                double* magnitudes, void* s_full, void* stream);
 
 /* K1: append n keys per unit at rows [row_offset, row_offset + n).
  * keys: [units][n][d] with `key_unit_stride` elements between units.

@@ -47,6 +47,8 @@ SIGNATURES = {
     "qjl_device_info": (c_i32, [P(c_i32), P(c_i32), P(c_i32)]),
     "qjl_detect_outliers": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i32, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "qjl_build_sketch": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp]),
+    "qjl_prefill_profile": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i32, c_i64, c_i32, c_vp, c_vp, c_i32,
+                                    c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "qjl_quantize_keys": (c_i32, [c_vp, c_i32, c_i64, c_i64, P(SketchDesc), c_vp, c_i32,
                                   P(KeyCacheDesc), c_i64, c_vp]),
     "qjl_sketch_query": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, P(SketchDesc), c_i32, c_vp, c_vp]),

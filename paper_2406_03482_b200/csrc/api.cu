@@ -215,6 +215,32 @@ int qjl_build_sketch(const double* s_in, const double* s_out, int m_in, int m_ou
                              (cudaStream_t)stream);
 }
 
+int qjl_prefill_profile(const void* keys, int dtype, int units, int64_t n0, int d, int64_t unit_stride, int h,
+                        const void* s_in, const void* s_out, int m_in, int m_out, int sketch_dtype,
+                        int32_t* channels, double* magnitudes, void* s_full, void* stream) {
+  QJL_CHECK_ARG(keys != nullptr, "keys is NULL");
+  QJL_CHECK_ARG(valid_dtype(dtype), "bad key dtype %d", dtype);
+  QJL_CHECK_ARG(units >= 1, "units must be >= 1");
+  QJL_CHECK_ARG(n0 >= 1, "prompt keys must be a non-empty n x d matrix");
+  QJL_CHECK_ARG(d >= 1 && d <= 1024, "d must be in [1, 1024]");
+  QJL_CHECK_ARG(h >= 0 && h <= d, "outlier count must be in [0, %d], got %d", d, h);
+  QJL_CHECK_ARG(h == 0 || channels != nullptr, "channels output is NULL");
+  QJL_CHECK_ARG(unit_stride >= n0 * d, "unit stride %lld < n0*d", (long long)unit_stride);
+  QJL_CHECK_ARG(s_full != nullptr, "s_full is NULL");
+  QJL_CHECK_ARG(valid_dtype(sketch_dtype), "bad sketch dtype %d", sketch_dtype);
+  QJL_CHECK_ARG((s_in == nullptr) == (m_in == 0) && (m_in == 0) == (d - h == 0),
+                "inlier sketch must be present exactly when d - h > 0");
+  QJL_CHECK_ARG((s_out == nullptr) == (m_out == 0) && (m_out == 0) == (h == 0),
+                "outlier sketch must be present exactly when h > 0");
+  if (h > 0 && d - h > 0 && (int64_t)m_out * (d - h) < (int64_t)m_in * h) {
+    set_error("outlier bit rate below inlier bit rate: m_out/h = %d/%d < m_in/(d-h) = %d/%d", m_out, h,
+              m_in, d - h);
+    return QJL_ERR_ARG;  // kvcache.py:219-226
+  }
+  return launch_prefill_profile(keys, dtype, units, n0, d, unit_stride, h, s_in, s_out, m_in, m_out,
+                                sketch_dtype, channels, magnitudes, s_full, (cudaStream_t)stream);
+}
+
 int qjl_quantize_keys(const void* keys, int dtype, int64_t n, int64_t key_unit_stride,
                       const qjl_sketch_t* sketch, const int32_t* channels, int h,
                       const qjl_key_cache_t* cache, int64_t row_offset, void* stream) {

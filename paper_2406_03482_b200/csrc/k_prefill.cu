@@ -2,6 +2,8 @@
 // key quantizer, value quantizer.  The tcgen05 tensor-core key quantizer for
 // bf16/fp16 keys lives in k_quant_tc.cu; this file's quantizer handles every
 // dtype with fp64 accumulation (fp32 keys, odd shapes, single-key shims).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -58,6 +60,23 @@ __global__ void __launch_bounds__(1024) k_detect_outliers(const T* __restrict__ 
 // block partials in a fixed order, then ranks.  |bf16| / |fp16| sums are exact in
 // fp64 at these lengths, so the result does not depend on the split.
 constexpr int kDetRows = 256;
+
+// |x| as fp64 without the F2F conversion pipe: for a normal 16-bit float the fp64 bit
+// pattern is the magnitude bits shifted into place plus an exponent rebias (exact);
+// zero and subnormal inputs (rare) take the converting path.
+__device__ __forceinline__ double abs_f64_bits(__nv_bfloat16 x) {
+  const uint32_t b = __bfloat16_as_ushort(x) & 0x7FFFu;
+  if ((b & 0x7F80u) == 0u) return fabs((double)__bfloat162float(x));
+  return __hiloint2double((int)((b << 13) + ((1023u - 127u) << 20)), 0);
+}
+__device__ __forceinline__ double abs_f64_bits(__half x) {
+  const uint32_t b = __half_as_ushort(x) & 0x7FFFu;
+  if ((b & 0x7C00u) == 0u) return fabs((double)__half2float(x));
+  return __hiloint2double((int)((b << 10) + ((1023u - 15u) << 20)), 0);
+}
+__device__ __forceinline__ double abs_f64_bits(float x) { return fabs((double)x); }
+__device__ __forceinline__ double abs_f64_bits(double x) { return fabs(x); }
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_detect_partial(const T* __restrict__ keys, int64_t n0, int d,
                                                         int64_t unit_stride, double* __restrict__ part) {
@@ -73,11 +92,12 @@ __global__ void __launch_bounds__(256) k_detect_partial(const T* __restrict__ ke
   for (int e = 0; e < EPV; ++e) acc[e] = 0.0;
   if (rs < rows_par) {
     const int64_t r_end = min((int64_t)(blk + 1) * kDetRows, n0);
+#pragma unroll 4
     for (int64_t r = (int64_t)blk * kDetRows + rs; r < r_end; r += rows_par) {
       const uint4 raw = __ldg(reinterpret_cast<const uint4*>(K + r * d + cg * EPV));
       const T* v = reinterpret_cast<const T*>(&raw);
 #pragma unroll
-      for (int e = 0; e < EPV; ++e) acc[e] += fabs(to_f64(v[e]));
+      for (int e = 0; e < EPV; ++e) acc[e] += abs_f64_bits(v[e]);
     }
 #pragma unroll
     for (int e = 0; e < EPV; ++e) sm_part[rs * d + cg * EPV + e] = acc[e];
@@ -90,27 +110,70 @@ __global__ void __launch_bounds__(256) k_detect_partial(const T* __restrict__ ke
   }
 }
 
+// Channel means from the block partials with all 1024 threads: P = 1024 / d chunks of
+// blocks per channel, each summed in block order with 8 loads in flight, then the P chunk
+// sums added in chunk order -- a fixed order, shared by every kernel that finishes the
+// detection, so they agree bit for bit.  mag: [d] means out; red: [1024] scratch.
+__device__ __forceinline__ void channel_means(const double* __restrict__ part, int u, int nblk, int d,
+                                              int64_t n0, double* mag, double* red) {
+  const int P = max(1, (int)blockDim.x / d);
+  const int c = threadIdx.x % d, k = threadIdx.x / d;
+  if (k < P) {
+    const int b0 = (int)((int64_t)k * nblk / P), b1 = (int)((int64_t)(k + 1) * nblk / P);
+    const double* p = part + (int64_t)u * nblk * d + c;
+    double s = 0.0;
+    int b = b0;
+    for (; b + 8 <= b1; b += 8) {
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldcg(p + (int64_t)(b + j) * d);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[j];
+    }
+    for (; b < b1; ++b) s += __ldcg(p + (int64_t)b * d);
+    red[k * d + c] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < d) {
+    double s = 0.0;
+    for (int j = 0; j < P; ++j) s += red[j * d + threadIdx.x];
+    mag[threadIdx.x] = s / (double)n0;
+  }
+  __syncthreads();
+}
+
+// rank of channel c by (magnitude desc, index asc), counted by P threads per channel
+__device__ __forceinline__ void channel_ranks(const double* mag, int d, int* rank) {
+  const int P = max(1, (int)blockDim.x / d);
+  const int c = threadIdx.x % d, k = threadIdx.x / d;
+  if (threadIdx.x < d) rank[threadIdx.x] = 0;
+  __syncthreads();
+  if (k < P) {
+    const double mc = mag[c];
+    const int j0 = (int)((int64_t)k * d / P), j1 = (int)((int64_t)(k + 1) * d / P);
+    int r = 0;
+    for (int j = j0; j < j1; ++j) {
+      const double mj = mag[j];
+      r += (mj > mc) || (mj == mc && j < c);
+    }
+    if (r) atomicAdd(&rank[c], r);
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(1024) k_detect_finish(const double* __restrict__ part, int nblk, int64_t n0,
                                                         int d, int h, int32_t* __restrict__ channels,
                                                         double* __restrict__ magnitudes) {
   __shared__ double mag[1024];
+  __shared__ double red[1024];
+  __shared__ int rank[1024];
   __shared__ int sel[1024];
   const int u = blockIdx.x;
+  channel_means(part, u, nblk, d, n0, mag, red);
+  channel_ranks(mag, d, rank);
   if (threadIdx.x < d) {
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += part[((int64_t)u * nblk + b) * d + threadIdx.x];
-    mag[threadIdx.x] = s / (double)n0;
-  }
-  __syncthreads();
-  if (threadIdx.x < d) {
-    const double mc = mag[threadIdx.x];
-    int rank = 0;
-    for (int j = 0; j < d; ++j) {
-      const double mj = mag[j];
-      rank += (mj > mc) || (mj == mc && j < (int)threadIdx.x);
-    }
-    sel[threadIdx.x] = rank < h;
-    if (magnitudes) magnitudes[(int64_t)u * d + threadIdx.x] = mc;
+    sel[threadIdx.x] = rank[threadIdx.x] < h;
+    if (magnitudes) magnitudes[(int64_t)u * d + threadIdx.x] = mag[threadIdx.x];
   }
   __syncthreads();
   if (threadIdx.x < d && sel[threadIdx.x]) {
@@ -236,6 +299,273 @@ int launch_build_sketch(const double* s_in, const double* s_out, int m_in, int m
     default: return QJL_ERR_ARG;
   }
   QJL_LAUNCH_CHECK("build_sketch");
+  return QJL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Fused prefill profile: the per-unit finish of the two-phase
+// detection (fixed-order sum of the block partials, mean, rank, channels) builds the
+// unit's zero-padded S_full in the same CTA, from the channel ranks it already holds
+// in shared memory -- no channels round trip, no separate build launch.  Same bits
+// as k_detect_finish followed by k_build_sketch.
+// ---------------------------------------------------------------------------
+template <typename TS>
+__global__ void __launch_bounds__(1024, 1) k_detect_finish_build(
+    const double* __restrict__ part, int nblk, int64_t n0, int d, int h, int32_t* __restrict__ channels,
+    double* __restrict__ magnitudes, const TS* __restrict__ s_in, const TS* __restrict__ s_out,
+    int m_in, int m_out, TS* __restrict__ s_full) {
+  __shared__ double mag[1024];
+  __shared__ double red[1024];
+  __shared__ int rank[1024];
+  __shared__ int src[1024];           // column c: inlier rank, or -1 - outlier rank
+  __shared__ int below[1024];
+  // grid (units, row slices): every CTA of a unit re-derives the ranking from the partials
+  // (parallel, cheap) and builds its slice of S_full rows; slice 0 publishes channels and
+  // magnitudes
+  const int u = blockIdx.x, c = threadIdx.x;
+  const bool publish = blockIdx.y == 0;
+#ifndef QJL_FB_ABLATE
+#define QJL_FB_ABLATE 0      // perf experiments: 1 skip the build, 2 skip the ranking too
+#endif
+  channel_means(part, u, nblk, d, n0, mag, red);
+  if (QJL_FB_ABLATE & 2) return;
+  channel_ranks(mag, d, rank);
+  // outlier flags as one bit per channel (warp ballots) -> prefix counts by popc
+  const bool is_out = c < d && rank[c] < h;
+  const unsigned bal = __ballot_sync(0xffffffffu, is_out);
+  if ((c & 31) == 0 && c < d) below[c >> 5] = (int)bal;
+  if (c < d && magnitudes && publish) magnitudes[(int64_t)u * d + c] = mag[c];
+  __syncthreads();
+  if (c < d) {
+    // ascending position among the outliers / among the inliers (kvcache.py:90-101)
+    int nb = __popc((unsigned)below[c >> 5] & ((1u << (c & 31)) - 1u));
+    for (int w = 0; w < (c >> 5); ++w) nb += __popc((unsigned)below[w]);
+    if (is_out && publish) channels[(int64_t)u * h + nb] = c;
+    src[c] = is_out ? -1 - nb : c - nb;
+  }
+  __syncthreads();
+  const int m_total = m_in + m_out, d_in = d - h;
+  const int r0 = (int)((int64_t)blockIdx.y * m_total / gridDim.y);
+  const int r1 = (int)((int64_t)(blockIdx.y + 1) * m_total / gridDim.y);
+  // S_in / S_out arrive in the operand dtype, so the build is a column scatter.  The
+  // slice's source rows are staged in shared memory first (contiguous, vector loads all
+  // in flight at once), then every thread assembles 16-byte chunks of output rows.
+  extern __shared__ __align__(16) uint8_t s_dyn[];
+  TS* s_rows = reinterpret_cast<TS*>(s_dyn);
+  const int ia = r0, ib = min(r1, m_in), nin = max(0, ib - ia);
+  const int oa = max(r0, m_in) - m_in, ob = r1 - m_in, nout = max(0, ob - oa);
+  // contiguous 16 B aligned spans go through one bulk copy (TMA engine, mbarrier
+  // completion); anything else is copied element-wise
+  __shared__ __align__(8) uint64_t stage_bar;
+  auto bulk_ok = [&](const TS* src, int64_t n_el, TS* dst) {
+    return ((uintptr_t)src & 15) == 0 && ((n_el * (int64_t)sizeof(TS)) & 15) == 0 && ((uintptr_t)dst & 15) == 0 &&
+           n_el * (int64_t)sizeof(TS) < (1 << 20);
+  };
+  TS* s_out_rows = s_rows + (((int64_t)nin * d_in * sizeof(TS) + 15) / 16 * 16) / sizeof(TS);
+  if (QJL_FB_ABLATE & 1) return;
+  const TS* src_a = s_in + (int64_t)ia * d_in;
+  const TS* src_b = s_out + (int64_t)oa * h;
+  const int64_t na = (int64_t)nin * d_in, nb = (int64_t)nout * h;
+  const bool bulk_a = !(QJL_FB_ABLATE & 4) && nin && bulk_ok(src_a, na, s_rows),
+             bulk_b = !(QJL_FB_ABLATE & 4) && nout && bulk_ok(src_b, nb, s_out_rows);
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&stage_bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t bytes = (uint32_t)((bulk_a ? na : 0) + (bulk_b ? nb : 0)) * sizeof(TS);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    if (bulk_a)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(s_rows)),
+                   "l"(src_a), "r"((uint32_t)(na * sizeof(TS))), "r"(bar)
+                   : "memory");
+    if (bulk_b)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(s_out_rows)),
+                   "l"(src_b), "r"((uint32_t)(nb * sizeof(TS))), "r"(bar)
+                   : "memory");
+  }
+  if (nin && !bulk_a && !(QJL_FB_ABLATE & 4))
+    for (int64_t i = threadIdx.x; i < na; i += blockDim.x) s_rows[i] = src_a[i];
+  if (nout && !bulk_b && !(QJL_FB_ABLATE & 4))
+    for (int64_t i = threadIdx.x; i < nb; i += blockDim.x) s_out_rows[i] = src_b[i];
+  __syncthreads();                     // barrier init visible; element-wise copies done
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W_%=;\n}\n" ::"r"(bar)
+      : "memory");
+  TS* out = s_full + (int64_t)u * m_total * d;
+  const TS zero = from_f64<TS>(0.0);
+  constexpr int V = 16 / (int)sizeof(TS);          // columns per 16-byte store
+  const int cpr = (d + V - 1) / V;
+  if (d % V == 0 && blockDim.x % cpr == 0) {
+    // every thread keeps the same V columns for all its rows: source columns in registers
+    const int c0 = (threadIdx.x % cpr) * V;
+    int ci[V], co[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int sc = src[c0 + j];
+      ci[j] = sc >= 0 ? sc : -1;
+      co[j] = sc < 0 ? -1 - sc : -1;
+    }
+    const int rstep = blockDim.x / cpr;
+    for (int r = r0 + threadIdx.x / cpr; r < r1; r += rstep) {
+      TS o[V];
+      if (r < m_in) {
+        const TS* row = s_rows + (r - ia) * d_in;
+#pragma unroll
+        for (int j = 0; j < V; ++j) o[j] = ci[j] >= 0 ? row[ci[j]] : zero;
+      } else {
+        const TS* row = s_out_rows + (r - m_in - oa) * h;
+#pragma unroll
+        for (int j = 0; j < V; ++j) o[j] = co[j] >= 0 ? row[co[j]] : zero;
+      }
+      if (!(QJL_FB_ABLATE & 8) || r < 0)
+        *reinterpret_cast<uint4*>(out + (int64_t)r * d + c0) = *reinterpret_cast<const uint4*>(o);
+    }
+    return;
+  }
+  for (int t = threadIdx.x; t < (r1 - r0) * cpr; t += blockDim.x) {
+    const int r = r0 + t / cpr, c0 = (t % cpr) * V;
+    TS o[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int c = c0 + j;
+      const int sc = c < d ? src[c] : 0;
+      TS v = zero;
+      if (r < m_in) {
+        if (sc >= 0) v = s_rows[(r - ia) * d_in + sc];
+      } else if (sc < 0) {
+        v = s_out_rows[(r - m_in - oa) * h + (-1 - sc)];
+      }
+      o[j] = v;
+    }
+    TS* dst = out + (int64_t)r * d + c0;
+    if (d % V == 0) {
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(o);
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; ++j)
+        if (c0 + j < d) dst[j] = o[j];
+    }
+  }
+}
+
+// S_full from operand-dtype S_in / S_out and given channels (fallback of the fused path)
+template <typename TS>
+__global__ void k_scatter_sketch(const TS* __restrict__ s_in, const TS* __restrict__ s_out, int m_in, int m_out,
+                                 int d, int h, const int32_t* __restrict__ channels, TS* __restrict__ s_full) {
+  __shared__ int src[1024];
+  const int u = blockIdx.y;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    int ro = -1, below = 0;
+    for (int j = 0; j < h; ++j) {
+      const int ch = channels[(int64_t)u * h + j];
+      ro = (ch == c) ? j : ro;
+      below += ch < c;
+    }
+    src[c] = ro >= 0 ? -1 - ro : c - below;
+  }
+  __syncthreads();
+  const int m_total = m_in + m_out, d_in = d - h;
+  TS* out = s_full + (int64_t)u * m_total * d;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < m_total * d; idx += gridDim.x * blockDim.x) {
+    const int r = idx / d, c = idx % d, sc = src[c];
+    TS v = from_f64<TS>(0.0);
+    if (r < m_in) {
+      if (sc >= 0) v = s_in[(int64_t)r * d_in + sc];
+    } else if (sc < 0) {
+      v = s_out[(int64_t)(r - m_in) * h + (-1 - sc)];
+    }
+    out[idx] = v;
+  }
+}
+
+static int launch_scatter_sketch(const void* s_in, const void* s_out, int m_in, int m_out, int d, int h,
+                                 const int32_t* channels, int units, int dtype, void* s_full, cudaStream_t st) {
+  const int m_total = m_in + m_out;
+  dim3 grid((m_total * d + 255) / 256 < 64 ? (m_total * d + 255) / 256 : 64, units);
+  switch (dtype) {
+#define QJL_SS(DT)                                                                                 \
+  case DT:                                                                                         \
+    k_scatter_sketch<Elem<DT>::T><<<grid, 256, 0, st>>>((const Elem<DT>::T*)s_in,                  \
+                                                        (const Elem<DT>::T*)s_out, m_in, m_out, d, \
+                                                        h, channels, (Elem<DT>::T*)s_full);        \
+    break;
+    QJL_SS(QJL_F32)
+    QJL_SS(QJL_F16)
+    QJL_SS(QJL_BF16)
+    QJL_SS(QJL_F64)
+#undef QJL_SS
+    default: return QJL_ERR_ARG;
+  }
+  QJL_LAUNCH_CHECK("scatter_sketch");
+  return QJL_OK;
+}
+
+int launch_prefill_profile(const void* keys, int dtype, int units, int64_t n0, int d, int64_t unit_stride,
+                           int h, const void* s_in, const void* s_out, int m_in, int m_out,
+                           int sketch_dtype, int32_t* channels, double* mags, void* s_full, cudaStream_t st) {
+  const size_t es = dtype_size(dtype);
+  const bool two_phase = n0 >= 2 * kDetRows && d <= 1024 && (d * es) % 16 == 0 && (unit_stride * es) % 16 == 0 &&
+                         ((uintptr_t)keys % 16) == 0 && 256 % (int)(d * es / 16) == 0 && h > 0;
+  if (!two_phase) {
+    int rc = h > 0 ? launch_detect_outliers(keys, dtype, units, n0, d, unit_stride, h, channels, mags, st)
+                   : QJL_OK;
+    if (rc != QJL_OK) return rc;
+    return launch_scatter_sketch(s_in, s_out, m_in, m_out, d, h, channels, units, sketch_dtype, s_full, st);
+  }
+  const int nblk = (int)((n0 + kDetRows - 1) / kDetRows);
+  double* part = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&part, (size_t)units * nblk * d * sizeof(double), st);
+  if (e != cudaSuccess) return cuda_status(e, "prefill_profile workspace");
+  const int tpr = (int)(d * es / 16), rows_par = 256 / tpr;
+  const size_t smem = (size_t)rows_par * d * sizeof(double);
+  dim3 grid(nblk, units);
+  switch (dtype) {
+#define QJL_PPP(DT)                                                                                  \
+  case DT: {                                                                                         \
+    auto kern = k_detect_partial<Elem<DT>::T>;                                                       \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    kern<<<grid, 256, smem, st>>>((const Elem<DT>::T*)keys, n0, d, unit_stride, part);               \
+    break;                                                                                           \
+  }
+    QJL_PPP(QJL_F32)
+    QJL_PPP(QJL_F16)
+    QJL_PPP(QJL_BF16)
+    QJL_PPP(QJL_F64)
+#undef QJL_PPP
+    default: cudaFreeAsync(part, st); return QJL_ERR_ARG;
+  }
+  // row slices: about one wave of 1024-thread CTAs (1 per SM) over all units, and few
+  // enough source rows per slice to stage them in <= 160 KB of shared memory
+  const size_t ts = dtype_size(sketch_dtype);
+  const size_t row_bytes = (size_t)std::max(d - h, h) * ts;          // widest source row
+  const int m_total = m_in + m_out;
+  int slices = std::max(1, device_sm_count() / units);
+  const int max_rows = std::max(1, (int)((160 * 1024 - 64) / row_bytes) - 1);
+  slices = std::max(slices, (m_total + max_rows - 1) / max_rows);
+  slices = std::min(slices, m_total);
+  const size_t smem_fb = ((size_t)(m_total + slices - 1) / slices + 1) * row_bytes + 64;
+  switch (sketch_dtype) {
+#define QJL_PPF(DT)                                                                                     \
+  case DT:                                                                                              \
+    cudaFuncSetAttribute(k_detect_finish_build<Elem<DT>::T>,                                            \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fb);                    \
+    k_detect_finish_build<Elem<DT>::T><<<dim3(units, slices), 1024, smem_fb, st>>>(part, nblk, n0, d, h, \
+                                                               channels, mags,                           \
+                                                               (const Elem<DT>::T*)s_in,                 \
+                                                               (const Elem<DT>::T*)s_out, m_in, m_out,   \
+                                                               (Elem<DT>::T*)s_full);                    \
+    break;
+    QJL_PPF(QJL_F32)
+    QJL_PPF(QJL_F16)
+    QJL_PPF(QJL_BF16)
+    QJL_PPF(QJL_F64)
+#undef QJL_PPF
+    default: cudaFreeAsync(part, st); return QJL_ERR_ARG;
+  }
+  cudaFreeAsync(part, st);
+  QJL_LAUNCH_CHECK("prefill_profile");
   return QJL_OK;
 }
 

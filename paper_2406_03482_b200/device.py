@@ -4,6 +4,7 @@ kv-head) pair).  This is the B200 hot path behind the reference API:
     reference (per key / per query, pkg/src/qjl/kvcache.py)   here (per launch, all units)
     KeyCacheState.create              :234-267                 DeviceKeyCache.create / set_sketches
     detect_outliers                   :104-123                 DeviceKeyCache.detect_outliers
+    detect_outliers + create + append (fused, F2)              DeviceKeyCache.prefill
     KeyCacheState.append              :293-306                 DeviceKeyCache.append_keys      (K1)
     quantize_value                    :140-161                 DeviceKeyCache.append_values
     KeyCacheState.estimate_logits     :322-329                 DeviceKeyCache.scores            (K2)
@@ -186,6 +187,35 @@ class DeviceKeyCache:
                                              _TORCH2QJL[self.sketch_dtype], self.s_full.data_ptr(),
                                              _stream()), "build_sketch")
         self._sketch_keepalive = (sin, sout)
+
+    def prefill(self, prompt_keys: torch.Tensor, values: torch.Tensor | None = None) -> None:
+        """Fused prompt profile + append: `qjl_prefill_profile` detects each
+        unit's outlier channels and builds its zero-padded S_full in one pass over the prompt
+        (kvcache.py:104-123, :234-267), then K1 quantizes the prompt into rows [n, n + n0)
+        (kvcache.py:293-306) and the values, if given, are quantized alongside."""
+        s = self.shape
+        pk = prompt_keys.contiguous()
+        if pk.dim() != 3 or pk.shape[0] != s.units or pk.shape[2] != s.d or pk.shape[1] == 0:
+            raise ValueError("prompt keys must be a non-empty [units, n0, d] tensor")
+        if getattr(self, "S_in_host", None) is None and getattr(self, "S_out_host", None) is None:
+            raise ValueError("no host sketches: build the cache with DeviceKeyCache.create")
+        dev = self.device
+        if getattr(self, "_sk_op", None) is None:
+            # S_in / S_out in the operand dtype (exact: the host copies are operand-rounded)
+            self._sk_op = tuple(None if S is None else
+                                torch.as_tensor(np.ascontiguousarray(S, np.float64)).to(dev, self.sketch_dtype)
+                                for S in (self.S_in_host, self.S_out_host))
+        sin, sout = self._sk_op
+        if self.s_full is None:
+            self.s_full = torch.empty(s.units, s.m_in + s.m_out, s.d, dtype=self.sketch_dtype, device=dev)
+        mags = torch.empty(s.units, s.d, dtype=torch.float64, device=dev)
+        _lib.check(self.lib.qjl_prefill_profile(pk.data_ptr(), _TORCH2QJL[pk.dtype], s.units, pk.shape[1],
+                                                s.d, pk.shape[1] * s.d, s.h, _ptr(sin), _ptr(sout),
+                                                s.m_in, s.m_out, _TORCH2QJL[self.sketch_dtype],
+                                                self.channels.data_ptr(), mags.data_ptr(),
+                                                self.s_full.data_ptr(), _stream()), "prefill_profile")
+        self.magnitudes = mags
+        self.append(pk, values)
 
     @staticmethod
     def make_sketches(d: int, h: int, m_in: int, m_out: int, seed: int = 0,

@@ -420,6 +420,31 @@ def measure_qjlc(device, seed, steps=10, warmup=3):
                     "the D2H of the records into pinned memory (PCIe bound)"}
 
 
+def measure_harness():
+    """Row F4: the statistical suites (harness.py:183-329) as batched device runs, wall
+    time end to end (host sketch draws + device orthogonalize / K1 / K2 + host stats)."""
+    import torch
+
+    from paper_2406_03482_b200 import harness as H
+
+    out = {}
+    for name, fn, kw in (("unbiasedness", H.run_unbiasedness_trial, {}),
+                         ("distortion", H.run_distortion_trial, dict(m=142)),
+                         ("orthogonal", H.run_orthogonal_comparison, {}),
+                         ("scores", H.run_score_trial, dict(m=64, trials=1000))):
+        fn(H.TrialConfig(**dict(kw, trials=100)))        # warm-up (library load, first launches)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = fn(H.TrialConfig(**kw))
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out[name] = {"config": dict(H.TrialConfig(**kw).__dict__), "seconds": dt,
+                     "trials_per_s": r.trials / dt, "passed": bool(r.passed)}
+    out["note"] = ("wall clock per suite, host draws included; the reference's pure-Python loop "
+                   "measures 5.9k / 1.1k / 5.2k / 149 trials/s on these configs (DESIGN.md 5)")
+    return out
+
+
 # --------------------------------------------------------------- GPU arm
 def run_gpu(args):
     import torch
@@ -595,6 +620,11 @@ def run_gpu(args):
             res["qjlc"] = measure_qjlc(device, args.seed)
         except Exception as e:                       # pragma: no cover
             res["qjlc"] = {"error": repr(e)[:200]}
+    if world == 1 and rank == 0 and not args.no_prefill:
+        try:
+            res["harness"] = measure_harness()
+        except Exception as e:                       # pragma: no cover
+            res["harness"] = {"error": repr(e)[:200]}
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline_leg(cache, q, w)
     if rank == 0:

@@ -25,6 +25,7 @@
  *   qjl_decode           <- quantized_decode (scores + softmax + weights @ values)
  *                                                       pkg/src/qjl/attention.py:56-71
  *   qjl_quantize_values  <- quantize_value             pkg/src/qjl/kvcache.py:140-161
+ *   qjl_orthogonalize    <- orthogonalize (batched)   pkg/src/qjl/sketch.py:82-103
  *   qjl_qjlc_export      <- write_cache record loop    pkg/src/qjl/kvcache.py:389-437
  *   qjl_qjlc_import      <- read_cache record loop     pkg/src/qjl/kvcache.py:440-520
  *
@@ -136,7 +137,8 @@ QJL_API int qjl_prefill_profile(const void* keys, int dtype, int units, int64_t 
                                 double* magnitudes, void* s_full, void* stream);
 
 /* K1: append n keys per unit at rows [row_offset, row_offset + n).
- * keys: [units][n][d] with `key_unit_stride` elements between units.
+ * keys: [units][n][d] with `key_unit_stride` elements between units (0: every unit
+ * quantizes the same n keys, e.g. one key set under many per-unit sketches).
  * channels: [units][h] outlier channels (for the norm split), may be NULL if h == 0. */
 QJL_API int qjl_quantize_keys(const void* keys, int dtype, int64_t n, int64_t key_unit_stride,
                       const qjl_sketch_t* sketch, const int32_t* channels, int h,
@@ -180,6 +182,13 @@ QJL_API int qjl_timing_read(double* total_ms, int* launches, int reset);
 /* Value quantizer: v [units][n][d] -> value cache rows [row_offset, row_offset + n). */
 QJL_API int qjl_quantize_values(const void* v, int dtype, int64_t n, int64_t unit_stride,
                         const qjl_value_cache_t* values, int64_t row_offset, void* stream);
+
+/* orthogonalize (sketch.py:82-103) for a batch of sketches: gaussian / out [batch][m][d]
+ * fp64.  Rows are taken in blocks of <= d; each block is replaced by the sign-corrected
+ * thin QR factor of its transpose (positive diag R), rows rescaled to norm sqrt(d).
+ * Used by the statistical suites.  d * min(m, d) * 8 <= 200 KB. */
+QJL_API int qjl_orthogonalize(const double* gaussian, int batch, int m, int d, double* out,
+                              void* stream);
 
 /* QJLC cache files (write_cache / read_cache, pkg/src/qjl/kvcache.py:368-520).
  * One record per token, little-endian, in append order (kvcache.py:430-436, :472):

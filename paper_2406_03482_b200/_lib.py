@@ -63,6 +63,7 @@ SIGNATURES = {
     "qjl_timing_enable": (c_i32, [c_i32]),
     "qjl_timing_read": (c_i32, [P(c_dbl), P(c_i32), c_i32]),
     "qjl_quantize_values": (c_i32, [c_vp, c_i32, c_i64, c_i64, P(ValueCacheDesc), c_i64, c_vp]),
+    "qjl_orthogonalize": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "qjl_qjlc_record_bytes": (c_i64, [c_i32, c_i32, c_i32]),
     "qjl_qjlc_export": (c_i32, [P(KeyCacheDesc), P(ValueCacheDesc), c_i32, c_i32, c_i64, c_i64, c_vp,
                                 c_i64, c_vp]),

@@ -253,7 +253,7 @@ int qjl_quantize_keys(const void* keys, int dtype, int64_t n, int64_t key_unit_s
                 (long long)(row_offset + n), (long long)cache->capacity);
   QJL_CHECK_ARG(h >= 0 && h <= cache->d && (h == 0 || channels), "bad outlier channels");
   QJL_CHECK_ARG((h > 0) == (cache->m_out > 0), "outlier sketch must be present exactly when h > 0");
-  QJL_CHECK_ARG(key_unit_stride >= n * cache->d, "key unit stride too small");
+  QJL_CHECK_ARG(key_unit_stride == 0 || key_unit_stride >= n * cache->d, "key unit stride too small");
   if (n == 0) return QJL_OK;
   int rc = launch_quantize_keys_tc(keys, dtype, n, key_unit_stride, *sketch, channels, h, *cache,
                                    row_offset, (cudaStream_t)stream);
@@ -454,6 +454,18 @@ int qjl_qjlc_import(const uint8_t* records, int64_t unit_stride, int64_t n, int 
   if (n == 0) return QJL_OK;
   return launch_qjlc_import(records, unit_stride, m_in_file, m_out_file, n, *keys, values, row_offset,
                             (cudaStream_t)stream);
+}
+
+int qjl_orthogonalize(const double* gaussian, int batch, int m, int d, double* out, void* stream) {
+  QJL_CHECK_ARG(gaussian != nullptr && out != nullptr, "sketch pointers must be set");
+  QJL_CHECK_ARG(batch >= 1, "batch must be >= 1");
+  QJL_CHECK_ARG(m >= 1 && d >= 1, "sketch dimensions must be positive, got m=%d, d=%d", m, d);
+  const int k = d < m ? d : m;
+  if ((size_t)k * d * sizeof(double) > 200 * 1024 || k > 256) {
+    set_error("orthogonalize stages a d x min(m, d) fp64 block in shared memory: d=%d is too large", d);
+    return QJL_ERR_UNSUPPORTED;
+  }
+  return launch_orthogonalize(gaussian, batch, m, d, out, (cudaStream_t)stream);
 }
 
 }  // extern "C"

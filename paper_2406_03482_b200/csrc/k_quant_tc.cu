@@ -544,7 +544,7 @@ int launch_quantize_keys_tc(const void* keys, int dtype, int64_t n, int64_t kus,
   using namespace qtc;
   if (getenv("QJL_FORCE_SIMT")) return QJL_ERR_UNSUPPORTED;
   if (kc.d != kK || !(dtype == QJL_BF16 || dtype == QJL_F16) || sk.dtype != dtype) return QJL_ERR_UNSUPPORTED;
-  if (h > 64 || kus % 8 != 0) return QJL_ERR_UNSUPPORTED;
+  if (h > 64 || kus % 8 != 0 || kus == 0) return QJL_ERR_UNSUPPORTED;   // kus == 0: shared keys (SIMT)
   if (((uintptr_t)keys & 15) || ((uintptr_t)sk.s_full & 15)) return QJL_ERR_UNSUPPORTED;
   const int MT = kc.m_in + kc.m_out;
   const int abf = dtype == QJL_BF16;

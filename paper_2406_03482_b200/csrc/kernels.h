@@ -58,6 +58,9 @@ int launch_decode_umma(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, i
                        int q_dtype, int G, const qjl_sketch_t& sk, float inv_t, float* out, float* lse,
                        void* ws, size_t ws_bytes, cudaStream_t st);
 
+// batched block-wise sketch orthogonalization (k_orth.cu)
+int launch_orthogonalize(const double* g, int batch, int m, int d, double* out, cudaStream_t st);
+
 // QJLC cache records <-> device cache layout (k_qjlc.cu)
 int64_t qjlc_record_bytes(int d, int m_in_file, int m_out_file);
 int launch_qjlc_export(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int mfi, int mfo,

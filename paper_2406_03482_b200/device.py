@@ -143,6 +143,15 @@ class DeviceKeyCache:
         return _lib.SketchDesc(_ptr(self.s_full), _TORCH2QJL[self.sketch_dtype], 0,
                                (s.m_in + s.m_out) * s.d)
 
+    def set_unit_sketches(self, s_full: torch.Tensor) -> None:
+        """Give every unit its own zero-padded S_full [units, m_in + m_out, d] (operand
+        dtype, on the device) -- e.g. one independent sketch per statistical trial."""
+        s = self.shape
+        if tuple(s_full.shape) != (s.units, s.m_in + s.m_out, s.d) or s_full.dtype != self.sketch_dtype:
+            raise ValueError(f"per-unit sketches must be {self.sketch_dtype} "
+                             f"[{s.units}, {s.m_in + s.m_out}, {s.d}], got {s_full.dtype} {tuple(s_full.shape)}")
+        self.s_full = s_full.contiguous()
+
     def workspace(self, nbytes: int) -> torch.Tensor:
         if self._ws is None or self._ws.numel() < nbytes:
             self._ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)

@@ -156,6 +156,25 @@ def main() -> None:
             g[f"qjlc_{name}_out"] = np.stack(
                 [ref.quantized_decode(q, st_r, ref.read_cache(path)[1]).output for q in qs])
 
+    # ---------------- statistical suites (harness.py:183-329) ----------------
+    from qjl_ref import harness as hz
+    suites = {
+        "unb_sphere": ("run_unbiasedness_trial", dict(d=64, m=8, trials=300, seed=3, distribution="sphere")),
+        "unb_outlier_iid": ("run_unbiasedness_trial", dict(d=32, m=16, trials=200, seed=4,
+                                                           distribution="outlier", orthogonalize=False)),
+        "dist_m64": ("run_distortion_trial", dict(d=64, m=64, trials=300, seed=5, distribution="gaussian")),
+        "dist_m8": ("run_distortion_trial", dict(d=64, m=8, trials=300, seed=5, distribution="gaussian")),
+        "scores": ("run_score_trial", dict(d=32, m=64, n=64, trials=100, seed=6)),
+        "orth": ("run_orthogonal_comparison", dict(d=64, m=16, trials=300, seed=7)),
+    }
+    fields = ["passed", "trials", "mean_estimate", "true_value", "stderr", "z_score", "failure_fraction",
+              "threshold", "fraction_within_bound", "variance_ratio", "score_err_p50", "score_err_p90",
+              "score_err_p99", "score_err_max"]
+    g["harness_fields"] = np.array(fields)
+    for name, (fn, kw) in suites.items():
+        row = getattr(hz, fn)(hz.TrialConfig(**kw)).to_row()
+        g[f"harness_{name}"] = np.array([np.nan if row.get(f) is None else float(row[f]) for f in fields])
+
     # ---------------- values (per-token, reference semantics) ----------------
     vals = rsk.rng_from_seed(ref.derive_seed(33, 1)).standard_normal((64, 32))
     vals[3] = 5.0                                    # constant token -> scale 0

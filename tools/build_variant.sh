@@ -10,7 +10,7 @@ mkdir -p $OUT
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 FLAGS="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr $DEFS"
 pids=()
-for f in api k_prefill k_scores k_decode_simt k_decode_tc k_decode_umma k_quant_tc k_qjlc; do
+for f in api k_prefill k_scores k_decode_simt k_decode_tc k_decode_umma k_quant_tc k_qjlc k_orth; do
   nvcc $FLAGS -Xptxas -v -c $SRC/$f.cu -o $OUT/$f.o 2> $OUT/$f.ptxas.log &
   pids+=($!)
 done

@@ -111,12 +111,37 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// the same on precomputed 32-bit shared-window addresses (no generic->shared conversion
+// in the main loop)
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void bar_sync1() { asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
                : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
                                           uint32_t acc) {
@@ -238,7 +263,8 @@ struct Layout {
   static constexpr int oRed = oBsc;                     // flush scratch aliases Bsc/Bpv
   static constexpr int oStage = oBpv + 4 * 2048;
   static constexpr int oMax = oStage + kStages * kStageBytes;   // [4 warps][8] tile maxima
-  static constexpr int oBar = oMax + 4 * 8 * 4;
+  static constexpr int oQc = oMax + 4 * 8 * 4;                  // [4 queries] float4 estimator constants
+  static constexpr int oBar = oQc + 4 * 16;
   static constexpr int kBars = 2 * kStages + 6;
   static constexpr int oTmem = oBar + kBars * 8;
   static constexpr int oFlag = oTmem + 4;
@@ -406,6 +432,11 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   uint64_t* mx_rdy = sc_bar + 3;            // 4 warps: tile maxima in smem
   uint64_t* p_rdy = sc_bar + 4;             // 4 warps: PV operands (B smem, A TMEM) ready
   uint64_t* bsc_bar = sc_bar + 5;           // the unit's score B image landed (bulk copy)
+  // 32-bit shared addresses of the barriers and stages, computed once
+  const uint32_t s_sm = smem_u32(sm);
+  const uint32_t a_full = s_sm + L::oBar, a_empty = a_full + 8 * kStages;
+  const uint32_t a_sc = a_full + 16 * kStages, a_pv = a_sc + 8, a_ardy = a_sc + 16, a_mx = a_sc + 24,
+                 a_p = a_sc + 32, a_bsc = a_sc + 40;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::oTmem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = P.ctas;
@@ -458,50 +489,55 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   // a single-thread cp.async.bulk is ~15 instructions; spreading them keeps the warps
   // balanced at the tile barriers).  Copies may complete before the expect_tx arrive;
   // the phase cannot complete until that arrive.
-  int iss_u = u_first, iss_lt = lt_first, iss_i = 0;
+  int iss_u = u_first, iss_lt = lt_first, iss_i = 0, iss_s = 0;
+  uint32_t iss_ph = 0;                      // parity of the empty barrier of stage iss_s
   auto issue_next = [&]() {
-    const int i = iss_i;
-    const int s = i % kStages;
-    if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+    const int s = iss_s;
+    if (iss_i >= kStages) mbar_wait(a_empty + 8 * s, iss_ph);
     const int64_t tok = (int64_t)iss_lt * kTile;
     const int64_t row = (int64_t)iss_u * P.kc.capacity + tok;
     const int64_t vrow = (int64_t)iss_u * P.vc.capacity + tok;
-    uint8_t* st = sm + L::oStage + s * L::kStageBytes;
+    const uint32_t st = s_sm + L::oStage + s * L::kStageBytes;
+    const uint32_t fb = a_full + 8 * s;
     if (QJL_UD_ABLATE & 1024) {                    // memory test: bits_in + codes only (8 KB/tile)
       if (warp == 0) {
-        mbar_expect_tx(&full[s], L::kBitsIn + L::kCodes);
-        bulk_g2s(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, &full[s]);
+        mbar_expect_tx(fb, L::kBitsIn + L::kCodes);
+        bulk_g2s(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, fb);
       } else if (warp == 1) {
-        bulk_g2s(st + L::oCodes, (const uint8_t*)P.vc.codes + vrow * 32, L::kCodes, &full[s]);
+        bulk_g2s(st + L::oCodes, (const uint8_t*)P.vc.codes + vrow * 32, L::kCodes, fb);
       }
     } else if (QJL_UD_ABLATE & 2048) {             // memory test: no norms (bits, codes, consts)
       if (warp == 0) {
-        mbar_expect_tx(&full[s], L::kBitsIn + L::kCodes + L::kBitsOut + 2 * L::kConst);
-        bulk_g2s(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, &full[s]);
+        mbar_expect_tx(fb, L::kBitsIn + L::kCodes + L::kBitsOut + 2 * L::kConst);
+        bulk_g2s(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, fb);
       } else if (warp == 1) {
-        bulk_g2s(st + L::oCodes, (const uint8_t*)P.vc.codes + vrow * 32, L::kCodes, &full[s]);
+        bulk_g2s(st + L::oCodes, (const uint8_t*)P.vc.codes + vrow * 32, L::kCodes, fb);
       } else if (warp == 2) {
-        if (KCO) bulk_g2s(st + L::oBitsOut, P.kc.bits_out + row * (KCO * 4), L::kBitsOut, &full[s]);
+        if (KCO) bulk_g2s(st + L::oBitsOut, P.kc.bits_out + row * (KCO * 4), L::kBitsOut, fb);
       } else {
-        bulk_g2s(st + L::oZero, (const uint8_t*)P.vc.zero + vrow * 8, L::kConst, &full[s]);
-        bulk_g2s(st + L::oScale, (const uint8_t*)P.vc.scale + vrow * 8, L::kConst, &full[s]);
+        bulk_g2s(st + L::oZero, (const uint8_t*)P.vc.zero + vrow * 8, L::kConst, fb);
+        bulk_g2s(st + L::oScale, (const uint8_t*)P.vc.scale + vrow * 8, L::kConst, fb);
       }
     } else if (warp == 0) {
-      mbar_expect_tx(&full[s], L::kStageBytes);
-      bulk_g2s(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, &full[s]);
+      mbar_expect_tx(fb, L::kStageBytes);
+      bulk_g2s(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, fb);
     } else if (warp == 1) {
-      bulk_g2s(st + L::oCodes, (const uint8_t*)P.vc.codes + vrow * 32, L::kCodes, &full[s]);
+      bulk_g2s(st + L::oCodes, (const uint8_t*)P.vc.codes + vrow * 32, L::kCodes, fb);
     } else if (warp == 2) {
-      bulk_g2s(st + L::oNormIn, P.kc.norm_in + row, L::kNorm, &full[s]);
+      bulk_g2s(st + L::oNormIn, P.kc.norm_in + row, L::kNorm, fb);
       if (KCO) {
-        bulk_g2s(st + L::oBitsOut, P.kc.bits_out + row * (KCO * 4), L::kBitsOut, &full[s]);
-        bulk_g2s(st + L::oNormOut, P.kc.norm_out + row, L::kNorm, &full[s]);
+        bulk_g2s(st + L::oBitsOut, P.kc.bits_out + row * (KCO * 4), L::kBitsOut, fb);
+        bulk_g2s(st + L::oNormOut, P.kc.norm_out + row, L::kNorm, fb);
       }
     } else {
-      bulk_g2s(st + L::oZero, (const uint8_t*)P.vc.zero + vrow * 8, L::kConst, &full[s]);
-      bulk_g2s(st + L::oScale, (const uint8_t*)P.vc.scale + vrow * 8, L::kConst, &full[s]);
+      bulk_g2s(st + L::oZero, (const uint8_t*)P.vc.zero + vrow * 8, L::kConst, fb);
+      bulk_g2s(st + L::oScale, (const uint8_t*)P.vc.scale + vrow * 8, L::kConst, fb);
     }
     ++iss_i;
+    if (++iss_s == kStages) {
+      iss_s = 0;
+      if (iss_i > kStages) iss_ph ^= 1;     // stages are re-armed from the second round on
+    }
     iss_lt += lt_step;
     if (iss_lt >= P.tpu) { iss_lt = 0; ++iss_u; }
   };
@@ -511,21 +547,24 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   // per-thread running state: token-side partials (l, Z) and dim-side output (acc)
   float m_run[4], l_part[4], acc[4];
   float2 Z[4][2];                      // [q][group pair]
-  float4 qcr[4];                       // per-query estimator constants
+  // per-query estimator constants live in shared memory (L::oQc), not in 16 registers
+  const float4* qcs = reinterpret_cast<const float4*>(sm + L::oQc);
   const float wrow = (tid & 3) == 0 ? 1.f : (tid & 3) == 1 ? 0.25f : (tid & 3) == 2 ? 0.0625f : 0.015625f;
   uint32_t tphase = 0;                      // parity of the per-tile barriers
 
   uint32_t bsc_phase = 0, bsc_par = 0;      // bsc_phase: 0 = wait for the copy before the next MMA
   auto load_unit = [&](int u) {
     bsc_phase = 0;
+    // the unit's estimator constants -> smem; the first reader is behind the tile's first
+    // CTA barrier (and the previous unit's last reader is behind flush's barriers)
+    if (tid < 4) reinterpret_cast<float4*>(sm + L::oQc)[tid] = P.qconst[(int64_t)u * 4 + tid];
     // the unit's score B image: one bulk copy; only the MMA issuer waits for it
     if (tid == 0) {
-      mbar_expect_tx(bsc_bar, L::NH * 2048);
-      bulk_g2s(sm + L::oBsc, P.bsc + (size_t)u * L::NH * 2048, L::NH * 2048, bsc_bar);
+      mbar_expect_tx(a_bsc, L::NH * 2048);
+      bulk_g2s(s_sm + L::oBsc, P.bsc + (size_t)u * L::NH * 2048, L::NH * 2048, a_bsc);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      qcr[q] = P.qconst[(int64_t)u * 4 + q];
       m_run[q] = -INFINITY;
       l_part[q] = 0.f;
       acc[q] = 0.f;
@@ -629,6 +668,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   };
 
   asm volatile("griddepcontrol.wait;" ::: "memory");   // Bsc / qconst come from k_uprep
+  const int n32 = (int)P.n;                            // n <= capacity < 2^30 (supported())
   int cur_u = -1;
   int u = u_first, lt = lt_first;
   int s = 0;
@@ -640,11 +680,11 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       cur_u = u;
     }
     if (lane == 0 && it + kLookahead < ntiles) issue_next();
-    mbar_wait(&full[s], full_phase);
+    mbar_wait(a_full + 8 * s, full_phase);
     const uint8_t* st = sm + L::oStage + s * L::kStageBytes;
     if (QJL_UD_ABLATE & 512) {                       // memory pipeline only
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) mbar_arrive(a_empty + 8 * s);
       lt += lt_step;
       if (lt >= P.tpu) { lt = 0; ++u; }
       if (++s == kStages) { s = 0; full_phase ^= 1; }
@@ -653,7 +693,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     }
     auto body = [&](auto mask_tag) {
     constexpr bool MASK = decltype(mask_tag)::value;
-    const bool valid = !MASK || (int64_t)lt * kTile + tid < P.n;   // this thread's token is < n
+    const bool valid = !MASK || lt * kTile + tid < n32;            // this thread's token is < n
 
     // ---------------- 1. score A operand: masked sign words -> TMEM ----------------
     {
@@ -688,15 +728,15 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     tc_fence_before();
 #if QJL_UD_SPLIT
     __syncwarp();
-    if (lane == 0) mbar_arrive(a_rdy);
+    if (lane == 0) mbar_arrive(a_ardy);
 #else
     bar_sync1();
 #endif
     if (warp == 0 && !(QJL_UD_ABLATE & 1)) {
       if (elect_one()) {
-        if (QJL_UD_SPLIT) mbar_wait(a_rdy, tphase);
+        if (QJL_UD_SPLIT) mbar_wait(a_ardy, tphase);
         if (bsc_phase == 0) {                      // first tile of a unit: B image landed?
-          mbar_wait(bsc_bar, bsc_par);
+          mbar_wait(a_bsc, bsc_par);
           bsc_par ^= 1;
           bsc_phase = 1;
         }
@@ -716,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
             tc_mma_i8c<1>(tbase + L::cDsc + 16, tbase + 8 * (KCI + c),
                           dsc0 + (uint64_t)(h0 + (c >> 2) * 128 + (c & 3) * 2), ID);
         }
-        tc_commit(sc_bar);
+        tc_commit(a_sc);
       }
       __syncwarp();
     }
@@ -727,21 +767,9 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     uint2 zr = reinterpret_cast<const uint2*>(st + L::oZero)[tid];
     uint2 sr = reinterpret_cast<const uint2*>(st + L::oScale)[tid];
     if (!valid) zr = sr = make_uint2(0u, 0u);              // rows past n
-    // dim-side: this dim's P2T code words (4 tokens x 4 dims each; the thread's slot is d % 4)
-    uint32_t cw[32];
-    {
-      const uint4* cs = reinterpret_cast<const uint4*>(st + L::oCodes + (tid >> 2) * 128);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint4 x = cs[k];
-        cw[4 * k] = x.x; cw[4 * k + 1] = x.y; cw[4 * k + 2] = x.z; cw[4 * k + 3] = x.w;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);            // stage fully read by this warp
 
     // ---------------- 3. logits, tile maxima ----------------
-    if (!(QJL_UD_ABLATE & 1)) mbar_wait(sc_bar, tphase);
+    if (!(QJL_UD_ABLATE & 1)) mbar_wait(a_sc, tphase);
     tc_fence_after();
     float lg[4] = {nin, nin + 1.f, nin + 2.f, nin + 3.f};
     if (!(QJL_UD_ABLATE & 16)) {
@@ -753,11 +781,12 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       for (int q = 0; q < 4; ++q) {
         const int* di = reinterpret_cast<const int*>(dr + 4 * q);
         const float fi = fmaf((float)(di[2] + 256 * di[3]), 65536.f, (float)(di[0] + 256 * di[1]));
-        float l2 = nin * fmaf(qcr[q].x, fi, -qcr[q].y);
+        const float4 qc = qcs[q];
+        float l2 = nin * fmaf(qc.x, fi, -qc.y);
         if (KCO) {
           const int* dq = reinterpret_cast<const int*>(dr + 16 + 4 * q);
           const float fo = fmaf((float)(dq[2] + 256 * dq[3]), 65536.f, (float)(dq[0] + 256 * dq[1]));
-          l2 = fmaf(nout, fmaf(qcr[q].z, fo, -qcr[q].w), l2);
+          l2 = fmaf(nout, fmaf(qc.z, fo, -qc.w), l2);
         }
         lg[q] = valid ? l2 : -INFINITY;
       }
@@ -773,23 +802,32 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       if (lane == 0) {
         *reinterpret_cast<float4*>(mx + warp * 8) = make_float4(tm[0], tm[1], tm[2], tm[3]);
         mx[warp * 8 + 4] = smax_w;
-        if (QJL_UD_SPLIT) mbar_arrive(mx_rdy);   // release: the maxima are visible
+        if (QJL_UD_SPLIT) mbar_arrive(a_mx);   // release: the maxima are visible
       }
     }
     // A_pv row of dim tid (the score MMA is done, its A columns are free): 32 columns of
     // 4 tokens, value c * 4^(tid % 4) -- independent of the softmax, so it overlaps the
     // wait for the other warps' maxima
+    // (the code words are read from the stage only here, so they hold no registers
+    // across the score epilogue; the stage is released right after)
     {
       const uint32_t mk = 0x03030303u << (2 * (tid & 3));
-      if (!(QJL_UD_ABLATE & 8)) {
+      const uint4* cs = reinterpret_cast<const uint4*>(st + L::oCodes + (tid >> 2) * 128);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) cw[k] &= mk;
-        tmem_st16(tlane + 0, cw);
-        tmem_st16(tlane + 16, cw + 16);
+      for (int h = 0; h < 2; ++h) {
+        uint32_t cw[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint4 x = cs[4 * h + k];
+          cw[4 * k] = x.x & mk; cw[4 * k + 1] = x.y & mk; cw[4 * k + 2] = x.z & mk; cw[4 * k + 3] = x.w & mk;
+        }
+        if (!(QJL_UD_ABLATE & 8)) tmem_st16(tlane + 16 * h, cw);
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(a_empty + 8 * s);            // stage fully read by this warp
 #if QJL_UD_SPLIT
-    mbar_wait(mx_rdy, tphase);
+    mbar_wait(a_mx, tphase);
 #else
     if (!(QJL_UD_ABLATE & 64)) bar_sync1();
 #endif
@@ -806,7 +844,11 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       tmax[3] = fmaxf(fmaxf(a.w, b.w), fmaxf(c.w, e.w));
       smax = fmaxf(fmaxf(mx[4], mx[12]), fmaxf(mx[20], mx[28]));
     }
-    float alpha[4], p[4], K[4], invK[4];
+    // p = 2^(lg - m_new) = pt * et with pt = 2^(lg - tmax) <= 1 and the tile-uniform
+    // et = 2^(tmax - m_new); P' K = pt * scale * kPMax / smax <= kPMax, and the PV sums
+    // come back scaled by invK = et * smax / kPMax
+    const float ksm = smax > 0.f ? kPMax * rcp_approx(smax) : 0.f;
+    float alpha[4], p[4], pk[4], invK[4];
     bool moved = false;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -814,10 +856,11 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       alpha[q] = ex2(m_run[q] - m_new);
       moved |= alpha[q] != 1.f;
       m_run[q] = m_new;
-      p[q] = ex2(lg[q] - m_new);
-      const float bound = ex2(tmax[q] - m_new) * smax;     // >= every P' of head q in the tile
-      K[q] = bound > 0.f ? kPMax * rcp_approx(bound) : 0.f;
-      invK[q] = bound * (1.f / kPMax);
+      const float et = ex2(tmax[q] - m_new);
+      const float pt = ex2(lg[q] - tmax[q]);
+      p[q] = pt * et;
+      pk[q] = pt * ksm;
+      invK[q] = et * smax * (1.f / kPMax);
     }
     if (moved) {                                          // CTA-uniform
 #pragma unroll
@@ -840,8 +883,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
         const float2 pp = make_float2(p[q], p[q]);
         Z[q][0] = fma2(pp, z01, Z[q][0]);
         Z[q][1] = fma2(pp, z23, Z[q][1]);
-        const float pk = p[q] * K[q];
-        const float2 pk2 = make_float2(pk, pk);
+        const float2 pk2 = make_float2(pk[q], pk[q]);
         const float2 w01 = fma2(pk2, s01, mg), w23 = fma2(pk2, s23, mg);
         wv[q][0] = __float_as_uint(w01.x);
         wv[q][1] = __float_as_uint(w01.y);
@@ -869,7 +911,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     tc_fence_before();
 #if QJL_UD_SPLIT
     __syncwarp();
-    if (lane == 0) mbar_arrive(p_rdy);
+    if (lane == 0) mbar_arrive(a_p);
 #else
     bar_sync1();
 #endif
@@ -877,20 +919,20 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     // ---------------- 5. PV MMA ----------------
     if (warp == 0 && !(QJL_UD_ABLATE & 2)) {
       if (elect_one()) {
-        if (QJL_UD_SPLIT) mbar_wait(p_rdy, tphase);
+        if (QJL_UD_SPLIT) mbar_wait(a_p, tphase);
         tc_fence_after();
         constexpr uint32_t ID = idesc_i8(64, 1);
         tc_mma_i8c<0>(tbase + 32, tbase, dpv0, ID);
         tc_mma_i8c<1>(tbase + 32, tbase + 8, dpv0 + 32, ID);       // + 512 B per 32 tokens
         tc_mma_i8c<1>(tbase + 32, tbase + 16, dpv0 + 64, ID);
         tc_mma_i8c<1>(tbase + 32, tbase + 24, dpv0 + 96, ID);
-        tc_commit(pv_bar);
+        tc_commit(a_pv);
       }
       __syncwarp();
     }
 
     // ---------------- 6. accumulate (thread = dim) ----------------
-    if (!(QJL_UD_ABLATE & 2)) mbar_wait(pv_bar, tphase);
+    if (!(QJL_UD_ABLATE & 2)) mbar_wait(a_pv, tphase);
     tc_fence_after();
     if (!(QJL_UD_ABLATE & 2)) {
       const int G = warp;                                   // value group of dim tid
@@ -905,7 +947,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       }
     }
     };
-    if ((int64_t)(lt + 1) * kTile <= P.n) body(std::false_type{});
+    if ((lt + 1) * kTile <= n32) body(std::false_type{});
     else body(std::true_type{});
     lt += lt_step;
     if (lt >= P.tpu) { lt = 0; ++u; }
@@ -1605,7 +1647,8 @@ bool decode_umma_supported(const qjl_key_cache_t& kc, const qjl_value_cache_t& v
   int id;
   return vc.layout == QJL_VLAYOUT_P2T && kc.d == 128 && G >= 1 && G <= 4 &&
          ud::kc_dispatch(kc.m_in / 32, kc.m_out / 32, &id) && kc.capacity % ud::kTile == 0 &&
-         vc.capacity % ud::kTile == 0 && getenv("QJL_FORCE_SIMT") == nullptr;
+         vc.capacity % ud::kTile == 0 && kc.capacity < (int64_t(1) << 30) &&   // 32-bit token indices
+         getenv("QJL_FORCE_SIMT") == nullptr;
 }
 
 size_t decode_umma_workspace(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, int G) {

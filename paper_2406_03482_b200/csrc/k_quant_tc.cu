@@ -11,9 +11,10 @@
 //  * warp 1: single-thread tcgen05.mma issuer, M = 128 tokens, N = MT split into
 //    NC chunks of CH <= 256 columns, K = 128 (8 x K16), fp32 accumulators in two
 //    ping-pong TMEM buffers of 256 columns;
-//  * warps 2, 3, 12, 13: ||k_in||, ||k_out|| from the staged key tile, one token per
-//    thread: exact fp32 products, double-float (TwoSum) accumulation -> one fp16
-//    rounding, matching the reference's float64 norm stored at half precision;
+//  * warps 2, 3, 12, 13 (K-half 0) and 14-17 (K-half 1): ||k_in||, ||k_out|| from the
+//    staged key tile, one token row per thread pair: exact fp32 products, fp32 sums
+//    with an error bound that decides the fp16 rounding, double-float (TwoSum)
+//    recompute when it does not -> the reference's float64 norm at half precision;
 //  * warps 4-11: epilogue, one set of 4 warps per TMEM buffer -- tcgen05.ld
 //    32x32b (one token per thread), exact sign
 //    test `x >= 0` (set.ge: -0.0 -> 1, NaN -> 0), 32 bits per word, stored as
@@ -28,8 +29,11 @@ namespace qtc {
 
 constexpr int kM = 128;          // tokens per tile (UMMA M)
 constexpr int kK = 128;          // head dim
-constexpr int kThreads = 448;   // 14 warps: TMA, MMA, norms (2, 3, 12, 13), epilogue (4-11)
-constexpr int kPf = 3;          // key tiles prefetched into L2 ahead of the TMA stream
+constexpr int kThreads = 576;   // 18 warps: TMA, MMA, norms (2, 3, 12, 13 | 14-17), epilogue (4-11)
+#ifndef QJL_K1_PF
+#define QJL_K1_PF 3
+#endif
+constexpr int kPf = QJL_K1_PF;   // key tiles prefetched into L2 ahead of the TMA stream
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -170,7 +174,8 @@ struct QLayout {
   static constexpr int kBars = 2 * STAGES + 2 + 4;
   static constexpr int oTmemPtr = oBar + kBars * 8;
   static constexpr int oMask = oTmemPtr + 16;              // per-unit outlier channel list
-  static constexpr int kTotal = oMask + 64 * 4 + 1024;     // + alignment slack
+  static constexpr int oPart = oMask + 64 * 4;              // [2][128] K-half-1 partial sums
+  static constexpr int kTotal = oPart + 2 * 128 * 4 + 1024; // + alignment slack
 };
 
 struct QParams {
@@ -212,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&a_full[s], 1);
-      mbar_init(&a_empty[s], 1 + 4);      // MMA commit + 4 norm warps
+      mbar_init(&a_empty[s], 1 + 8);      // MMA commit + 8 norm warps
     }
     mbar_init(b_full, 1);
     mbar_init(b_empty, 1);
@@ -306,6 +311,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         if (++lt == P.tpu) { lt = 0; ++u; }
       }
     }
+  } else if (warp >= 14) {
+    // ===================== norms, K-half 1: partial sums of squares ================
+    const int nw = warp - 14;
+    const int row = nw * 32 + lane;
+    float* part = reinterpret_cast<float*>(sm + L::oPart);
+    for (int it = 0; it < ntiles; ++it) {
+      const int s = it % STAGES;
+      mbar_wait(&a_full[s], (it / STAGES) & 1);
+      const uint8_t* rowp = sm + L::oA + s * L::kABytes + L::kABytes / 2 + row * 128;
+      float2 acc2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                        make_float2(0.f, 0.f)};           // 8 chains of 8 exact squares
+      if (!(P.ablate & 2)) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((j ^ (row & 7)) << 4));
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = ABF ? make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xFFFF0000u))
+                                 : __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+            float2& c = acc2[e];
+            asm("{\n.reg .b64 x, y;\nmov.b64 x, {%2, %3};\nmov.b64 y, {%0, %1};\n"
+                "fma.rn.f32x2 y, x, x, y;\nmov.b64 {%0, %1}, y;\n}"
+                : "+f"(c.x), "+f"(c.y)
+                : "f"(f.x), "f"(f.y));
+          }
+        }
+      }
+      part[(it & 1) * 128 + row] =
+          ((acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y)) + ((acc2[2].x + acc2[2].y) + (acc2[3].x + acc2[3].y));
+      asm volatile("bar.sync %0, 64;" ::"r"(4 + nw) : "memory");   // hand the partial to the pair
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_empty[s]);
+    }
   } else if (warp < 4 || warp >= 12) {
     // ============================ norms (fp64, exact products) =====================
     const int nw = warp < 4 ? warp - 2 : warp - 10;  // norm warp 0..3
@@ -335,9 +374,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       };
       float all32 = 0.f;
       if (!(P.ablate & 2)) {
-        float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        float2 acc2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                          make_float2(0.f, 0.f)};         // 8 chains of 8 exact squares
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
+        for (int hf = 0; hf < 1; ++hf) {         // K-half 0 here, K-half 1 in the pair warp
           const uint8_t* rowp = a + hf * (L::kABytes / 2) + row * 128;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {          // 16-byte chunk j (swizzled position j ^ row%8)
@@ -346,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 f = elem_pair(w[e]);
-              float2& c = acc2[e & 1];
+              float2& c = acc2[e];
               asm("{\n.reg .b64 x, y;\nmov.b64 x, {%2, %3};\nmov.b64 y, {%0, %1};\n"
                   "fma.rn.f32x2 y, x, x, y;\nmov.b64 {%0, %1}, y;\n}"
                   : "+f"(c.x), "+f"(c.y)
@@ -354,8 +394,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
             }
           }
         }
-        all32 = (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y);
+        all32 = ((acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y)) +
+                ((acc2[2].x + acc2[2].y) + (acc2[3].x + acc2[3].y));
       }
+      asm volatile("bar.sync %0, 64;" ::"r"(4 + nw) : "memory");     // pair's K-half-1 partial
+      all32 += reinterpret_cast<const float*>(sm + L::oPart)[(it & 1) * 128 + row];
       double outl = 0.0;
       for (int j = 0; j < P.h; ++j) {             // outlier channels: read them back
         const int c = chan[j];
@@ -365,45 +408,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         const float x = ABF ? __uint_as_float((uint32_t)bits << 16) : __half2float(__ushort_as_half(bits));
         outl += (double)(x * x);                  // <= 64 exact terms, tiny fp64 work
       }
-      double in64 = fmax((double)all32 - outl, 0.0);
-      {
-        const double err = (double)all32 * 2e-6;  // 128 terms in 4 fp32 chains: <= 32 ulp each
-        const uint16_t lo = f64_to_f16_bits(sqrt(fmax(in64 - err, 0.0)));
-        const uint16_t hi = f64_to_f16_bits(sqrt(in64 + err));
-        if (lo != hi && !(P.ablate & 2)) {        // undecided: exact double-float recompute
-          float hs[4] = {0.f, 0.f, 0.f, 0.f}, ls[4] = {0.f, 0.f, 0.f, 0.f};
-          auto two_sum_add = [&](int k, float x) {
-            const float p = x * x;
-            const float t = hs[k] + p;
-            const float z = t - hs[k];
-            ls[k] += (hs[k] - (t - z)) + (p - z);
-            hs[k] = t;
-          };
-#pragma unroll 1
-          for (int hf = 0; hf < 2; ++hf) {
-            const uint8_t* rowp = a + hf * (L::kABytes / 2) + row * 128;
-#pragma unroll 1
-            for (int j = 0; j < 8; ++j) {
-              const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((j ^ (row & 7)) << 4));
-              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      // fp16 rounding decided in fp32: the exact squared norm lies within e32 of in32.
+      // all32 = p0 + p1, each half summed in 8 fp32 chains of 8 exact squares combined
+      // pairwise: <= 7 + 3 roundings of 2^-24 * (half sum) per half (all terms >= 0), one
+      // more for p0 + p1, and outl32 and the subtraction add 2^-24 * all each: <= 13 *
+      // 2^-24 * all = 7.7e-7 * all.  sqrt.rn and the widening products add <= 2 ulp per
+      // side.  When both ends round to the same fp16 that is the norm.
+      const float outl32 = (float)outl;
+      const float in32 = fmaxf(all32 - outl32, 0.f);
+      const float e32 = all32 * 8.5e-7f;
+      uint16_t nin16 = f32_to_f16_bits(sqrtf(fmaxf(in32 - e32, 0.f)) * (1.f - 2.4e-7f));
+      const bool in_ok = nin16 == f32_to_f16_bits(sqrtf(in32 + e32) * (1.f + 2.4e-7f));
+      const float so = sqrtf(outl32);             // outl is exact; outl32 within 2^-24
+      uint16_t nout16 = f32_to_f16_bits(so * (1.f - 4e-7f));
+      if (nout16 != f32_to_f16_bits(so * (1.f + 4e-7f))) nout16 = f64_to_f16_bits(sqrt(outl));
+      // Undecided rows (rare): the warp recomputes each one cooperatively -- lane l squares
+      // elements 4l .. 4l + 3 of the row exactly and the fp64 sum is reduced across lanes
+      // (exact for these 16-bit-significand squares), so a single undecided token costs the
+      // warp ~20 instructions instead of a divergent 128-element double-float pass.
+      unsigned amb = __ballot_sync(0xffffffffu, !in_ok) & (P.ablate & 2 ? 0u : 0xffffffffu);
+      while (amb) {
+        const int src = __ffs(amb) - 1;
+        amb &= amb - 1;
+        const int r = nw * 32 + src;               // token row being recomputed
+        const int hf = lane >> 4, ch = (lane >> 1) & 7;
+        const uint2 v = *reinterpret_cast<const uint2*>(a + hf * (L::kABytes / 2) + r * 128 +
+                                                        ((ch ^ (r & 7)) << 4) + (lane & 1) * 8);
+        const float2 f0 = elem_pair(v.x), f1 = elem_pair(v.y);
+        double t = ((double)(f0.x * f0.x) + (double)(f0.y * f0.y)) + ((double)(f1.x * f1.x) + (double)(f1.y * f1.y));
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = elem_pair(w[e]);
-                two_sum_add(e, f.x);
-                two_sum_add(e, f.y);
-              }
-            }
-          }
-          double all = 0.0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) all += (double)hs[k] + (double)ls[k];
-          in64 = fmax(all - outl, 0.0);
-        }
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == src) nin16 = f64_to_f16_bits(sqrt(fmax(t - outl, 0.0)));
       }
       if (tok < P.n) {
         const int64_t crow = (int64_t)u * P.kc.capacity + P.row_offset + tok;
-        P.kc.norm_in[crow] = f64_to_f16_bits(sqrt(in64));
-        if (m_out > 0) P.kc.norm_out[crow] = f64_to_f16_bits(sqrt(outl));
+        P.kc.norm_in[crow] = nin16;
+        if (m_out > 0) P.kc.norm_out[crow] = nout16;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_empty[s]);

@@ -80,6 +80,14 @@ __device__ __forceinline__ void tc_mma_f16(uint32_t tmem_d, uint64_t adesc, uint
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
+// same, compile-time accumulate flag
+template <int ACC>
+__device__ __forceinline__ void tc_mma_f16c(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "n"(ACC));
+}
 // K-major, SWIZZLE_128B smem matrix descriptor (rows of 128 B, 8-row atoms 1024 B apart)
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   uint64_t d = 0;
@@ -165,13 +173,17 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t* r) {
 template <int MT, int NC, int STAGES>
 struct QLayout {
   static constexpr int CH = MT / NC;                       // columns per N chunk
+  // TMEM accumulator buffers: NBUF of BUFW columns (512 in all), so the MMA can run
+  // NBUF - 1 chunks ahead of the epilogue
+  static constexpr int BUFW = CH <= 64 ? 64 : CH <= 128 ? 128 : 256;
+  static constexpr int NBUF = 512 / BUFW;
   static constexpr int kBHalf = MT * 128;                  // one K-half of S_full (bytes)
   static constexpr int kABytes = kM * kK * 2;              // one key tile (32 KB)
   static constexpr int oB = 0;                             // S_full: [2 halves][MT rows][128 B]
   static constexpr int oA = 2 * kBHalf;                    // key tiles: [STAGES][2 halves][128][128 B]
   static constexpr int oBar = oA + STAGES * kABytes;
-  // barriers: a_full[S], a_empty[S], b_full, b_empty, t_full[2], t_empty[2]
-  static constexpr int kBars = 2 * STAGES + 2 + 4;
+  // barriers: a_full[S], a_empty[S], b_full, b_empty, t_full[NBUF], t_empty[NBUF]
+  static constexpr int kBars = 2 * STAGES + 2 + 2 * NBUF;
   static constexpr int oTmemPtr = oBar + kBars * 8;
   static constexpr int oMask = oTmemPtr + 16;              // per-unit outlier channel list
   static constexpr int oPart = oMask + 64 * 4;              // [2][128] K-half-1 partial sums
@@ -206,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
   uint64_t* b_full = bars + 2 * STAGES;
   uint64_t* b_empty = b_full + 1;
   uint64_t* t_full = b_full + 2;
-  uint64_t* t_empty = b_full + 4;
+  uint64_t* t_empty = t_full + L::NBUF;
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(sm + L::oTmemPtr);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int C = gridDim.x;
@@ -221,9 +233,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     }
     mbar_init(b_full, 1);
     mbar_init(b_empty, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < L::NBUF; ++b) {
       mbar_init(&t_full[b], 1);
-      mbar_init(&t_empty[b], 4);          // the 4 epilogue warps of buffer b's set
+      mbar_init(&t_empty[b], 4);          // the 4 epilogue warps of the chunk's set
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_keys) : "memory");
@@ -288,20 +300,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         const int s = it % STAGES;
         mbar_wait(&a_full[s], (it / STAGES) & 1);
         tc_fence_after();
-        const uint32_t a_base = smem_u32(sm + L::oA + s * L::kABytes);
-        const uint32_t b_base = smem_u32(sm + L::oB);
-        for (int c = 0; c < NC; ++c, ++chunk) {
-          const int buf = chunk & 1;
-          if (chunk >= 2) mbar_wait(&t_empty[buf], ((chunk >> 1) - 1) & 1);
-          tc_fence_after();
-          const uint32_t d_tmem = tmem + buf * 256;
+        // descriptors built once; the start-address field (bits 0-13, 16-byte units) takes
+        // the K / chunk offsets as plain adds (all shared addresses are < 256 KB)
+        const uint64_t ad0 = sw128_desc(smem_u32(sm + L::oA + s * L::kABytes));
+        const uint64_t bd0 = sw128_desc(smem_u32(sm + L::oB));
+        const bool do_mma = !(P.ablate & 4);
 #pragma unroll
-          for (int k = 0; k < kK / 16; ++k) {
-            if (P.ablate & 4) break;
-            const int hf = k >> 2, kk = k & 3;   // K-half, 32-byte step inside the 128-byte row
-            const uint64_t ad = sw128_desc(a_base + hf * (L::kABytes / 2) + kk * 32);
-            const uint64_t bd = sw128_desc(b_base + hf * L::kBHalf + c * CH * 128 + kk * 32);
-            tc_mma_f16(d_tmem, ad, bd, IDESC, k > 0 ? 1u : 0u);
+        for (int c = 0; c < NC; ++c, ++chunk) {
+          const int buf = chunk % L::NBUF;
+          if (chunk >= L::NBUF) mbar_wait(&t_empty[buf], ((chunk / L::NBUF) - 1) & 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem + buf * L::BUFW;
+          if (do_mma) {
+#pragma unroll
+            for (int k = 0; k < kK / 16; ++k) {
+              const int hf = k >> 2, kk = k & 3;   // K-half, 32-byte step inside the 128-byte row
+              const uint64_t ad = ad0 + (uint64_t)((hf * (L::kABytes / 2) + kk * 32) >> 4);
+              const uint64_t bd = bd0 + (uint64_t)((hf * L::kBHalf + c * CH * 128 + kk * 32) >> 4);
+              if (k == 0) tc_mma_f16c<0>(d_tmem, ad, bd, IDESC);
+              else tc_mma_f16c<1>(d_tmem, ad, bd, IDESC);
+            }
           }
           tc_commit(&t_full[buf]);
         }
@@ -452,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
   } else {
     // =============================== epilogue ====================================
     const int ew = warp & 3;                     // TMEM lane quadrant: lanes 32*ew .. 32*ew + 31
-    const int set = (warp - 4) >> 2;             // this warp set drains TMEM buffer `set`
+    const int set = (warp - 4) >> 2;             // this warp set drains the chunks of parity `set`
     const int row = ew * 32 + lane;              // token row of the tile
     int u = u_first, lt = lt_first, chunk = 0;
     for (int it = 0; it < ntiles; ++it) {
@@ -460,14 +478,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       const bool valid = tok < P.n;
       const int64_t crow = (int64_t)u * P.kc.capacity + P.row_offset + tok;
       for (int c = 0; c < NC; ++c, ++chunk) {
-        const int buf = chunk & 1;
-        if (buf != set) continue;
-        mbar_wait(&t_full[buf], (chunk >> 1) & 1);
+        if ((chunk & 1) != set) continue;      // the two warp sets alternate chunks
+        const int buf = chunk % L::NBUF;
+        mbar_wait(&t_full[buf], (chunk / L::NBUF) & 1);
         tc_fence_after();
 #pragma unroll 1
         for (int g64 = 0; g64 < (P.ablate & 1 ? 0 : CH / 64); ++g64) {
           uint32_t r[64];
-          tmem_ld64(tmem + ((uint32_t)(ew * 32) << 16) + buf * 256 + g64 * 64, r);
+          tmem_ld64(tmem + ((uint32_t)(ew * 32) << 16) + buf * L::BUFW + g64 * 64, r);
           const uint32_t w0 = QJL_K1_FASTSIGN ? sign_word_fast(r) : sign_word(r);
           const uint32_t w1 = QJL_K1_FASTSIGN ? sign_word_fast(r + 32) : sign_word(r + 32);
           const int sr = c * CH + g64 * 64;      // first sketch row of the word pair
@@ -487,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         }
         if constexpr (CH % 64 == 32) {           // trailing 32-column group of the chunk
           uint32_t r[32];
-          tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + buf * 256 + (CH - 32), r);
+          tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + buf * L::BUFW + (CH - 32), r);
           const uint32_t w = QJL_K1_FASTSIGN ? sign_word_fast(r) : sign_word(r);
           const int sr = c * CH + CH - 32;
           if (valid) {
@@ -588,6 +606,9 @@ int launch_quantize_keys_tc(const void* keys, int dtype, int64_t n, int64_t kus,
   if (((uintptr_t)keys & 15) || ((uintptr_t)sk.s_full & 15)) return QJL_ERR_UNSUPPORTED;
   const int MT = kc.m_in + kc.m_out;
   const int abf = dtype == QJL_BF16;
+#ifndef QJL_K1_NC576
+#define QJL_K1_NC576 3       // 192-column chunks (2 TMEM buffers); 96-column chunks measured 24% slower
+#endif
 #define QJL_QT(MTV, NCV, SV)                                                                             \
   if (MT == MTV)                                                                                         \
     return abf ? launch_impl<MTV, NCV, SV, 1>(keys, n, kus, sk, ch, h, kc, row_offset, st)               \
@@ -596,7 +617,7 @@ int launch_quantize_keys_tc(const void* keys, int dtype, int64_t n, int64_t kus,
   QJL_QT(320, 2, 3)   // m_in 256 + m_out 64 (configs 3/5)
   QJL_QT(384, 2, 3)   // m_in 256 + m_out 128 (config 2)
   QJL_QT(512, 2, 2)   // m = 512, no outliers
-  QJL_QT(576, 3, 2)   // m_in 512 + m_out 64 (config 4)
+  QJL_QT(576, QJL_K1_NC576, 2)   // m_in 512 + m_out 64 (config 4)
 #undef QJL_QT
   return QJL_ERR_UNSUPPORTED;
 }

@@ -198,6 +198,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
         "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -416,7 +421,9 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
 }
 
 // ----------------------------------------------------------------- main kernel
-template <int KCI, int KCO>
+// NQ: query heads the epilogue processes (1, 2 or 4 >= G): MHA (G = 1) skips the work of
+// three padding heads
+template <int KCI, int KCO, int NQ>
 __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(const Params P) {
   using L = Layout<KCI, KCO>;
   constexpr int KC = KCI + KCO;
@@ -564,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       bulk_g2s(s_sm + L::oBsc, P.bsc + (size_t)u * L::NH * 2048, L::NH * 2048, a_bsc);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       m_run[q] = -INFINITY;
       l_part[q] = 0.f;
       acc[q] = 0.f;
@@ -577,7 +584,9 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     // token-side partials -> warp sums -> smem (the Bsc/Bpv region is free now)
     float v[20];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int i = 0; i < 20; ++i) v[i] = 0.f;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
       v[q] = l_part[q];
       v[4 + 4 * q + 0] = Z[q][0].x;
       v[4 + 4 * q + 1] = Z[q][0].y;
@@ -585,7 +594,8 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       v[4 + 4 * q + 3] = Z[q][1].y;
     }
 #pragma unroll
-    for (int i = 0; i < 20; ++i) v[i] = warp_sum(v[i]);
+    for (int i = 0; i < 20; ++i)
+      if (i < NQ || (i >= 4 && (i - 4) / 4 < NQ)) v[i] = warp_sum(v[i]);
     float* red = reinterpret_cast<float*>(sm + L::oRed);
     bar_sync1();                        // everyone is done with Bsc/Bpv
     if (lane == 0)
@@ -606,7 +616,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     float* mypart = P.part + ((int64_t)u * P.max_seg + slot) * P.G * kRec;
     const int grp = tid >> 5;           // value group of dim tid
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       if (q < P.G) {
         float lq = 0.f, zq = 0.f;
 #pragma unroll
@@ -774,11 +784,19 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     float lg[4] = {nin, nin + 1.f, nin + 2.f, nin + 3.f};
     if (!(QJL_UD_ABLATE & 16)) {
       uint32_t dr[32];
-      tmem_ld16(tlane + L::cDsc, dr);
-      if (KCO) tmem_ld16(tlane + L::cDsc + 16, dr + 16);
+      if (NQ == 4) {
+        tmem_ld16(tlane + L::cDsc, dr);
+        if (KCO) tmem_ld16(tlane + L::cDsc + 16, dr + 16);
+      } else if (NQ == 2) {
+        tmem_ld8(tlane + L::cDsc, dr);
+        if (KCO) tmem_ld8(tlane + L::cDsc + 16, dr + 16);
+      } else {
+        tmem_ld4(tlane + L::cDsc, dr);
+        if (KCO) tmem_ld4(tlane + L::cDsc + 16, dr + 16);
+      }
       tmem_wait_ld();
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < NQ; ++q) {
         const int* di = reinterpret_cast<const int*>(dr + 4 * q);
         const float fi = fmaf((float)(di[2] + 256 * di[3]), 65536.f, (float)(di[0] + 256 * di[1]));
         const float4 qc = qcs[q];
@@ -796,9 +814,9 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       const uint32_t hm = hmax2u(sr.x, sr.y);
       const float2 hf = h2f2(hm);
       const float smax_w = warp_max_f32(fmaxf(hf.x, hf.y));
-      float tm[4];
+      float tm[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) tm[q] = warp_max_f32(lg[q]);
+      for (int q = 0; q < NQ; ++q) tm[q] = warp_max_f32(lg[q]);
       if (lane == 0) {
         *reinterpret_cast<float4*>(mx + warp * 8) = make_float4(tm[0], tm[1], tm[2], tm[3]);
         mx[warp * 8 + 4] = smax_w;
@@ -851,7 +869,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     float alpha[4], p[4], pk[4], invK[4];
     bool moved = false;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       const float m_new = fmaxf(m_run[q], tmax[q]);          // finite: every tile has a valid token
       alpha[q] = ex2(m_run[q] - m_new);
       moved |= alpha[q] != 1.f;
@@ -864,7 +882,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     }
     if (moved) {                                          // CTA-uniform
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < NQ; ++q) {
         const float2 a2 = make_float2(alpha[q], alpha[q]), z2 = make_float2(0.f, 0.f);
         l_part[q] *= alpha[q];
         acc[q] *= alpha[q];
@@ -878,7 +896,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     {
       const float2 mg = make_float2(kMagic, kMagic);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < NQ; ++q) {
         l_part[q] += p[q];
         const float2 pp = make_float2(p[q], p[q]);
         Z[q][0] = fma2(pp, z01, Z[q][0]);
@@ -897,7 +915,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     {
       uint4* bpv = reinterpret_cast<uint4*>(sm + L::oBpv) + tid;
 #pragma unroll
-      for (int q = 0; q < 4 && !(QJL_UD_ABLATE & 8); ++q) {
+      for (int q = 0; q < NQ && !(QJL_UD_ABLATE & 8); ++q) {
         uint32_t o[4];
 #pragma unroll
         for (int G = 0; G < 4; ++G) {
@@ -921,7 +939,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       if (elect_one()) {
         if (QJL_UD_SPLIT) mbar_wait(a_p, tphase);
         tc_fence_after();
-        constexpr uint32_t ID = idesc_i8(64, 1);
+        constexpr uint32_t ID = idesc_i8(16 * NQ, 1);           // N = (head, group, digit)
         tc_mma_i8c<0>(tbase + 32, tbase, dpv0, ID);
         tc_mma_i8c<1>(tbase + 32, tbase + 8, dpv0 + 32, ID);       // + 512 B per 32 tokens
         tc_mma_i8c<1>(tbase + 32, tbase + 16, dpv0 + 64, ID);
@@ -938,10 +956,10 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       const int G = warp;                                   // value group of dim tid
       uint32_t dd[4][4];                                    // [head q][lo, mid, hi, pad]
 #pragma unroll
-      for (int q = 0; q < 4; ++q) tmem_ld4(tlane + 32 + 16 * q + 4 * G, dd[q]);
+      for (int q = 0; q < NQ; ++q) tmem_ld4(tlane + 32 + 16 * q + 4 * G, dd[q]);
       tmem_wait_ld();
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < NQ; ++q) {
         const float f = fmaf((float)(int)dd[q][2], 65536.f, (float)((int)dd[q][0] + 256 * (int)dd[q][1]));
         acc[q] = fmaf(f, invK[q] * wrow, acc[q]);
       }
@@ -1516,19 +1534,19 @@ struct Plan {
   size_t bsc_off, qconst_off, part_off, cnt_off, total;
 };
 
-template <int KCI, int KCO>
+template <int KCI, int KCO, int NQ>
 static int occupancy() {
   using L = Layout<KCI, KCO>;
   static int occ = -1;
   if (occ < 0) {
-    cudaFuncSetAttribute(k_udecode<KCI, KCO>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
-    cudaFuncSetAttribute(k_udecode<KCI, KCO>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_udecode<KCI, KCO, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    cudaFuncSetAttribute(k_udecode<KCI, KCO, NQ>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int o = 0;
     // The runtime's occupancy calculator reports 1 CTA/SM for kernels that use tcgen05
     // (it cannot know the TMEM footprint), so resident CTAs are derived from the
     // register file, shared memory and the 512 TMEM columns directly.
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k_udecode<KCI, KCO>);
+    cudaFuncGetAttributes(&fa, k_udecode<KCI, KCO, NQ>);
     int dev = 0, smem_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
@@ -1539,8 +1557,8 @@ static int occupancy() {
     const int tmem_cap = 512 / L::kAlloc;
     occ = o < 1 ? 1 : (o > tmem_cap ? tmem_cap : o);
     if (getenv("QJL_DEBUG"))
-      fprintf(stderr, "k_udecode<%d,%d>: %d CTAs/SM (regs %d -> %d, smem %d/%d -> %d, tmem cols %d)\n", KCI, KCO,
-              occ, fa.numRegs, by_regs, L::kTotal, smem_sm, by_smem, L::kAlloc);
+      fprintf(stderr, "k_udecode<%d,%d,%d>: %d CTAs/SM (regs %d -> %d, smem %d/%d -> %d, tmem cols %d)\n", KCI,
+              KCO, NQ, occ, fa.numRegs, by_regs, L::kTotal, smem_sm, by_smem, L::kAlloc);
   }
   return occ;
 }
@@ -1575,16 +1593,22 @@ static bool kc_dispatch(int kci, int kco, int* id) {
     if (pairs[i][0] == kci && pairs[i][1] == kco) { *id = i; return true; }
   return false;
 }
-static int occupancy_by_id(int id) {
+static int nq_of(int G) { return G <= 1 ? 1 : G <= 2 ? 2 : 4; }
+template <int NQ>
+static int occupancy_by_id_nq(int id) {
   switch (id) {
-    case 0: return occupancy<8, 2>();
-    case 1: return occupancy<8, 4>();
-    case 2: return occupancy<8, 0>();
-    case 3: return occupancy<16, 2>();
-    case 4: return occupancy<16, 0>();
-    case 5: return occupancy<16, 4>();
+    case 0: return occupancy<8, 2, NQ>();
+    case 1: return occupancy<8, 4, NQ>();
+    case 2: return occupancy<8, 0, NQ>();
+    case 3: return occupancy<16, 2, NQ>();
+    case 4: return occupancy<16, 0, NQ>();
+    case 5: return occupancy<16, 4, NQ>();
   }
   return 1;
+}
+static int occupancy_by_id(int id, int G) {
+  const int nq = nq_of(G);
+  return nq == 1 ? occupancy_by_id_nq<1>(id) : nq == 2 ? occupancy_by_id_nq<2>(id) : occupancy_by_id_nq<4>(id);
 }
 static int occupancy_ws_by_id(int id) {
   switch (id) {
@@ -1617,7 +1641,7 @@ static Plan make_plan(const qjl_key_cache_t& kc, int64_t n, int G, int id) {
     }
   }
   if (!p.ws) {
-    const int64_t slots = (int64_t)device_sm_count() * occupancy_by_id(id);
+    const int64_t slots = (int64_t)device_sm_count() * occupancy_by_id(id, G);
     p.ctas = (int)(p.T < slots ? p.T : slots);
   }
   p.grouped = (p.ctas >= kc.units && getenv("QJL_UD_CONTIG") == nullptr) ? 1 : 0;
@@ -1725,8 +1749,7 @@ static int launch_umma_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
       cfg.dynamicSmemBytes = WLayout<KCI, KCO>::kTotal;
     }
   }
-  if (!plan.ws) {
-    occupancy<KCI, KCO>();
+  if (!plan.ws) {                               // (smem attributes: occupancy<> in launch_u)
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = Layout<KCI, KCO>::kTotal;
   }
@@ -1738,11 +1761,18 @@ static int launch_umma_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
   cfg.numAttrs = 1;
   timing_begin(st);
   cudaError_t e = cudaSuccess;
+  auto launch_u = [&]() -> cudaError_t {
+    switch (nq_of(G)) {
+      case 1: occupancy<KCI, KCO, 1>(); return cudaLaunchKernelEx(&cfg, k_udecode<KCI, KCO, 1>, P);
+      case 2: occupancy<KCI, KCO, 2>(); return cudaLaunchKernelEx(&cfg, k_udecode<KCI, KCO, 2>, P);
+      default: occupancy<KCI, KCO, 4>(); return cudaLaunchKernelEx(&cfg, k_udecode<KCI, KCO, 4>, P);
+    }
+  };
   if constexpr (KCI + KCO <= 12) {
     if (plan.ws) e = cudaLaunchKernelEx(&cfg, k_wdecode<KCI, KCO>, P);
-    else e = cudaLaunchKernelEx(&cfg, k_udecode<KCI, KCO>, P);
+    else e = launch_u();
   } else {
-    e = cudaLaunchKernelEx(&cfg, k_udecode<KCI, KCO>, P);
+    e = launch_u();
   }
   timing_end(st);
   if (e != cudaSuccess) return cuda_status(e, "decode_umma");

@@ -21,6 +21,8 @@ pytestmark = pytest.mark.gpu
     (16, 2000, 1, 4, 256, 128),     # MHA, config-2 sketch sizes
     (4, 3000, 4, 0, 256, 0),        # no outliers
     (4, 3000, 3, 8, 512, 64),       # m = 512, G = 3
+    (8, 5000, 2, 8, 256, 64),       # G = 2 (two-head epilogue)
+    (6, 2500, 1, 8, 512, 64),       # G = 1 with m = 512 (one-head epilogue)
 ])
 def test_umma_matches_simt(cuda, U, n, G, h, m_in, m_out):
     c, q = _cache(U, n, G, h, m_in, m_out, seed=U * 7 + n, layout="p2t")

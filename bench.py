@@ -420,6 +420,42 @@ def measure_qjlc(device, seed, steps=10, warmup=3):
                     "the D2H of the records into pinned memory (PCIe bound)"}
 
 
+def measure_generation_step(cache, q, steps=50):
+    """Row F1: one generation step at C3 = append every unit's new token (key + value)
+    and decode over the grown cache.  `decode_step` fuses the append into the step's
+    query-sketch kernel; `separate` is K1 + value quantizer launches, then the decode.
+    Each step re-appends the last row (the bench cache is full), so the decode covers the
+    same n = 32768 tokens as the headline measurement."""
+    import torch
+
+    U, G, d = q.shape
+    n0 = cache.n                                          # the step appends row n0 - 1 again
+    g = torch.Generator(device=q.device).manual_seed(7)
+    kn = torch.randn(U, d, generator=g, device=q.device).to(q.dtype)
+    vn = torch.randn(U, d, generator=g, device=q.device).to(q.dtype)
+    out = torch.empty(U, G, d, device=q.device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    res = {}
+    for mode in ("decode_step", "separate"):
+        for rep in range(2):                              # first round warms up
+            torch.cuda.synchronize()
+            e0.record()
+            for i in range(steps):
+                cache.n = cache.n_values = n0 - 1
+                if mode == "decode_step":
+                    cache.decode_step(q, kn, vn, out=out)
+                else:
+                    cache.append(kn[:, None, :], vn[:, None, :])
+                    cache.decode(q, out=out)
+            e1.record()
+            torch.cuda.synchronize()
+            res[mode] = e0.elapsed_time(e1) / steps * 1e3
+    cache.n = cache.n_values = n0
+    return {"decode_step_us": res["decode_step"], "separate_us": res["separate"],
+            "note": "append one token per unit (64 units) + decode over n = 32768 tokens; "
+                    "decode_step fuses K1 + value quantizer into the query-sketch kernel"}
+
+
 def measure_harness():
     """Row F4: the statistical suites (harness.py:183-329) as batched device runs, wall
     time end to end (host sketch draws + device orthogonalize / K1 / K2 + host stats)."""
@@ -610,6 +646,11 @@ def run_gpu(args):
         res["output_gather"] = {"collective": "all_gather_into_tensor (NCCL)", "ms": gather_ms,
                                 "bytes": int(out.numel() * out.element_size() * world),
                                 "note": "outside the timed decode region; units are independent"}
+    if world == 1 and rank == 0 and not args.no_prefill and args.layout == "p2t":
+        try:
+            res["generation_step"] = measure_generation_step(cache, q)
+        except Exception as e:                       # pragma: no cover
+            res["generation_step"] = {"error": repr(e)[:200]}
     if world == 1 and rank == 0 and not args.no_prefill:
         try:
             res["prefill"] = measure_prefill(device, args.seed)

@@ -25,6 +25,8 @@
  *   qjl_decode           <- quantized_decode (scores + softmax + weights @ values)
  *                                                       pkg/src/qjl/attention.py:56-71
  *   qjl_quantize_values  <- quantize_value             pkg/src/qjl/kvcache.py:140-161
+ *   qjl_decode_step      <- append + quantize_value + quantized_decode, one step
+ *                                                       kvcache.py:293-306, attention.py:56-71
  *   qjl_orthogonalize    <- orthogonalize (batched)   pkg/src/qjl/sketch.py:82-103
  *   qjl_qjlc_export      <- write_cache record loop    pkg/src/qjl/kvcache.py:389-437
  *   qjl_qjlc_import      <- read_cache record loop     pkg/src/qjl/kvcache.py:440-520
@@ -171,6 +173,18 @@ QJL_API int qjl_decode(const qjl_key_cache_t* cache, const qjl_value_cache_t* va
                const void* q, int q_dtype, int G, const qjl_sketch_t* sketch,
                float inv_temperature, float* out, float* lse, void* workspace,
                size_t workspace_bytes, void* stream);
+
+/* One generation step (Algorithm 1 of the paper): append the new token of
+ * every unit -- k_new / v_new [units][d] in q_dtype -- at row n (K1 + value quantizer
+ * arithmetic, fused into the query-sketch kernel), then decode over rows [0, n + 1).
+ * channels [units][h] is the outlier profile.  Tensor-core path only (P2T values);
+ * QJL_ERR_UNSUPPORTED otherwise (callers then append and decode separately).  Workspace:
+ * qjl_decode_workspace(cache, values, n + 1, G). */
+QJL_API int qjl_decode_step(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int64_t n,
+                            const void* q, int q_dtype, int G, const qjl_sketch_t* sketch,
+                            const int32_t* channels, int h, const void* k_new, const void* v_new,
+                            float inv_temperature, float* out, float* lse, void* workspace,
+                            size_t workspace_bytes, void* stream);
 
 /* Benchmark timing hook: while enabled, the dominant kernel of every qjl_decode /
  * qjl_quantize_keys call is bracketed by CUDA events recorded on its launch stream.

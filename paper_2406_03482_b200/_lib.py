@@ -60,6 +60,8 @@ SIGNATURES = {
     "qjl_decode_workspace": (c_sz, [P(KeyCacheDesc), P(ValueCacheDesc), c_i64, c_i32]),
     "qjl_decode": (c_i32, [P(KeyCacheDesc), P(ValueCacheDesc), c_i64, c_vp, c_i32, c_i32,
                            P(SketchDesc), c_flt, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "qjl_decode_step": (c_i32, [P(KeyCacheDesc), P(ValueCacheDesc), c_i64, c_vp, c_i32, c_i32, P(SketchDesc),
+                                c_vp, c_i32, c_vp, c_vp, c_flt, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "qjl_timing_enable": (c_i32, [c_i32]),
     "qjl_timing_read": (c_i32, [P(c_dbl), P(c_i32), c_i32]),
     "qjl_quantize_values": (c_i32, [c_vp, c_i32, c_i64, c_i64, P(ValueCacheDesc), c_i64, c_vp]),

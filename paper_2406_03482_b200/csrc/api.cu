@@ -468,4 +468,30 @@ int qjl_orthogonalize(const double* gaussian, int batch, int m, int d, double* o
   return launch_orthogonalize(gaussian, batch, m, d, out, (cudaStream_t)stream);
 }
 
+int qjl_decode_step(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int64_t n, const void* q,
+                    int q_dtype, int G, const qjl_sketch_t* sketch, const int32_t* channels, int h,
+                    const void* k_new, const void* v_new, float inv_temperature, float* out, float* lse,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  QJL_TRY(check_key_cache(cache));
+  QJL_TRY(check_value_cache(values, cache->d, cache->units));
+  QJL_TRY(check_sketch(sketch));
+  QJL_CHECK_ARG(q && out && k_new && v_new, "NULL pointer");
+  QJL_CHECK_ARG(valid_dtype(q_dtype) && q_dtype != QJL_F64, "bad query dtype %d", q_dtype);
+  QJL_CHECK_ARG(G >= 1, "G must be >= 1");
+  QJL_CHECK_ARG(inv_temperature > 0.f, "temperature must be positive");
+  QJL_CHECK_ARG(h >= 0 && (h == 0 || channels != nullptr), "channels is NULL");
+  QJL_CHECK_ARG(n >= 0 && n + 1 <= cache->capacity && n + 1 <= values->capacity, "n + 1 exceeds capacity");
+  if (!decode_umma_supported(*cache, *values, G)) {
+    set_error("decode_step runs on the tcgen05 path (P2T values, supported sketch widths); append + decode instead");
+    return QJL_ERR_UNSUPPORTED;
+  }
+  const size_t need = qjl_decode_workspace(cache, values, n + 1, G);
+  if (!workspace || workspace_bytes < need) {
+    set_error("decode workspace needs %zu bytes (got %zu)", need, workspace_bytes);
+    return QJL_ERR_WORKSPACE;
+  }
+  return launch_decode_step_umma(*cache, *values, n, q, q_dtype, G, *sketch, channels, h, k_new, v_new,
+                                 inv_temperature, out, lse, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
 }  // extern "C"

@@ -62,6 +62,19 @@ constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kPMax = 8.0e6f;                  // P' fixed-point full scale (< 2^23 - 32896)
 constexpr float kMagic = 8421504.f;              // 2^23 + 32896
 
+// Decode-step append: the new token of every unit, quantized inside the
+// query-sketch kernel (which streams S_full anyway) and written at row `row` before the
+// decode kernel -- PDL-ordered after it -- reads rows [0, row + 1).
+struct Append {
+  const void* k;               // [units][128] in the query dtype; nullptr: no append
+  const void* v;               // [units][128]
+  qjl_key_cache_t kc;
+  qjl_value_cache_t vc;
+  const int32_t* channels;     // [units][h]
+  int h;
+  int64_t row;
+};
+
 struct Params {
   qjl_key_cache_t kc;
   qjl_value_cache_t vc;
@@ -294,10 +307,11 @@ __device__ __forceinline__ A to_acc(T x) {
 // digits.  B image: row n = 4 q + digit, K byte k of a side <-> chunk c = k / 32 and,
 // within it, (s, i) = ((k % 32) / 4, k % 4) <-> sign bit j = 32 c + 8 i + s (the A side
 // masks word c with 0x01010101 << s).
-template <typename TQ, typename TS, int KCI, int KCO>
+template <typename TQ, typename TS, int KCI, int KCO, bool APPEND>
 __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, const TS* __restrict__ s_full,
                                                int64_t s_unit_stride, float inv_t, uint8_t* __restrict__ bsc,
-                                               float4* __restrict__ qconst, int* __restrict__ counters) {
+                                               float4* __restrict__ qconst, int* __restrict__ counters,
+                                               const Append A) {
   using L = Layout<KCI, KCO>;
   constexpr int MI = KCI * 32, MO = KCO * 32, MT = MI + MO;
   constexpr int d = 128;
@@ -314,6 +328,18 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
     const int g = i / d;
     qs[g][i % d] = g < G ? to_acc<acc_t>(q[((int64_t)u * G + g) * d + i % d]) : (acc_t)0;
   }
+  // decode-step append (APPEND): the new key / value of this unit
+  __shared__ double kd[APPEND ? d : 1], vd[APPEND ? d : 1];
+  __shared__ unsigned char outl_ch[APPEND ? d : 1];
+  __shared__ uint32_t aw[APPEND ? MT / 32 : 1];   // sign words of the new key
+  __shared__ double an[4][2];                 // [warp][inlier, outlier] sums of squares
+  if (APPEND) {
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+      kd[i] = to_f64(reinterpret_cast<const TQ*>(A.k)[(int64_t)u * d + i]);
+      vd[i] = to_f64(reinterpret_cast<const TQ*>(A.v)[(int64_t)u * d + i]);
+      outl_ch[i] = 0;
+    }
+  }
   if (threadIdx.x < 8) mxbits[threadIdx.x >> 1][threadIdx.x & 1] = 0u;
   // let the decode kernel launch now: its prologue and first bulk copies overlap us
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -323,6 +349,7 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
     const TS* row = S + (int64_t)r * d;
     constexpr int EPV = 16 / (int)sizeof(TS);
     acc_t a[4] = {0, 0, 0, 0};
+    double pr = 0.0;                           // APPEND: S_r . k_new, exact products, fp64 sum
 #pragma unroll 4
     for (int e0 = 0; e0 < d; e0 += EPV) {
       const uint4 raw = __ldg(reinterpret_cast<const uint4*>(row + e0));
@@ -332,7 +359,13 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
         const acc_t s = to_acc<acc_t>(sv[k]);
 #pragma unroll
         for (int g = 0; g < 4; ++g) a[g] = fma(s, qs[g][e0 + k], a[g]);
+        if (APPEND) pr = fma((double)s, kd[e0 + k], pr);
       }
+    }
+    if (APPEND) {
+      // bit = (p >= 0): -0.0 -> 1, NaN -> 0 (estimator.py:119-121)
+      const uint32_t bw = __ballot_sync(0xffffffffu, pr >= 0.0);
+      if (lane == 0) aw[wid] = bw;
     }
     float wm[4];
 #pragma unroll
@@ -369,9 +402,75 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
     if (lane == 0) red[g][side][1] = (double)acc * red[g][side][0];
   }
   __syncthreads();
+  // ---- decode-step append, the rest of the math (exactly the arithmetic of K1's fp64
+  // path and of the value quantizer, kvcache.py:293-306, :140-161)
+  double vzero = 0.0, vscale = 0.0;
+  uint32_t vbyte = 0;                         // this lane's P2T byte (dims 4a..4a+3)
+  constexpr bool app = APPEND;
+  if (app) {
+    if (threadIdx.x < A.h) outl_ch[A.channels[(int64_t)u * A.h + threadIdx.x]] = 1;
+    __syncthreads();
+    if (wid < 4) {
+      // norms of the inlier / outlier parts (fp64, one fp16 rounding each), and the
+      // value group wid = dims 32 wid .. 32 wid + 31
+      const int dim = threadIdx.x;
+      const double x2 = kd[dim] * kd[dim];
+      const double sin = warp_sum_f64(outl_ch[dim] ? 0.0 : x2);
+      const double sout = warp_sum_f64(outl_ch[dim] ? x2 : 0.0);
+      if (lane == 0) {
+        an[wid][0] = sin;
+        an[wid][1] = sout;
+      }
+      const double x = vd[dim];
+      double mn = x, mx = x;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      const int levels = (1 << A.vc.bits) - 1;
+      const double spread = mx - mn;
+      vzero = mn;
+      vscale = spread == 0.0 ? 0.0 : spread / (double)levels;
+      int code = 0;
+      if (spread != 0.0) code = (int)fmin(fmax(rint((x - mn) / vscale), 0.0), (double)levels);
+      uint32_t b = (uint32_t)code << (2 * (lane & 3));
+      b |= __shfl_xor_sync(0xffffffffu, b, 1);
+      b |= __shfl_xor_sync(0xffffffffu, b, 2);
+      vbyte = b;
+    }
+    __syncthreads();
+  }
   // Everything above overlaps the previous decode's tail (this grid is launched with
   // programmatic dependent launch); the workspace writes below must wait for it.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (app) {
+    const int64_t crow = (int64_t)u * A.kc.capacity + A.row;
+    if (threadIdx.x < MT / 32) {
+      const int w = threadIdx.x;
+      if (w < MI / 32) reinterpret_cast<uint32_t*>(A.kc.bits_in + crow * (MI / 8))[w] = aw[w];
+      else reinterpret_cast<uint32_t*>(A.kc.bits_out + crow * (MO / 8))[w - MI / 32] = aw[w];
+    }
+    if (threadIdx.x == 0) {
+      const double sin = (an[0][0] + an[1][0]) + (an[2][0] + an[3][0]);
+      const double sout = (an[0][1] + an[1][1]) + (an[2][1] + an[3][1]);
+      A.kc.norm_in[crow] = f64_to_f16_bits(sqrt(sin));
+      if (MO) A.kc.norm_out[crow] = f64_to_f16_bits(sqrt(sout));
+    }
+    if (wid < 4) {
+      const int64_t vrow = (int64_t)u * A.vc.capacity + A.row;
+      if ((lane & 3) == 0) {
+        int64_t byte;
+        int sh;
+        p2t_pos(vrow, threadIdx.x, &byte, &sh);
+        reinterpret_cast<uint8_t*>(A.vc.codes)[byte] = (uint8_t)vbyte;
+      }
+      if (lane == 0) {
+        reinterpret_cast<uint16_t*>(A.vc.zero)[vrow * 4 + wid] = f64_to_f16_bits(vzero);
+        reinterpret_cast<uint16_t*>(A.vc.scale)[vrow * 4 + wid] = f64_to_f16_bits(vscale);
+      }
+    }
+  }
   if (threadIdx.x == 0) counters[u] = 0;
   // B image bytes, 4 per thread iteration (one u32 of a swizzled 16-byte chunk)
   uint8_t* out = bsc + (size_t)u * L::NH * 2048;
@@ -548,6 +647,9 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     iss_lt += lt_step;
     if (iss_lt >= P.tpu) { iss_lt = 0; ++iss_u; }
   };
+
+  // the first copies overlap the prep grid (PDL); a decode step that appends a token
+  // launches this kernel without PDL, so the prep's cache writes are complete here
   if (lane == 0)
     for (int i = 0; i < kLookahead && i < ntiles; ++i) issue_next();
 
@@ -1685,8 +1787,12 @@ size_t decode_umma_workspace(const qjl_key_cache_t& kc, const qjl_value_cache_t&
 template <int KCI, int KCO>
 static int launch_umma_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, const void* q,
                             int q_dtype, int G, const qjl_sketch_t& sk, float inv_t, float* out, float* lse, void* ws,
-                            const ud::Plan& plan, cudaStream_t st) {
+                            const ud::Plan& plan, const ud::Append& app, cudaStream_t st) {
   using namespace ud;
+  if (app.k != nullptr && plan.ws) {             // the opt-in WS kernel prefetches before the prep ends
+    set_error("decode_step: the warp-specialized decode (QJL_UD_WS) does not take appends");
+    return QJL_ERR_UNSUPPORTED;
+  }
   uint8_t* w = (uint8_t*)ws;
   uint8_t* bsc = w + plan.bsc_off;
   float4* qconst = (float4*)(w + plan.qconst_off);
@@ -1704,8 +1810,10 @@ static int launch_umma_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
   pcfg.numAttrs = 1;
   cudaError_t pe = cudaErrorInvalidValue;
 #define QJL_UPREP(TQ, TS)                                                                              \
-  pe = cudaLaunchKernelEx(&pcfg, k_uprep<TQ, TS, KCI, KCO>, (const TQ*)q, G, (const TS*)sk.s_full,     \
-                          sk.unit_stride, inv_t, bsc, qconst, counters)
+  pe = app.k ? cudaLaunchKernelEx(&pcfg, k_uprep<TQ, TS, KCI, KCO, true>, (const TQ*)q, G,            \
+                                  (const TS*)sk.s_full, sk.unit_stride, inv_t, bsc, qconst, counters, app) \
+             : cudaLaunchKernelEx(&pcfg, k_uprep<TQ, TS, KCI, KCO, false>, (const TQ*)q, G,           \
+                                  (const TS*)sk.s_full, sk.unit_stride, inv_t, bsc, qconst, counters, app)
 #define QJL_UPREP_S(TQ)                                                  \
   switch (sk.dtype) {                                                    \
     case QJL_BF16: QJL_UPREP(TQ, __nv_bfloat16); break;                  \
@@ -1756,7 +1864,8 @@ static int launch_umma_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = timing_enabled() ? 0 : 1;
+  // no PDL after a prep that appends: the decode's first copies must see the new row
+  attr[0].val.programmaticStreamSerializationAllowed = (timing_enabled() || app.k != nullptr) ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   timing_begin(st);
@@ -1780,9 +1889,9 @@ static int launch_umma_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
   return QJL_OK;
 }
 
-int launch_decode_umma(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, const void* q,
-                       int q_dtype, int G, const qjl_sketch_t& sk, float inv_t, float* out, float* lse, void* ws,
-                       size_t ws_bytes, cudaStream_t st) {
+static int launch_umma_any(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, const void* q,
+                           int q_dtype, int G, const qjl_sketch_t& sk, float inv_t, float* out, float* lse, void* ws,
+                           size_t ws_bytes, const ud::Append& app, cudaStream_t st) {
   int id;
   if (!ud::kc_dispatch(kc.m_in / 32, kc.m_out / 32, &id)) return QJL_ERR_UNSUPPORTED;
   const ud::Plan plan = ud::make_plan(kc, n, G, id);
@@ -1791,14 +1900,36 @@ int launch_decode_umma(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, i
     return QJL_ERR_WORKSPACE;
   }
   switch (id) {
-    case 0: return launch_umma_impl<8, 2>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, st);
-    case 1: return launch_umma_impl<8, 4>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, st);
-    case 2: return launch_umma_impl<8, 0>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, st);
-    case 3: return launch_umma_impl<16, 2>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, st);
-    case 4: return launch_umma_impl<16, 0>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, st);
-    case 5: return launch_umma_impl<16, 4>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, st);
+    case 0: return launch_umma_impl<8, 2>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, app, st);
+    case 1: return launch_umma_impl<8, 4>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, app, st);
+    case 2: return launch_umma_impl<8, 0>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, app, st);
+    case 3: return launch_umma_impl<16, 2>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, app, st);
+    case 4: return launch_umma_impl<16, 0>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, app, st);
+    case 5: return launch_umma_impl<16, 4>(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, plan, app, st);
   }
   return QJL_ERR_UNSUPPORTED;
+}
+
+int launch_decode_umma(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, const void* q,
+                       int q_dtype, int G, const qjl_sketch_t& sk, float inv_t, float* out, float* lse, void* ws,
+                       size_t ws_bytes, cudaStream_t st) {
+  ud::Append none{};
+  return launch_umma_any(kc, vc, n, q, q_dtype, G, sk, inv_t, out, lse, ws, ws_bytes, none, st);
+}
+
+int launch_decode_step_umma(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, const void* q,
+                            int q_dtype, int G, const qjl_sketch_t& sk, const int32_t* channels, int h,
+                            const void* k_new, const void* v_new, float inv_t, float* out, float* lse, void* ws,
+                            size_t ws_bytes, cudaStream_t st) {
+  ud::Append app{};
+  app.k = k_new;
+  app.v = v_new;
+  app.kc = kc;
+  app.vc = vc;
+  app.channels = channels;
+  app.h = h;
+  app.row = n;                                   // the new token's row; decode over n + 1
+  return launch_umma_any(kc, vc, n + 1, q, q_dtype, G, sk, inv_t, out, lse, ws, ws_bytes, app, st);
 }
 
 }  // namespace qjl

@@ -57,6 +57,12 @@ size_t decode_umma_workspace(const qjl_key_cache_t& kc, const qjl_value_cache_t&
 int launch_decode_umma(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, const void* q,
                        int q_dtype, int G, const qjl_sketch_t& sk, float inv_t, float* out, float* lse,
                        void* ws, size_t ws_bytes, cudaStream_t st);
+// decode step with append: the new token (k_new, v_new [units][128], query dtype) is
+// quantized into row n by the query-sketch kernel, then rows [0, n + 1) are decoded
+int launch_decode_step_umma(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, const void* q,
+                            int q_dtype, int G, const qjl_sketch_t& sk, const int32_t* channels, int h,
+                            const void* k_new, const void* v_new, float inv_t, float* out, float* lse, void* ws,
+                            size_t ws_bytes, cudaStream_t st);
 
 // batched block-wise sketch orthogonalization (k_orth.cu)
 int launch_orthogonalize(const double* g, int batch, int m, int d, double* out, cudaStream_t st);

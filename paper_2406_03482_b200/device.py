@@ -340,7 +340,46 @@ class DeviceKeyCache:
                                        ws.data_ptr(), ws.numel(), _stream()), "decode")
         return out
 
-    # ------------------------------------------------------------- factory
+    def decode_step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,
+                    temperature: float = 1.0, out: torch.Tensor | None = None,
+                    lse: torch.Tensor | None = None) -> torch.Tensor:
+        """One generation step (Algorithm 1): append the new token of every unit
+        (k_new, v_new [U, d]) at row n, then decode q [U, G, d] over rows [0, n + 1).
+        On the tcgen05 path the append is fused into the step's query-sketch kernel;
+        otherwise it runs as K1 + value quantizer launches before the decode."""
+        if temperature <= 0:
+            raise ValueError(f"temperature must be positive, got {temperature}")
+        s = self.shape
+        q = self._check_q(q)
+        kn, vn = k_new.contiguous(), v_new.contiguous()
+        if tuple(kn.shape) != (s.units, s.d) or tuple(vn.shape) != (s.units, s.d):
+            raise ValueError(f"new token must be [units, d] = [{s.units}, {s.d}]")
+        if self.n != self.n_values:
+            raise ValueError(f"cache holds {self.n} keys but {self.n_values} value tokens")
+        if self.n + 1 > s.capacity:
+            raise ValueError(f"cache capacity {s.capacity} exceeded")
+        G = q.shape[1]
+        if out is None:
+            out = torch.empty(s.units, G, s.d, dtype=torch.float32, device=self.device)
+        kd, vd, sd = self.key_desc(), self.value_desc(), self.sketch_desc()
+        n = self.n
+        ws_b = int(self.lib.qjl_decode_workspace(ctypes.byref(kd), ctypes.byref(vd), n + 1, G))
+        ws = self.workspace(ws_b)
+        rc = -2
+        if kn.dtype == q.dtype and vn.dtype == q.dtype:
+            rc = self.lib.qjl_decode_step(ctypes.byref(kd), ctypes.byref(vd), n, q.data_ptr(),
+                                          _TORCH2QJL[q.dtype], G, ctypes.byref(sd), self.channels.data_ptr(),
+                                          s.h, kn.data_ptr(), vn.data_ptr(), 1.0 / float(temperature),
+                                          out.data_ptr(), _ptr(lse), ws.data_ptr(), ws.numel(), _stream())
+        if rc == _lib.QJL_ERR_UNSUPPORTED:
+            self.append(kn[:, None, :], vn[:, None, :])
+            return self.decode(q, temperature, out=out, lse=lse)
+        _lib.check(rc, "decode_step")
+        self.n += 1
+        self.n_values += 1
+        return out
+
+    # ------------------------------------------------------------- factory    # ------------------------------------------------------------- factory
     @classmethod
     def create(cls, units: int, d: int, m_in: int, h: int = 0, m_out: int | None = None,
                capacity: int = 4096, seed: int = 0, orthogonalize_sketches: bool = True,

@@ -103,7 +103,7 @@ def round_to_operand(entries: np.ndarray, dtype: str) -> np.ndarray:
     """
     import torch
 
-    t = torch.from_numpy(np.ascontiguousarray(entries, dtype=np.float64))
+    t = torch.from_numpy(np.array(entries, dtype=np.float64))
     tdt = {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16,
            "f16": torch.float16}[dtype]
     return t.to(tdt).to(torch.float64).numpy()

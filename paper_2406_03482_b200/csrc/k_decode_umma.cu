@@ -307,6 +307,9 @@ __device__ __forceinline__ A to_acc(T x) {
 // digits.  B image: row n = 4 q + digit, K byte k of a side <-> chunk c = k / 32 and,
 // within it, (s, i) = ((k % 32) / 4, k % 4) <-> sign bit j = 32 c + 8 i + s (the A side
 // masks word c with 0x01010101 << s).
+#ifndef QJL_PREP_ABLATE
+#define QJL_PREP_ABLATE 0   // perf experiment only: 1 skip the S.q loop, 2 skip the B image build
+#endif
 template <typename TQ, typename TS, int KCI, int KCO, bool APPEND>
 __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, const TS* __restrict__ s_full,
                                                int64_t s_unit_stride, float inv_t, uint8_t* __restrict__ bsc,
@@ -316,18 +319,38 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
   constexpr int MI = KCI * 32, MO = KCO * 32, MT = MI + MO;
   constexpr int d = 128;
   using acc_t = typename std::conditional<(sizeof(TS) <= 2), float, double>::type;
-  __shared__ acc_t qs[4][d];
+  constexpr bool F32 = std::is_same<acc_t, float>::value;
+  __shared__ acc_t qs[F32 ? 1 : 4][d];                // fp64 path: [head][dim]
+  __shared__ float4 qs4[F32 ? d : 1];                 // fp32 path: the 4 heads of a dim
   __shared__ float sq[4][MT];
-  __shared__ int32_t si[4][MT];
+  __shared__ __align__(16) uint8_t img[L::NH * 2048]; // the score B image, built in place
   __shared__ unsigned int mxbits[4][2];
   __shared__ double red[4][2][2];   // [q][side][sigma, sum]
   const int u = blockIdx.x;
   const TS* S = s_full + (int64_t)u * s_unit_stride;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < 4 * d; i += blockDim.x) {
-    const int g = i / d;
-    qs[g][i % d] = g < G ? to_acc<acc_t>(q[((int64_t)u * G + g) * d + i % d]) : (acc_t)0;
+  // 16-bit sketches: the thread's whole S row (256 B) is requested before anything else,
+  // so one memory round trip covers it
+  uint4 srow[F32 ? 16 : 1];
+  if constexpr (F32) {
+    const uint4* rp = reinterpret_cast<const uint4*>(S + (int64_t)threadIdx.x * d);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) srow[i] = (QJL_PREP_ABLATE & 1) ? make_uint4(0, 0, 0, 0) : __ldg(rp + i);
   }
+  if constexpr (F32) {
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+      float v[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) v[g] = g < G ? to_f32(q[((int64_t)u * G + g) * d + i]) : 0.f;
+      qs4[i] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+  } else {
+    for (int i = threadIdx.x; i < 4 * d; i += blockDim.x) {
+      const int g = i / d;
+      qs[g][i % d] = g < G ? to_acc<acc_t>(q[((int64_t)u * G + g) * d + i % d]) : (acc_t)0;
+    }
+  }
+  for (int i = threadIdx.x; i < L::NH * 128; i += blockDim.x) reinterpret_cast<uint4*>(img)[i] = make_uint4(0, 0, 0, 0);
   // decode-step append (APPEND): the new key / value of this unit
   __shared__ double kd[APPEND ? d : 1], vd[APPEND ? d : 1];
   __shared__ unsigned char outl_ch[APPEND ? d : 1];
@@ -349,18 +372,30 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
     const TS* row = S + (int64_t)r * d;
     constexpr int EPV = 16 / (int)sizeof(TS);
     acc_t a[4] = {0, 0, 0, 0};
+    float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);   // fp32 path, FFMA2 pairs
     double pr = 0.0;                           // APPEND: S_r . k_new, exact products, fp64 sum
-#pragma unroll 4
+#pragma unroll
     for (int e0 = 0; e0 < d; e0 += EPV) {
-      const uint4 raw = __ldg(reinterpret_cast<const uint4*>(row + e0));
+      if (QJL_PREP_ABLATE & 1) break;
+      const uint4 raw = F32 ? srow[(e0 / EPV) & (F32 ? 15 : 0)] : __ldg(reinterpret_cast<const uint4*>(row + e0));
       const TS* sv = reinterpret_cast<const TS*>(&raw);
 #pragma unroll
       for (int k = 0; k < EPV; ++k) {
         const acc_t s = to_acc<acc_t>(sv[k]);
+        if constexpr (F32) {                   // same per-head fma.rn chain, two heads per FFMA2
+          const float4 qv = qs4[e0 + k];
+          const float2 s2 = make_float2(s, s);
+          a01 = fma2(s2, make_float2(qv.x, qv.y), a01);
+          a23 = fma2(s2, make_float2(qv.z, qv.w), a23);
+        } else {
 #pragma unroll
-        for (int g = 0; g < 4; ++g) a[g] = fma(s, qs[g][e0 + k], a[g]);
+          for (int g = 0; g < 4; ++g) a[g] = fma(s, qs[g][e0 + k], a[g]);
+        }
         if (APPEND) pr = fma((double)s, kd[e0 + k], pr);
       }
+    }
+    if constexpr (F32) {
+      a[0] = a01.x; a[1] = a01.y; a[2] = a23.x; a[3] = a23.y;
     }
     if (APPEND) {
       // bit = (p >= 0): -0.0 -> 1, NaN -> 0 (estimator.py:119-121)
@@ -393,9 +428,20 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
     long long acc = 0;
     for (int j = lo + lane; j < hi; j += 32) {
       const int sh = (j - lo) & 7;
-      const int32_t x = (int32_t)rint((double)sq[g][j] * inv / (double)(1 << sh));
-      si[g][j] = x;
+      int32_t x = (int32_t)rint((double)sq[g][j] * inv / (double)(1 << sh));
       acc += (long long)x * (1ll << sh);
+      // four balanced int8 digits of x -> B image rows n = 4 g + t at K byte
+      // k = 32 c + 4 s + i of the side (sign bit jj = 32 c + 8 i + s), SWIZZLE_128B
+      const int jj = j - lo;
+      const int kside = 32 * (jj >> 5) + 4 * (jj & 7) + ((jj >> 3) & 3);
+      const int h = (side ? L::NHI : 0) + (kside >> 7), kk = kside & 127;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int8_t lo8 = (int8_t)(x & 0xFF);
+        x = (x - (int32_t)lo8) >> 8;
+        const int n = 4 * g + t;
+        img[h * 2048 + (n >> 3) * 1024 + (n & 7) * 128 + ((((kk >> 4) ^ (n & 7)) << 4) | (kk & 15))] = (uint8_t)lo8;
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -472,35 +518,11 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
     }
   }
   if (threadIdx.x == 0) counters[u] = 0;
-  // B image bytes, 4 per thread iteration (one u32 of a swizzled 16-byte chunk)
-  uint8_t* out = bsc + (size_t)u * L::NH * 2048;
-  for (int w = threadIdx.x; w < L::NH * 512; w += blockDim.x) {
-    const int h = w / 512, rem = (w % 512) * 4;      // byte offset inside the half image
-    const int n = (rem / 1024) * 8 + (rem % 1024) / 128;
-    const int pchunk = (rem % 128) / 16, b0 = rem % 16;
-    const int kk0 = ((pchunk ^ (n % 8)) * 16) + b0;  // logical K byte inside the half
-    const int qd = n >> 2, digit = n & 3;
-    const bool side = h >= L::NHI;
-    const int kside = (side ? h - L::NHI : h) * 128;
-    const int ksize = side ? MO : MI;
-    uint32_t v = 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int k = kside + kk0 + e;
-      int8_t dg = 0;
-      if (k < ksize) {
-        const int c = k / 32, s = (k % 32) / 4, i = k % 4;
-        int32_t x = si[qd][(side ? MI : 0) + 32 * c + 8 * i + s];
-#pragma unroll
-        for (int t = 0; t <= 3; ++t) {
-          const int8_t lo8 = (int8_t)(x & 0xFF);
-          if (t == digit) dg = lo8;
-          x = (x - (int32_t)lo8) >> 8;
-        }
-      }
-      v |= (uint32_t)(uint8_t)dg << (8 * e);
-    }
-    reinterpret_cast<uint32_t*>(out + h * 2048)[w % 512] = v;
+  // the B image (built in shared memory above) -> workspace, 16-byte stores
+  {
+    uint4* out = reinterpret_cast<uint4*>(bsc + (size_t)u * L::NH * 2048);
+    for (int i = threadIdx.x; i < ((QJL_PREP_ABLATE & 2) ? 0 : L::NH * 128); i += blockDim.x)
+      out[i] = reinterpret_cast<const uint4*>(img)[i];
   }
   if (threadIdx.x < 4) {
     const int g = threadIdx.x;

@@ -363,6 +363,93 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
       outl_ch[i] = 0;
     }
   }
+  // ---- decode-step append (APPEND), done before the dependent decode may launch: the
+  // new row is written and fenced here, so the decode's first copies (issued before its
+  // grid-dependency wait) already see it.  Row n is padding for the previous step's
+  // decode (masked), so writing it while that decode drains is harmless.  Arithmetic:
+  // K1's fp64 path and the value quantizer's (kvcache.py:293-306, :140-161).
+  double vzero = 0.0, vscale = 0.0;
+  uint32_t vbyte = 0;                         // this lane's P2T byte (dims 4a..4a+3)
+  if constexpr (APPEND) {
+    __syncthreads();                          // kd / vd / outl_ch
+    if (threadIdx.x < A.h) outl_ch[A.channels[(int64_t)u * A.h + threadIdx.x]] = 1;
+    {
+      // S_r . k_new: exact products of the 16-bit operands, fp64 sum; bit = (p >= 0):
+      // -0.0 -> 1, NaN -> 0 (estimator.py:119-121)
+      const int r = threadIdx.x;
+      double pr = 0.0;
+      if constexpr (F32) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const TS* sv = reinterpret_cast<const TS*>(&srow[i]);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) pr = fma((double)to_f32(sv[k]), kd[8 * i + k], pr);
+        }
+      } else {
+        const TS* row = S + (int64_t)r * d;
+        for (int e = 0; e < d; ++e) pr = fma(to_f64(row[e]), kd[e], pr);
+      }
+      const uint32_t bw = __ballot_sync(0xffffffffu, pr >= 0.0);
+      if (lane == 0) aw[wid] = bw;
+    }
+    __syncthreads();                          // outl_ch, aw
+    if (wid < 4) {
+      // norms of the inlier / outlier parts (fp64, one fp16 rounding each), and the
+      // value group wid = dims 32 wid .. 32 wid + 31
+      const int dim = threadIdx.x;
+      const double x2 = kd[dim] * kd[dim];
+      const double sin = warp_sum_f64(outl_ch[dim] ? 0.0 : x2);
+      const double sout = warp_sum_f64(outl_ch[dim] ? x2 : 0.0);
+      if (lane == 0) {
+        an[wid][0] = sin;
+        an[wid][1] = sout;
+      }
+      const double x = vd[dim];
+      double mn = x, mx = x;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      const int levels = (1 << A.vc.bits) - 1;
+      const double spread = mx - mn;
+      vzero = mn;
+      vscale = spread == 0.0 ? 0.0 : spread / (double)levels;
+      int code = 0;
+      if (spread != 0.0) code = (int)fmin(fmax(rint((x - mn) / vscale), 0.0), (double)levels);
+      uint32_t b = (uint32_t)code << (2 * (lane & 3));
+      b |= __shfl_xor_sync(0xffffffffu, b, 1);
+      b |= __shfl_xor_sync(0xffffffffu, b, 2);
+      vbyte = b;
+    }
+    __syncthreads();                          // an
+    const int64_t crow = (int64_t)u * A.kc.capacity + A.row;
+    if (threadIdx.x < MT / 32) {
+      const int w = threadIdx.x;
+      if (w < MI / 32) reinterpret_cast<uint32_t*>(A.kc.bits_in + crow * (MI / 8))[w] = aw[w];
+      else reinterpret_cast<uint32_t*>(A.kc.bits_out + crow * (MO / 8))[w - MI / 32] = aw[w];
+    }
+    if (threadIdx.x == 0) {
+      const double sin = (an[0][0] + an[1][0]) + (an[2][0] + an[3][0]);
+      const double sout = (an[0][1] + an[1][1]) + (an[2][1] + an[3][1]);
+      A.kc.norm_in[crow] = f64_to_f16_bits(sqrt(sin));
+      if (MO) A.kc.norm_out[crow] = f64_to_f16_bits(sqrt(sout));
+    }
+    if (wid < 4) {
+      const int64_t vrow = (int64_t)u * A.vc.capacity + A.row;
+      if ((lane & 3) == 0) {
+        int64_t byte;
+        int sh;
+        p2t_pos(vrow, threadIdx.x, &byte, &sh);
+        reinterpret_cast<uint8_t*>(A.vc.codes)[byte] = (uint8_t)vbyte;
+      }
+      if (lane == 0) {
+        reinterpret_cast<uint16_t*>(A.vc.zero)[vrow * 4 + wid] = f64_to_f16_bits(vzero);
+        reinterpret_cast<uint16_t*>(A.vc.scale)[vrow * 4 + wid] = f64_to_f16_bits(vscale);
+      }
+    }
+    __threadfence();
+  }
   if (threadIdx.x < 8) mxbits[threadIdx.x >> 1][threadIdx.x & 1] = 0u;
   // let the decode kernel launch now: its prologue and first bulk copies overlap us
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -373,7 +460,6 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
     constexpr int EPV = 16 / (int)sizeof(TS);
     acc_t a[4] = {0, 0, 0, 0};
     float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);   // fp32 path, FFMA2 pairs
-    double pr = 0.0;                           // APPEND: S_r . k_new, exact products, fp64 sum
 #pragma unroll
     for (int e0 = 0; e0 < d; e0 += EPV) {
       if (QJL_PREP_ABLATE & 1) break;
@@ -391,16 +477,10 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
 #pragma unroll
           for (int g = 0; g < 4; ++g) a[g] = fma(s, qs[g][e0 + k], a[g]);
         }
-        if (APPEND) pr = fma((double)s, kd[e0 + k], pr);
       }
     }
     if constexpr (F32) {
       a[0] = a01.x; a[1] = a01.y; a[2] = a23.x; a[3] = a23.y;
-    }
-    if (APPEND) {
-      // bit = (p >= 0): -0.0 -> 1, NaN -> 0 (estimator.py:119-121)
-      const uint32_t bw = __ballot_sync(0xffffffffu, pr >= 0.0);
-      if (lane == 0) aw[wid] = bw;
     }
     float wm[4];
 #pragma unroll
@@ -448,75 +528,9 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
     if (lane == 0) red[g][side][1] = (double)acc * red[g][side][0];
   }
   __syncthreads();
-  // ---- decode-step append, the rest of the math (exactly the arithmetic of K1's fp64
-  // path and of the value quantizer, kvcache.py:293-306, :140-161)
-  double vzero = 0.0, vscale = 0.0;
-  uint32_t vbyte = 0;                         // this lane's P2T byte (dims 4a..4a+3)
-  constexpr bool app = APPEND;
-  if (app) {
-    if (threadIdx.x < A.h) outl_ch[A.channels[(int64_t)u * A.h + threadIdx.x]] = 1;
-    __syncthreads();
-    if (wid < 4) {
-      // norms of the inlier / outlier parts (fp64, one fp16 rounding each), and the
-      // value group wid = dims 32 wid .. 32 wid + 31
-      const int dim = threadIdx.x;
-      const double x2 = kd[dim] * kd[dim];
-      const double sin = warp_sum_f64(outl_ch[dim] ? 0.0 : x2);
-      const double sout = warp_sum_f64(outl_ch[dim] ? x2 : 0.0);
-      if (lane == 0) {
-        an[wid][0] = sin;
-        an[wid][1] = sout;
-      }
-      const double x = vd[dim];
-      double mn = x, mx = x;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      }
-      const int levels = (1 << A.vc.bits) - 1;
-      const double spread = mx - mn;
-      vzero = mn;
-      vscale = spread == 0.0 ? 0.0 : spread / (double)levels;
-      int code = 0;
-      if (spread != 0.0) code = (int)fmin(fmax(rint((x - mn) / vscale), 0.0), (double)levels);
-      uint32_t b = (uint32_t)code << (2 * (lane & 3));
-      b |= __shfl_xor_sync(0xffffffffu, b, 1);
-      b |= __shfl_xor_sync(0xffffffffu, b, 2);
-      vbyte = b;
-    }
-    __syncthreads();
-  }
   // Everything above overlaps the previous decode's tail (this grid is launched with
   // programmatic dependent launch); the workspace writes below must wait for it.
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (app) {
-    const int64_t crow = (int64_t)u * A.kc.capacity + A.row;
-    if (threadIdx.x < MT / 32) {
-      const int w = threadIdx.x;
-      if (w < MI / 32) reinterpret_cast<uint32_t*>(A.kc.bits_in + crow * (MI / 8))[w] = aw[w];
-      else reinterpret_cast<uint32_t*>(A.kc.bits_out + crow * (MO / 8))[w - MI / 32] = aw[w];
-    }
-    if (threadIdx.x == 0) {
-      const double sin = (an[0][0] + an[1][0]) + (an[2][0] + an[3][0]);
-      const double sout = (an[0][1] + an[1][1]) + (an[2][1] + an[3][1]);
-      A.kc.norm_in[crow] = f64_to_f16_bits(sqrt(sin));
-      if (MO) A.kc.norm_out[crow] = f64_to_f16_bits(sqrt(sout));
-    }
-    if (wid < 4) {
-      const int64_t vrow = (int64_t)u * A.vc.capacity + A.row;
-      if ((lane & 3) == 0) {
-        int64_t byte;
-        int sh;
-        p2t_pos(vrow, threadIdx.x, &byte, &sh);
-        reinterpret_cast<uint8_t*>(A.vc.codes)[byte] = (uint8_t)vbyte;
-      }
-      if (lane == 0) {
-        reinterpret_cast<uint16_t*>(A.vc.zero)[vrow * 4 + wid] = f64_to_f16_bits(vzero);
-        reinterpret_cast<uint16_t*>(A.vc.scale)[vrow * 4 + wid] = f64_to_f16_bits(vscale);
-      }
-    }
-  }
   if (threadIdx.x == 0) counters[u] = 0;
   // the B image (built in shared memory above) -> workspace, 16-byte stores
   {
@@ -1886,8 +1900,7 @@ static int launch_umma_impl(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  // no PDL after a prep that appends: the decode's first copies must see the new row
-  attr[0].val.programmaticStreamSerializationAllowed = (timing_enabled() || app.k != nullptr) ? 0 : 1;
+  attr[0].val.programmaticStreamSerializationAllowed = timing_enabled() ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   timing_begin(st);

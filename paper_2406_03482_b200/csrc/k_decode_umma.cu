@@ -1770,7 +1770,7 @@ static Plan make_plan(const qjl_key_cache_t& kc, int64_t n, int G, int id) {
   // 4-CTA kernel at C3) when the score operand fits (KC <= 12) and every unit gets its
   // own CTA group
   p.ws = 0;
-  if (id <= 2 && getenv("QJL_UD_WS") != nullptr && getenv("QJL_UD_CONTIG") == nullptr) {
+  if (id <= 2 && getenv("QJL_UD_WS") != nullptr) {
     const int64_t wslots = (int64_t)device_sm_count() * occupancy_ws_by_id(id);
     const int wctas = (int)(p.T < wslots ? p.T : wslots);
     if (wctas >= kc.units) {
@@ -1782,7 +1782,10 @@ static Plan make_plan(const qjl_key_cache_t& kc, int64_t n, int G, int id) {
     const int64_t slots = (int64_t)device_sm_count() * occupancy_by_id(id, G);
     p.ctas = (int)(p.T < slots ? p.T : slots);
   }
-  p.grouped = (p.ctas >= kc.units && getenv("QJL_UD_CONTIG") == nullptr) ? 1 : 0;
+  // contiguous stream-K ranges by default (every CTA within one tile of the mean); the
+  // grouped schedule (QJL_UD_GROUPED=1) has uneven group sizes when CTAs / units is not
+  // an integer and measured 2 % (C3) to 13 % (C5) slower
+  p.grouped = (p.ctas >= kc.units && getenv("QJL_UD_GROUPED") != nullptr) ? 1 : 0;
   int ms = 1;
   for (int u = 0; u < kc.units; ++u) {
     int ns;

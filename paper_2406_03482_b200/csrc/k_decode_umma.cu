@@ -146,6 +146,24 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
+#ifndef QJL_UD_EVICT_FIRST
+#define QJL_UD_EVICT_FIRST 1   // the streamed cache tiles are read once per step: evict them first
+#endif
+// same, with an L2 cache-policy hint (the cache stream must not evict the small per-step
+// data -- sketches, B images, partials -- that the prep and the merge re-read)
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void bar_sync1() { asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -660,6 +678,23 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
         bulk_g2s(st + L::oZero, (const uint8_t*)P.vc.zero + vrow * 8, L::kConst, fb);
         bulk_g2s(st + L::oScale, (const uint8_t*)P.vc.scale + vrow * 8, L::kConst, fb);
       }
+    } else if (QJL_UD_EVICT_FIRST) {
+      const uint64_t pol = evict_first_policy();
+      if (warp == 0) {
+        mbar_expect_tx(fb, L::kStageBytes);
+        bulk_g2s_hint(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, fb, pol);
+      } else if (warp == 1) {
+        bulk_g2s_hint(st + L::oCodes, (const uint8_t*)P.vc.codes + vrow * 32, L::kCodes, fb, pol);
+      } else if (warp == 2) {
+        bulk_g2s_hint(st + L::oNormIn, P.kc.norm_in + row, L::kNorm, fb, pol);
+        if (KCO) {
+          bulk_g2s_hint(st + L::oBitsOut, P.kc.bits_out + row * (KCO * 4), L::kBitsOut, fb, pol);
+          bulk_g2s_hint(st + L::oNormOut, P.kc.norm_out + row, L::kNorm, fb, pol);
+        }
+      } else {
+        bulk_g2s_hint(st + L::oZero, (const uint8_t*)P.vc.zero + vrow * 8, L::kConst, fb, pol);
+        bulk_g2s_hint(st + L::oScale, (const uint8_t*)P.vc.scale + vrow * 8, L::kConst, fb, pol);
+      }
     } else if (warp == 0) {
       mbar_expect_tx(fb, L::kStageBytes);
       bulk_g2s(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, fb);
@@ -675,6 +710,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       bulk_g2s(st + L::oZero, (const uint8_t*)P.vc.zero + vrow * 8, L::kConst, fb);
       bulk_g2s(st + L::oScale, (const uint8_t*)P.vc.scale + vrow * 8, L::kConst, fb);
     }
+
     ++iss_i;
     if (++iss_s == kStages) {
       iss_s = 0;

@@ -807,47 +807,63 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     }
     int* flag = reinterpret_cast<int*>(sm + L::oFlag);
     if (ns > 1) {
-      __threadfence();
+      // publish: the CTA's partial writes are ordered before the counter increment by
+      // one cumulative fence after the barrier (not one fence per thread)
       bar_sync1();
-      if (tid == 0) *flag = (atomicAdd(&P.counters[u], 1) == ns - 1);
+      if (tid == 0) {
+        __threadfence();
+        *flag = (atomicAdd(&P.counters[u], 1) == ns - 1);
+      }
       bar_sync1();
       if (!*flag) return;
       __threadfence();
     } else {
       bar_sync1();
     }
+    // last CTA of the unit: merge the ns partials.  (1) warp q turns the segments' (m, l)
+    // into normalized weights w_s = 2^(m_s - M) / L in smem; (2) every thread sums its
+    // (q, dim) outputs over the segments with all loads of a chunk in flight.
     const float* up = P.part + (int64_t)u * P.max_seg * P.G * kRec;
-    // loads of the ns partials are independent: issue them 16 at a time so the merge
-    // costs ~ceil(ns / 16) L2 round trips instead of 3 * ns dependent ones
-    for (int i = tid; i < P.G * 128; i += kThreads) {
-      const int qq = i >> 7, dim = i & 127;
-      float M = -INFINITY, Ls = 0.f, a = 0.f;
-      for (int s0 = 0; s0 < ns; s0 += 16) {
-        float mv[16], lv[16], av[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const float* W = up + ((s0 + k) * P.G + qq) * kRec;
-          const bool ok = s0 + k < ns;
-          mv[k] = ok ? __ldcg(W) : -INFINITY;
-          lv[k] = ok ? __ldcg(W + 1) : 0.f;
-          av[k] = ok ? __ldcg(W + 2 + dim) : 0.f;
-        }
-        float Mc = M;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) Mc = fmaxf(Mc, mv[k]);
-        const float rs = (M == -INFINITY) ? 0.f : ex2(M - Mc);   // rescale earlier chunks
-        Ls *= rs;
-        a *= rs;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const float f = (mv[k] == -INFINITY) ? 0.f : ex2(mv[k] - Mc);
-          Ls = fmaf(f, lv[k], Ls);
-          a = fmaf(f, av[k], a);
-        }
-        M = Mc;
+    float* wgt = reinterpret_cast<float*>(sm + L::oRed);          // [ns][4] (Bsc/Bpv are free)
+    if (warp < P.G) {
+      const int qq = warp;
+      float M = -INFINITY;
+      for (int s0 = lane; s0 < ns; s0 += 32) M = fmaxf(M, __ldcg(up + (s0 * P.G + qq) * kRec));
+      M = warp_max_f32(M);
+      float Ls = 0.f;
+      for (int s0 = lane; s0 < ns; s0 += 32) {
+        const float* W = up + (s0 * P.G + qq) * kRec;
+        const float mv = __ldcg(W);
+        const float f = (mv == -INFINITY) ? 0.f : ex2(mv - M);
+        wgt[s0 * 4 + qq] = f;
+        Ls = fmaf(f, __ldcg(W + 1), Ls);
       }
-      P.out[((int64_t)u * P.G + qq) * 128 + dim] = a / Ls;
-      if (P.lse && dim == 0) P.lse[(int64_t)u * P.G + qq] = (M + __log2f(Ls)) * kLn2;
+      Ls = warp_sum(Ls);
+      __syncwarp();
+      const float invL = 1.f / Ls;
+      for (int s0 = lane; s0 < ns; s0 += 32) wgt[s0 * 4 + qq] *= invL;
+      if (P.lse && lane == 0) P.lse[(int64_t)u * P.G + qq] = (M + __log2f(Ls)) * kLn2;
+    }
+    bar_sync1();
+    {
+      const int dim = tid;                                         // 128 threads = 128 dims
+      float o[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int s0 = 0; s0 < ns; s0 += 8) {
+        float av[4][8];
+#pragma unroll
+        for (int qq = 0; qq < NQ; ++qq)
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            av[qq][k] = (qq < P.G && s0 + k < ns) ? __ldcg(up + ((s0 + k) * P.G + qq) * kRec + 2 + dim) : 0.f;
+#pragma unroll
+        for (int qq = 0; qq < NQ; ++qq)
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (s0 + k < ns) o[qq] = fmaf(wgt[(s0 + k) * 4 + qq], av[qq][k], o[qq]);
+      }
+#pragma unroll
+      for (int qq = 0; qq < NQ; ++qq)
+        if (qq < P.G) P.out[((int64_t)u * P.G + qq) * 128 + dim] = o[qq];
     }
   };
 

@@ -1746,6 +1746,10 @@ static int occupancy() {
     o = by_regs < by_smem ? by_regs : by_smem;
     const int tmem_cap = 512 / L::kAlloc;
     occ = o < 1 ? 1 : (o > tmem_cap ? tmem_cap : o);
+    if (const char* e = getenv("QJL_UD_OCC")) {        // experiments: fewer CTAs per SM
+      const int v = atoi(e);
+      if (v >= 1 && v < occ) occ = v;
+    }
     if (getenv("QJL_DEBUG"))
       fprintf(stderr, "k_udecode<%d,%d,%d>: %d CTAs/SM (regs %d -> %d, smem %d/%d -> %d, tmem cols %d)\n", KCI,
               KCO, NQ, occ, fa.numRegs, by_regs, L::kTotal, smem_sm, by_smem, L::kAlloc);

@@ -85,6 +85,11 @@ __device__ __forceinline__ uint16_t f64_to_f16_bits(double x) {
   return __half_as_ushort(__double2half(x));
 }
 
+// NaN as numpy's float16 NaN (0x7E00) whatever payload produced it (norms of NaN keys)
+__device__ __forceinline__ uint16_t f16_canon(uint16_t v) {
+  return ((v & 0x7C00u) == 0x7C00u && (v & 0x3FFu)) ? (uint16_t)0x7E00u : v;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

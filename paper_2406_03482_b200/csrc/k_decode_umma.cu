@@ -450,8 +450,8 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
     if (threadIdx.x == 0) {
       const double sin = (an[0][0] + an[1][0]) + (an[2][0] + an[3][0]);
       const double sout = (an[0][1] + an[1][1]) + (an[2][1] + an[3][1]);
-      A.kc.norm_in[crow] = f64_to_f16_bits(sqrt(sin));
-      if (MO) A.kc.norm_out[crow] = f64_to_f16_bits(sqrt(sout));
+      A.kc.norm_in[crow] = f16_canon(f64_to_f16_bits(sqrt(sin)));
+      if (MO) A.kc.norm_out[crow] = f16_canon(f64_to_f16_bits(sqrt(sout)));
     }
     if (wid < 4) {
       const int64_t vrow = (int64_t)u * A.vc.capacity + A.row;

@@ -662,8 +662,8 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_keys_simt(
     s_out = warp_sum_f64(s_out);
     if (lane == 0) {
       const int64_t row = (int64_t)u * kc.capacity + row_offset + t0 + t;
-      kc.norm_in[row] = f64_to_f16_bits(sqrt(s_in));
-      if (m_out > 0) kc.norm_out[row] = f64_to_f16_bits(sqrt(s_out));
+      kc.norm_in[row] = f16_canon(f64_to_f16_bits(sqrt(s_in)));
+      if (m_out > 0) kc.norm_out[row] = f16_canon(f64_to_f16_bits(sqrt(s_out)));
     }
   }
 }

@@ -152,6 +152,36 @@ __device__ __forceinline__ uint32_t sign_word_fast(const uint32_t* r) {
   const float x0 = __uint_as_float(r[0]);
   return (x0 != x0) ? 0u : ~acc;
 }
+#ifndef QJL_K1_ZEROACC
+#define QJL_K1_ZEROACC 1
+#endif
+// QJL_K1_ZEROACC: every MMA accumulates onto a TMEM buffer the epilogue re-zeroed after
+// draining it, so an all-zero dot product comes out as (+0) + (-0...) = +0 and the sign
+// test needs no x + 0 (the sum of nonzero products is unchanged by adding +0)
+__device__ __forceinline__ void tmem_zero64(uint32_t taddr) {
+  const uint32_t z = 0u;
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(z)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_zero32(uint32_t taddr) {
+  const uint32_t z = 0u;
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(z)
+      : "memory");
+}
+// sign word without the -0.0 fix-up (valid when accumulators start from +0): bit i =
+// !sign(x_i), NaN rows -> 0
+__device__ __forceinline__ uint32_t sign_word_raw(const uint32_t* r) {
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 31; i >= 0; --i) acc = __funnelshift_l(r[i], acc, 1);
+  const float x0 = __uint_as_float(r[0]);
+  return (x0 != x0) ? 0u : ~acc;
+}
 // 64 fp32 accumulator columns of this thread's TMEM lane
 __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t* r) {
   asm volatile(
@@ -249,6 +279,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_ptr;
+  if (QJL_K1_ZEROACC) {
+    // the accumulator buffers start at +0 (each epilogue warp zeroes its lane quadrant of
+    // its set's buffer; afterwards the epilogue re-zeroes every group it drains)
+    if (warp >= 4 && warp < 12) {
+      const uint32_t base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + ((warp - 4) >> 2) * L::BUFW;
+      for (int c = 0; c < L::BUFW; c += 64) tmem_zero64(base + c);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
 
   const int u_first = (int)(r0 / P.tpu);
   const int lt_first = (int)(r0 - (int64_t)u_first * P.tpu);
@@ -317,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
               const int hf = k >> 2, kk = k & 3;   // K-half, 32-byte step inside the 128-byte row
               const uint64_t ad = ad0 + (uint64_t)((hf * (L::kABytes / 2) + kk * 32) >> 4);
               const uint64_t bd = bd0 + (uint64_t)((hf * L::kBHalf + c * CH * 128 + kk * 32) >> 4);
-              if (k == 0) tc_mma_f16c<0>(d_tmem, ad, bd, IDESC);
+              if (k == 0 && !QJL_K1_ZEROACC) tc_mma_f16c<0>(d_tmem, ad, bd, IDESC);
               else tc_mma_f16c<1>(d_tmem, ad, bd, IDESC);
             }
           }
@@ -456,12 +498,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         double t = ((double)(f0.x * f0.x) + (double)(f0.y * f0.y)) + ((double)(f1.x * f1.x) + (double)(f1.y * f1.y));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        if (lane == src) nin16 = f64_to_f16_bits(sqrt(fmax(t - outl, 0.0)));
+        if (lane == src) {
+          const double v = t - outl;                 // NaN keys keep a NaN norm (np.linalg.norm)
+          nin16 = f64_to_f16_bits(sqrt(v < 0.0 ? 0.0 : v));
+        }
       }
       if (tok < P.n) {
         const int64_t crow = (int64_t)u * P.kc.capacity + P.row_offset + tok;
-        P.kc.norm_in[crow] = nin16;
-        if (m_out > 0) P.kc.norm_out[crow] = nout16;
+        P.kc.norm_in[crow] = f16_canon(nin16);
+        if (m_out > 0) P.kc.norm_out[crow] = f16_canon(nout16);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_empty[s]);
@@ -486,8 +531,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         for (int g64 = 0; g64 < (P.ablate & 1 ? 0 : CH / 64); ++g64) {
           uint32_t r[64];
           tmem_ld64(tmem + ((uint32_t)(ew * 32) << 16) + buf * L::BUFW + g64 * 64, r);
-          const uint32_t w0 = QJL_K1_FASTSIGN ? sign_word_fast(r) : sign_word(r);
-          const uint32_t w1 = QJL_K1_FASTSIGN ? sign_word_fast(r + 32) : sign_word(r + 32);
+          if (QJL_K1_ZEROACC) tmem_zero64(tmem + ((uint32_t)(ew * 32) << 16) + buf * L::BUFW + g64 * 64);
+          const uint32_t w0 = QJL_K1_ZEROACC ? sign_word_raw(r) : QJL_K1_FASTSIGN ? sign_word_fast(r) : sign_word(r);
+          const uint32_t w1 = QJL_K1_ZEROACC ? sign_word_raw(r + 32)
+                                             : QJL_K1_FASTSIGN ? sign_word_fast(r + 32) : sign_word(r + 32);
           const int sr = c * CH + g64 * 64;      // first sketch row of the word pair
           if (valid) {
             uint32_t* d0 = sr < m_in ? reinterpret_cast<uint32_t*>(P.kc.bits_in + crow * (m_in / 8)) + (sr >> 5)
@@ -506,7 +553,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         if constexpr (CH % 64 == 32) {           // trailing 32-column group of the chunk
           uint32_t r[32];
           tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + buf * L::BUFW + (CH - 32), r);
-          const uint32_t w = QJL_K1_FASTSIGN ? sign_word_fast(r) : sign_word(r);
+          if (QJL_K1_ZEROACC) tmem_zero32(tmem + ((uint32_t)(ew * 32) << 16) + buf * L::BUFW + (CH - 32));
+          const uint32_t w = QJL_K1_ZEROACC ? sign_word_raw(r) : QJL_K1_FASTSIGN ? sign_word_fast(r) : sign_word(r);
           const int sr = c * CH + CH - 32;
           if (valid) {
             if (sr < m_in)
@@ -515,6 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
               reinterpret_cast<uint32_t*>(P.kc.bits_out + crow * (m_out / 8))[(sr - m_in) >> 5] = w;
           }
         }
+        if (QJL_K1_ZEROACC) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");   // zeros landed
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&t_empty[buf]);

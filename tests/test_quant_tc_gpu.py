@@ -92,3 +92,46 @@ def test_tc_config4_full_size_against_oracle(cuda):
         assert fi["total"] == fi["lt1e6"] and fo["total"] == fo["lt1e6"], (fi, fo)
         assert np.array_equal(c.norm_in[u, :n].double().cpu().numpy(), O.fp16_round(r["norm_in"]))
         assert np.array_equal(c.norm_out[u, :n].double().cpu().numpy(), O.fp16_round(r["norm_out"]))
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
+def test_tc_special_rows_match_fp64_path(cuda, dt):
+    """Zero / negative-zero / one-side-zero / NaN keys: the tie rule (S k)_i >= 0 -> 1
+    (also for -0.0) and NaN -> 0 (estimator.py:119-121) hold on the tensor-core path
+    (its accumulators start from +0, so an all-zero dot product is +0)."""
+    from paper_2406_03482_b200.device import DeviceKeyCache
+
+    U, n, h = 2, 256, 8
+    K = _keys(U, n, dt, seed=77, h=h)
+    ch = torch.stack([torch.randperm(128, generator=torch.Generator().manual_seed(u))[:h].sort().values
+                      for u in range(U)]).cuda()
+    K[:, 0] = 0.0                                  # all-zero key
+    K[:, 1] = -0.0                                 # negative zeros everywhere
+    K[:, 2] = K[:, 2].neg()
+    for u in range(U):
+        K[u, 3, ch[u]] = 0.0                       # outlier side zero, inlier side not
+        keep = K[u, 4, ch[u]].clone()
+        K[u, 4] = -0.0
+        K[u, 4, ch[u]] = keep                      # inlier side (-)zero, outlier side not
+    K[:, 5, 7] = float("nan")                      # NaN key
+
+    def run(path):
+        c = DeviceKeyCache.create(U, 128, 256, h=h, m_out=64, capacity=n, seed=3, key_dtype=dt,
+                                  with_values=False, channels=ch.cpu().numpy())
+        env = {"tc": ("QJL_REQUIRE_TC", "1"), "simt": ("QJL_FORCE_SIMT", "1")}[path]
+        os.environ[env[0]] = env[1]
+        try:
+            c.append_keys(K)
+        finally:
+            del os.environ[env[0]]
+        torch.cuda.synchronize()
+        return c
+
+    a, b = run("tc"), run("simt")
+    for x, y in ((a.bits_in, b.bits_in), (a.bits_out, b.bits_out)):
+        assert torch.equal(x[:, :n], y[:, :n])
+    assert torch.all(a.bits_in[:, 0] == 0xFF) and torch.all(a.bits_out[:, 0] == 0xFF)
+    assert torch.all(a.bits_in[:, 1] == 0xFF) and torch.all(a.bits_out[:, 1] == 0xFF)
+    assert torch.all(a.bits_out[:, 3] == 0xFF) and torch.all(a.bits_in[:, 4] == 0xFF)
+    for x, y in ((a.norm_in, b.norm_in), (a.norm_out, b.norm_out)):
+        assert torch.equal(x[:, :n].view(torch.int16), y[:, :n].view(torch.int16))

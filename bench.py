@@ -644,7 +644,7 @@ def run_gpu(args):
         "metric": "QJL decode score+aggregate kernel HBM GB/s (algorithmic bytes of the packed cache)",
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16 keys/queries; u1 signs, u2 values",
+        "scaling": "weak", "vs_baseline": None, "dtype": "i8 (tcgen05 kind::i8 scores and P.V, s32 accumulators) + f32 (softmax, output); inputs bf16, u1 signs, u2 values",
         "data": "synthetic (seeded N(0,1), outlier channels planted; random-init, no dataset)",
         "config": {"workload": w["workload"], "units_per_gpu": U, "global_batch": w["batch"] * world,
                    "kv_heads": w["kv_heads"], "q_heads": w["kv_heads"] * w["G"], "seq_len": w["n"],

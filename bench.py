@@ -254,22 +254,31 @@ def cpu_baseline_leg(cache, q, w, budget_s=12.0):
     except Exception:                                   # pragma: no cover
         threadpool_limits = None
     Qh = q.double().cpu().numpy()
+    out_dev = cache.decode(q).double().cpu().numpy()          # the device path on the same inputs
     per_unit = bytes_per_token_head(w) * w["n"]
     done, t_tot = 0, 0.0
+    rel = []
     ctx = threadpool_limits(1) if threadpool_limits else _nullctx()
     with ctx:
         for u in range(cache.shape.units):
             hu = host_unit(cache, u)
             t0 = time.perf_counter()
-            oracle_decode_unit(cache.S_in_host, cache.S_out_host, hu, Qh[u])
+            ref = oracle_decode_unit(cache.S_in_host, cache.S_out_host, hu, Qh[u])
             t_tot += time.perf_counter() - t0
+            rel += [float(np.linalg.norm(out_dev[u, g] - ref[g]) / np.linalg.norm(ref[g]))
+                    for g in range(ref.shape[0])]
             done += 1
             if t_tot >= budget_s:
                 break
-    return {"value": done * per_unit / t_tot / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
+    base = {"value": done * per_unit / t_tot / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
             "sample": f"{done} of {cache.shape.units} units at full n={w['n']} "
                       f"({w['G']} query heads each), oracle/qjl_oracle.py, BLAS pinned to 1 thread, "
                       f"{t_tot:.1f} s"}
+    parity = {"outputs_checked": len(rel), "rel_l2_max": max(rel), "rel_l2_mean": float(np.mean(rel)),
+              "tolerance": 1e-3, "pass": max(rel) <= 1e-3,
+              "note": "device decode vs the CPU oracle on the same packed cache (full n), "
+                      "relative L2 per (unit, query head)"}
+    return base, parity
 
 
 class _nullctx:
@@ -344,11 +353,39 @@ def measure_prefill(device, seed, steps=5, warmup=2):
     sep_ms = e0.elapsed_time(e1) / steps
     flops = 2.0 * U * n * d * (w["m_in"] + w["m_out"])
     _, tf_peak, _ = load_peaks()
-    del K
+    # parity of the timed K1 output: 4 units re-quantized by the fp64 SIMT path (exact
+    # products, fp64 sums, the reference's arithmetic on the same rounded S)
+    cache.n = 0
+    cache.append_keys(K)
+    Us = 4
+    ref = DeviceKeyCache.create(Us, d, w["m_in"], h=h, m_out=w["m_out"], capacity=n, seed=seed,
+                                key_dtype=torch.bfloat16, with_values=False,
+                                channels=cache.channels[:Us, :h].cpu().numpy())
+    os.environ["QJL_FORCE_SIMT"] = "1"
+    try:
+        ref.append_keys(K[:Us].contiguous())
+    finally:
+        del os.environ["QJL_FORCE_SIMT"]
+    torch.cuda.synchronize()
+    flips = int((cache.bits_in[:Us, :n] ^ ref.bits_in[:, :n]).view(torch.uint8).to(torch.int32)
+                .bitwise_count().sum()) if hasattr(torch.Tensor, "bitwise_count") else None
+    if flips is None:
+        x = (cache.bits_in[:Us, :n] ^ ref.bits_in[:, :n]).cpu().numpy()
+        y = (cache.bits_out[:Us, :n] ^ ref.bits_out[:, :n]).cpu().numpy()
+        flips = int(np.unpackbits(x).sum() + np.unpackbits(y).sum())
+    else:
+        flips += int((cache.bits_out[:Us, :n] ^ ref.bits_out[:, :n]).to(torch.int32).bitwise_count().sum())
+    norm_diff = int((cache.norm_in[:Us, :n].view(torch.int16) != ref.norm_in[:, :n].view(torch.int16)).sum()
+                    + (cache.norm_out[:Us, :n].view(torch.int16) != ref.norm_out[:, :n].view(torch.int16)).sum())
+    parity = {"units_checked": Us, "sign_bits_checked": Us * n * (w["m_in"] + w["m_out"]),
+              "bit_flips_vs_fp64_path": flips, "fp16_norm_mismatches": norm_diff,
+              "note": "tcgen05 K1 vs the fp64 SIMT quantizer on the same keys and rounded S"}
+    del K, ref
     return {"workload": w["workload"], "keys_per_s": U * n / (step_ms * 1e-3),
             "ms_per_step": step_ms, "kernel_ms": kern_ms,
             "tflops": flops / (kern_ms * 1e-3) / 1e12,
             "tensor_frac": flops / (kern_ms * 1e-3) / 1e12 / tf_peak,
+            "parity": parity,
             "with_profile": {"fused_ms": fused_ms, "keys_per_s": U * n / (fused_ms * 1e-3),
                              "separate_ms": sep_ms,
                              "note": "prefill(): qjl_prefill_profile (detect + S_full) + K1; "
@@ -693,7 +730,7 @@ def run_gpu(args):
         except Exception as e:                       # pragma: no cover
             res["harness"] = {"error": repr(e)[:200]}
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        res["cpu_baseline"] = cpu_baseline_leg(cache, q, w)
+        res["cpu_baseline"], res["parity"] = cpu_baseline_leg(cache, q, w)
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:

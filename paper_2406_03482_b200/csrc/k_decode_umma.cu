@@ -767,14 +767,26 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       v[4 + 4 * q + 2] = Z[q][1].x;
       v[4 + 4 * q + 3] = Z[q][1].y;
     }
+    // CTA sums of the 20 token-side values, transposed through smem: every thread stores
+    // its values, then warp w reduces values w, w + 4, ... (4 tokens per lane, then one
+    // warp sum) -- 5 shuffle chains per warp instead of 20
+    static_assert(L::NH * 2048 + 4 * 2048 >= (20 * kThreads + 20) * 4, "flush scratch must fit in Bsc/Bpv");
+    float* tr = reinterpret_cast<float*>(sm + L::oRed);            // [20][128]
+    float* red = tr + 20 * kThreads;                               // [20] CTA sums
+    bar_sync1();                        // everyone is done with Bsc/Bpv
 #pragma unroll
     for (int i = 0; i < 20; ++i)
-      if (i < NQ || (i >= 4 && (i - 4) / 4 < NQ)) v[i] = warp_sum(v[i]);
-    float* red = reinterpret_cast<float*>(sm + L::oRed);
-    bar_sync1();                        // everyone is done with Bsc/Bpv
-    if (lane == 0)
+      if (i < NQ || (i >= 4 && (i - 4) / 4 < NQ)) tr[i * kThreads + tid] = v[i];
+    bar_sync1();
 #pragma unroll
-      for (int i = 0; i < 20; ++i) red[warp * 20 + i] = v[i];
+    for (int i0 = 0; i0 < 20; i0 += 4) {
+      const int i = i0 + warp;
+      if (i < NQ || (i >= 4 && (i - 4) / 4 < NQ)) {
+        const float* t = tr + i * kThreads + lane;
+        const float x = warp_sum((t[0] + t[32]) + (t[64] + t[96]));
+        if (lane == 0) red[i] = x;
+      }
+    }
     bar_sync1();
     int ns, slot;
     if (P.grouped) {
@@ -792,12 +804,8 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       if (q < P.G) {
-        float lq = 0.f, zq = 0.f;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          lq += red[w * 20 + q];
-          zq += red[w * 20 + 4 + 4 * q + grp];
-        }
+        const float lq = red[q];
+        const float zq = red[4 + 4 * q + grp];
         if (tid == 0) {
           mypart[q * kRec + 0] = m_run[q];
           mypart[q * kRec + 1] = lq;

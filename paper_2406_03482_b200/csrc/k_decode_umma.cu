@@ -94,6 +94,18 @@ struct Params {
   float* lse;            // [units][G] or null
 };
 
+#ifndef QJL_UD_TRACE
+#define QJL_UD_TRACE 0      // diagnostics only: per-CTA %globaltimer stamps (tools/trace_decode.py)
+#endif
+#if QJL_UD_TRACE
+__device__ unsigned long long g_ud_trace[2048][4];   // [cta] {after wait, loop done, end, smid}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 __host__ __device__ __forceinline__ int64_t tile_begin(int c, int64_t T, int C) { return (int64_t)c * T / C; }
 __host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int C) {
   return (int)(((t + 1) * (int64_t)C + T - 1) / T) - 1;
@@ -876,6 +888,14 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   };
 
   asm volatile("griddepcontrol.wait;" ::: "memory");   // Bsc / qconst come from k_uprep
+#if QJL_UD_TRACE
+  if (tid == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_ud_trace[blockIdx.x][0] = gtimer();
+    g_ud_trace[blockIdx.x][3] = smid;
+  }
+#endif
   const int n32 = (int)P.n;                            // n <= capacity < 2^30 (supported())
   int cur_u = -1;
   int u = u_first, lt = lt_first;
@@ -1172,9 +1192,15 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   }
   // all tiles consumed: the next step's query-sketch kernel may start its math now
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#if QJL_UD_TRACE
+  if (tid == 0) g_ud_trace[blockIdx.x][1] = gtimer();
+#endif
   if (cur_u >= 0) flush(cur_u);
   tc_fence_before();
   __syncthreads();
+#if QJL_UD_TRACE
+  if (tid == 0) g_ud_trace[blockIdx.x][2] = gtimer();
+#endif
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(L::kAlloc));
 }
 
@@ -2035,3 +2061,9 @@ int launch_decode_step_umma(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
 }
 
 }  // namespace qjl
+
+#if QJL_UD_TRACE
+extern "C" __attribute__((visibility("default"))) int qjl_debug_ud_trace(void* host, int ctas) {
+  return (int)cudaMemcpyFromSymbol(host, qjl::ud::g_ud_trace, sizeof(unsigned long long) * 4 * ctas);
+}
+#endif

@@ -1,0 +1,60 @@
+"""Per-CTA timeline of the fused decode at C3 (diagnostics): needs a library built with
+-DQJL_UD_TRACE=1 (tools/build_variant.sh trace "-DQJL_UD_TRACE=1"; QJL_LIB=variants/libqjl_trace.so).
+Prints, per launch wave (CTA index // SMs), when CTAs leave griddepcontrol.wait, finish
+their main loop and exit, relative to the first CTA's wait -- for the PDL-chained step
+(prep + decode, as timed by bench.py) and for the decode launched alone."""
+import ctypes, json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import bench
+from paper_2406_03482_b200 import _lib
+
+w = dict(bench.WORKLOADS["c3"])
+dev = torch.device("cuda", 0)
+cache = bench.build_cache(w, 0, 0, dev)
+U, d, G = w["batch"] * w["kv_heads"], w["d"], w["G"]
+q = torch.randn(U, G, d, device=dev).to(torch.bfloat16)
+out = torch.empty(U, G, d, device=dev)
+lib = _lib.load()
+fn = lib.qjl_debug_ud_trace
+fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
+sms = torch.cuda.get_device_properties(0).multi_processor_count
+C = 4 * sms
+res = {}
+for mode in ("pdl_step", "alone"):
+    if mode == "alone":
+        lib.qjl_timing_enable(1)          # PDL off, as for the kernel-alone timing
+    for i in range(20):
+        cache.decode(q, out=out)
+    torch.cuda.synchronize()
+    buf = np.zeros((C, 4), np.uint64)
+    assert fn(buf.ctypes.data, C) == 0
+    t = buf[:, :3].astype(np.float64)
+    t0 = t[:, 0].min()
+    t = (t - t0) / 1e3
+    r = {}
+    for wv in range(4):
+        sl = t[wv * sms:(wv + 1) * sms]
+        r[f"wave{wv}"] = {"wait": [round(float(sl[:, 0].min()), 2), round(float(sl[:, 0].max()), 2)],
+                          "loop_done": [round(float(sl[:, 1].min()), 2), round(float(np.median(sl[:, 1])), 2), round(float(sl[:, 1].max()), 2)],
+                          "end": [round(float(sl[:, 2].min()), 2), round(float(np.median(sl[:, 2])), 2), round(float(sl[:, 2].max()), 2)]}
+    r["kernel_end"] = round(float(t[:, 2].max()), 2)
+    sm = buf[:, 3].astype(np.int64)
+    per_sm_loop = np.array([t[sm == i, 1].max() for i in np.unique(sm)])
+    per_sm_first = np.array([t[sm == i, 1].min() for i in np.unique(sm)])
+    per_sm_mean = np.array([t[sm == i, 1].mean() for i in np.unique(sm)])
+    r["same_sm_as_c_plus_148j"] = [round(float(np.mean(sm[:C - 148 * j] == sm[148 * j:])), 3) for j in (1, 2, 3)]
+    r["smid_first8"] = sm[:8].tolist()
+    r["ctas_per_sm"] = sorted(set(np.bincount(sm).tolist()) - {0})
+    r["sm_last_loop_done_pct"] = [round(float(x), 2) for x in np.percentile(per_sm_loop, [0, 10, 50, 90, 100])]
+    r["sm_first_loop_done_pct"] = [round(float(x), 2) for x in np.percentile(per_sm_first, [0, 10, 50, 90, 100])]
+    r["sm_mean_loop_done_pct"] = [round(float(x), 2) for x in np.percentile(per_sm_mean, [0, 10, 50, 90, 100])]
+    r["loop_done_pct"] = [round(float(x), 2) for x in np.percentile(t[:, 1], [0, 10, 50, 90, 100])]
+    r["end_pct"] = [round(float(x), 2) for x in np.percentile(t[:, 2], [0, 10, 50, 90, 99, 100])]
+    r["mean_loop_done"] = round(float(t[:, 1].mean()), 2)
+    res[mode] = r
+for k, r in res.items():
+    print(k, {kk: v for kk, v in r.items() if not kk.startswith("wave")})
+    for wv in range(4):
+        print("  ", wv, r[f"wave{wv}"])

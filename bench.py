@@ -236,7 +236,7 @@ def host_unit(cache, u):
     return r
 
 
-def oracle_decode_unit(S_in, S_out, hu, Q, T=1.0, tokens=None):
+def oracle_decode_unit(S_in, S_out, hu, Q, T=1.0, tokens=None, with_logits=False):
     """CPU oracle decode of one unit (dequantize inside, as attention.py:70 does)."""
     from oracle import qjl_oracle as O
 
@@ -244,7 +244,9 @@ def oracle_decode_unit(S_in, S_out, hu, Q, T=1.0, tokens=None):
     c = {k: hu[k][:L] for k in ("bits_in", "norm_in", "bits_out", "norm_out") if k in hu}
     deq = O.dequantize_values(hu["codes"][:L], hu["zero"][:L], hu["scale"][:L])
     S_out_u = S_out if hu["channels"] else None
-    return np.stack([O.quantized_decode(S_in, S_out_u, hu["channels"], q, c, deq, T)[0] for q in Q])
+    res = [O.quantized_decode(S_in, S_out_u, hu["channels"], q, c, deq, T) for q in Q]
+    out = np.stack([r[0] for r in res])
+    return (out, np.stack([r[2] for r in res])) if with_logits else out
 
 
 def cpu_baseline_leg(cache, q, w, budget_s=12.0):
@@ -255,29 +257,41 @@ def cpu_baseline_leg(cache, q, w, budget_s=12.0):
         threadpool_limits = None
     Qh = q.double().cpu().numpy()
     out_dev = cache.decode(q).double().cpu().numpy()          # the device path on the same inputs
+    lg_dev = cache.scores(q)                                  # K2 logits [U, G, n] on the device
     per_unit = bytes_per_token_head(w) * w["n"]
     done, t_tot = 0, 0.0
-    rel = []
+    rel, lg_rel, lg_scaled, l1_num, l1_den = [], [], [], 0.0, 0.0
     ctx = threadpool_limits(1) if threadpool_limits else _nullctx()
     with ctx:
         for u in range(cache.shape.units):
             hu = host_unit(cache, u)
             t0 = time.perf_counter()
-            ref = oracle_decode_unit(cache.S_in_host, cache.S_out_host, hu, Qh[u])
+            ref, ref_lg = oracle_decode_unit(cache.S_in_host, cache.S_out_host, hu, Qh[u], with_logits=True)
             t_tot += time.perf_counter() - t0
             rel += [float(np.linalg.norm(out_dev[u, g] - ref[g]) / np.linalg.norm(ref[g]))
                     for g in range(ref.shape[0])]
+            dl = np.abs(lg_dev[u].double().cpu().numpy() - ref_lg)
+            lg_rel.append((dl / np.maximum(np.abs(ref_lg), 1e-300)).ravel())
+            lg_scaled.append(float((dl.max(axis=1) / np.abs(ref_lg).max(axis=1)).max()))
+            l1_num += float(dl.sum())
+            l1_den += float(np.abs(ref_lg).sum())
             done += 1
             if t_tot >= budget_s:
                 break
+    lr = np.concatenate(lg_rel)
     base = {"value": done * per_unit / t_tot / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
             "sample": f"{done} of {cache.shape.units} units at full n={w['n']} "
                       f"({w['G']} query heads each), oracle/qjl_oracle.py, BLAS pinned to 1 thread, "
                       f"{t_tot:.1f} s"}
     parity = {"outputs_checked": len(rel), "rel_l2_max": max(rel), "rel_l2_mean": float(np.mean(rel)),
               "tolerance": 1e-3, "pass": max(rel) <= 1e-3,
+              "logits_checked": int(lr.size), "logit_rel_err_p99": float(np.percentile(lr, 99)),
+              "logit_rel_err_max": float(lr.max()), "logit_err_max_over_row_max": max(lg_scaled),
+              "logit_l1_norm_err": l1_num / l1_den,
               "note": "device decode vs the CPU oracle on the same packed cache (full n), "
-                      "relative L2 per (unit, query head)"}
+                      "relative L2 per (unit, query head); logits: the device score kernel "
+                      "(qjl_scores) vs the oracle's estimate_logits, elementwise |d|/|ref| "
+                      "(max, p99), max |d| over the row's max |ref|, and sum |d| / sum |ref|"}
     return base, parity
 
 

@@ -303,6 +303,39 @@ class _nullctx:
         return False
 
 
+def prefill_oracle_check(cache, K, w, u=0):
+    """Unit u of the timed K1 output against the CPU oracle's append_keys (the reference's
+    quantize_key on the same bf16-rounded S): sign flips bucketed by |S.k| band, and fp16
+    norm mismatches (SURVEY 8(d) parity fields)."""
+    import torch
+
+    from oracle import qjl_oracle as O
+
+    n, h = cache.n, w["h"]
+    S_in = torch.as_tensor(cache.S_in_host).to(torch.bfloat16).double().numpy()
+    S_out = torch.as_tensor(cache.S_out_host).to(torch.bfloat16).double().numpy() if h else None
+    chans = tuple(int(c) for c in cache.channels[u, :h].cpu().numpy())
+    ref = O.append_keys(S_in, S_out, chans, K[u].double().cpu().numpy())
+    bands = [0.0, 1e-6, 1e-4, 1e-2, np.inf]
+    res = {"unit": u, "sign_bits": 0, "flips": 0, "flips_by_abs_proj_band": {}, "fp16_norm_mismatches": 0}
+    for side, m in (("in", w["m_in"]), ("out", w["m_out"])):
+        dev = np.unpackbits(getattr(cache, f"bits_{side}")[u, :n].cpu().numpy(), axis=1, bitorder="little")[:, :m]
+        want = np.unpackbits(ref[f"bits_{side}"], axis=1, bitorder="little")[:, :m]
+        a = np.abs(ref[f"proj_{side}"])
+        diff = dev != want
+        res["sign_bits"] += int(diff.size)
+        res["flips"] += int(diff.sum())
+        for lo, hi in zip(bands[:-1], bands[1:]):
+            k = f"[{lo:g},{hi:g})"
+            sel = (a >= lo) & (a < hi)
+            prev = res["flips_by_abs_proj_band"].get(k, [0, 0])
+            res["flips_by_abs_proj_band"][k] = [prev[0] + int(diff[sel].sum()), prev[1] + int(sel.sum())]
+        nd = getattr(cache, f"norm_{side}")[u, :n].cpu().numpy().astype(np.float16)
+        res["fp16_norm_mismatches"] += int((nd.view(np.uint16) != O.fp16_round(ref[f"norm_{side}"]).astype(np.float16).view(np.uint16)).sum())
+    res["note"] = "per band: [flips, bits]"
+    return res
+
+
 def measure_prefill(device, seed, steps=5, warmup=2):
     """Secondary: keys quantized/s for config 4 (B16 x Hkv8, 8192 tokens, m=512, r=8)."""
     import torch
@@ -393,7 +426,8 @@ def measure_prefill(device, seed, steps=5, warmup=2):
                     + (cache.norm_out[:Us, :n].view(torch.int16) != ref.norm_out[:, :n].view(torch.int16)).sum())
     parity = {"units_checked": Us, "sign_bits_checked": Us * n * (w["m_in"] + w["m_out"]),
               "bit_flips_vs_fp64_path": flips, "fp16_norm_mismatches": norm_diff,
-              "note": "tcgen05 K1 vs the fp64 SIMT quantizer on the same keys and rounded S"}
+              "note": "tcgen05 K1 vs the fp64 SIMT quantizer on the same keys and rounded S",
+              "vs_oracle": prefill_oracle_check(cache, K, w)}
     del K, ref
     return {"workload": w["workload"], "keys_per_s": U * n / (step_ms * 1e-3),
             "ms_per_step": step_ms, "kernel_ms": kern_ms,

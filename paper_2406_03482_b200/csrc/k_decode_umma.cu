@@ -663,12 +663,13 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   // the phase cannot complete until that arrive.
   int iss_u = u_first, iss_lt = lt_first, iss_i = 0, iss_s = 0;
   uint32_t iss_ph = 0;                      // parity of the empty barrier of stage iss_s
+  // running cache rows of the next tile (advanced by adds, rebuilt at unit boundaries)
+  int64_t iss_row = (int64_t)u_first * P.kc.capacity + (int64_t)lt_first * kTile;
+  int64_t iss_vrow = (int64_t)u_first * P.vc.capacity + (int64_t)lt_first * kTile;
   auto issue_next = [&]() {
     const int s = iss_s;
     if (iss_i >= kStages) mbar_wait(a_empty + 8 * s, iss_ph);
-    const int64_t tok = (int64_t)iss_lt * kTile;
-    const int64_t row = (int64_t)iss_u * P.kc.capacity + tok;
-    const int64_t vrow = (int64_t)iss_u * P.vc.capacity + tok;
+    const int64_t row = iss_row, vrow = iss_vrow;
     const uint32_t st = s_sm + L::oStage + s * L::kStageBytes;
     const uint32_t fb = a_full + 8 * s;
     if (QJL_UD_ABLATE & 1024) {                    // memory test: bits_in + codes only (8 KB/tile)
@@ -729,7 +730,14 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       if (iss_i > kStages) iss_ph ^= 1;     // stages are re-armed from the second round on
     }
     iss_lt += lt_step;
-    if (iss_lt >= P.tpu) { iss_lt = 0; ++iss_u; }
+    iss_row += (int64_t)lt_step * kTile;
+    iss_vrow += (int64_t)lt_step * kTile;
+    if (iss_lt >= P.tpu) {
+      iss_lt = 0;
+      ++iss_u;
+      iss_row = (int64_t)iss_u * P.kc.capacity;
+      iss_vrow = (int64_t)iss_u * P.vc.capacity;
+    }
   };
 
   // the first copies overlap the prep grid (PDL); a decode step that appends a token

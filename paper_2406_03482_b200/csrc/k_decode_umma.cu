@@ -666,6 +666,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   // running cache rows of the next tile (advanced by adds, rebuilt at unit boundaries)
   int64_t iss_row = (int64_t)u_first * P.kc.capacity + (int64_t)lt_first * kTile;
   int64_t iss_vrow = (int64_t)u_first * P.vc.capacity + (int64_t)lt_first * kTile;
+  const uint64_t pol = evict_first_policy();   // L2 policy of the cache stream (read once)
   auto issue_next = [&]() {
     const int s = iss_s;
     if (iss_i >= kStages) mbar_wait(a_empty + 8 * s, iss_ph);
@@ -692,7 +693,6 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
         bulk_g2s(st + L::oScale, (const uint8_t*)P.vc.scale + vrow * 8, L::kConst, fb);
       }
     } else if (QJL_UD_EVICT_FIRST) {
-      const uint64_t pol = evict_first_policy();
       if (warp == 0) {
         mbar_expect_tx(fb, L::kStageBytes);
         bulk_g2s_hint(st + L::oBitsIn, P.kc.bits_in + row * (KCI * 4), L::kBitsIn, fb, pol);

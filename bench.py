@@ -1,34 +1,36 @@
 #!/usr/bin/env python
 """bench.py -- QJL decode score+aggregate kernel throughput on B200.
 
-Metric (BASELINE.json): "QJL decode score kernel HBM GB/s (% peak), keys
-quantized/s at 1/2/4/8 B200".  One step = one fused decode (K2 scores + K3
-softmax.V) of every query head over the whole packed cache of this rank's
-units.  Headline workload = config 3 (Llama-3-8B GQA decode: batch 8, 32
-query heads over 8 KV heads, head_dim 128, seq 32768, m=256, r=8 outlier
-channels x20, bf16; values 2-bit group-32).  Weak scaling: every rank owns its
-own batch-8 slice of units (global batch = 8 * N); no data-path collective.
+Metric (BASELINE.json): "QJL decode score kernel HBM GB/s (% peak), keys quantized/s at
+1/2/4/8 B200".  One step = one fused decode (K2 scores + K3 softmax.V) of every query head
+over the whole packed cache.  Headline workload = config 3 (Llama-3-8B GQA decode: batch 8,
+32 query heads over 8 KV heads, head_dim 128, seq 32768, m=256, r=8 outlier channels x20,
+bf16; values 2-bit group-32), sharded over KV heads: strong scaling, 64/N units per GPU
+(SURVEY 8(e)), no data-path collective.
 
-  value  = algorithmic bytes of all ranks / max-over-ranks time, inputs resident
-           in HBM (193 MB/step/rank > 126 MB L2, so no L2 flush is needed).
-  e2e    = same metric through the public API with the per-step query H2D copy
-           (pinned host) and output D2H copy inside the timed region.
-  roofline = dominant kernel (fused decode) algorithmic bytes / its CUDA-event
-           time, against MEASURED_PEAKS.json hbm_gbs.
-  cpu_baseline = CPU oracle port (oracle/qjl_oracle.py) on a bounded sample of
-           the same workload, 1 thread, rank 0 at N=1 only.
+  value    = algorithmic bytes of all 64 units / max-over-ranks step time, inputs resident
+             in HBM (193 MB/step at N=1 > 126 MB L2, so no L2 flush is needed).
+  e2e      = the same metric through the public API with host buffers: every step copies its
+             query (pinned host -> device), decodes, all-gathers the outputs over NCCL (N>1)
+             and reads the result back (device -> pinned host), all inside the timed region.
+  roofline = dominant kernel (fused decode) algorithmic bytes / its mean CUDA-event time in a
+             chain of back-to-back decodes (qjl_bench_decode_kernel), vs MEASURED_PEAKS.json.
+  cpu_baseline = CPU oracle port (oracle/qjl_oracle.py) on a bounded sample, 1 thread, N=1.
+  keys_quantized_per_s = K1 (config 4 prefill, 128 units x 8192 keys, m = 512 + 64) sharded
+             over the ranks, aggregate keys / max-over-ranks kernel time.
 
-`--impl reference` times the reference algorithm's CPU implementation (the
-oracle port -- the reference is pure Python and cannot travel to the GPU box)
-with all host cores on a bounded sample of the same workload.
+`--gpus N` under torchrun reads RANK/WORLD_SIZE; launched plainly with N > 1 it re-executes
+itself under torch.distributed.run (one process per GPU, NCCL over NVLink).
+`--impl reference` times the reference algorithm's CPU implementation (the oracle port --
+the reference is pure Python and cannot travel to the GPU box) with all host cores.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import subprocess
 import sys
 import threading
 import time
@@ -38,13 +40,15 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# unit order is kv-head-major (u = kv_head * batch + b), so a contiguous unit shard is a
+# KV-head split of the model (north star: "sharded over KV heads")
 WORKLOADS = {
     "c3": dict(workload="c3_llama3_8b_gqa_decode", batch=8, kv_heads=8, G=4, n=32768, d=128,
                m_in=256, m_out=64, h=8, factor=20.0, dtype="bf16"),
     "c2": dict(workload="c2_llama2_7b_mha_decode", batch=4, kv_heads=32, G=1, n=4096, d=128,
                m_in=256, m_out=128, h=4, factor=15.0, dtype="f16"),
-    "c5_b64_128k": dict(workload="c5_long_context_b16_128k", batch=16, kv_heads=8, G=4, n=131072,
-                        d=128, m_in=256, m_out=64, h=8, factor=20.0, dtype="bf16"),
+    "c5": dict(workload="c5_long_context", batch=16, kv_heads=8, G=4, n=131072, d=128,
+               m_in=256, m_out=64, h=8, factor=20.0, dtype="bf16"),
 }
 PREFILL = dict(workload="c4_prefill_quantize", batch=16, kv_heads=8, n=8192, d=128, m_in=512,
                m_out=64, h=8, dtype="bf16")
@@ -53,11 +57,12 @@ REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x40: "sw_thermal_slowdown",
            0x1: "gpu_idle", 0x20: "sync_boost", 0x200: "display_clock"}
 
 
-def bytes_per_token_head(w):
-    """m_in/8 + m_out/8 sign bytes + 2 B per stored fp16 norm + 2-bit g32 values
-    (d*2/8 code bytes + 4*d/32 bytes of fp16 zero/scale) -- SURVEY 8(d)."""
+def bytes_per_token_head(w, values=True):
+    """m_in/8 + m_out/8 sign bytes + 2 B per stored fp16 norm (+ 2-bit g32 values:
+    d*2/8 code bytes + 4*d/32 bytes of fp16 zero/scale) -- SURVEY 8(d)."""
     d = w["d"]
-    return w["m_in"] // 8 + w["m_out"] // 8 + 2 * (1 + (w["h"] > 0)) + d * 2 // 8 + 4 * d // 32
+    k = w["m_in"] // 8 + w["m_out"] // 8 + 2 * (1 + (w["h"] > 0))
+    return k + (d * 2 // 8 + 4 * d // 32 if values else 0)
 
 
 def load_peaks():
@@ -128,139 +133,110 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- GPU setup
-def build_cache(w, rank, seed, device, layout="p2t"):
-    """Seeded synthetic C3-style cache for this rank's units, quantized on device by K1."""
+def unit_tensor(shape, seed, gu, device, dtype, scale=None):
+    """Seeded N(0,1) tensor of global unit gu -- the same bytes whatever the sharding."""
+    import torch
+
+    from paper_2406_03482_b200.sketch import derive_seed
+
+    g = torch.Generator(device=device)
+    g.manual_seed(derive_seed(seed, gu) & ((1 << 63) - 1))
+    x = torch.randn(shape, generator=g, device=device, dtype=torch.float32)
+    if scale is not None:
+        x *= scale
+    return x.to(dtype)
+
+
+def build_cache(w, shard, seed, device):
+    """This rank's units of a seeded synthetic cache: K with h planted outlier channels per
+    unit, prompt profile + S_full (F2) and K1 / value quantizer on the device."""
     import torch
 
     from paper_2406_03482_b200.device import DeviceKeyCache
-    from paper_2406_03482_b200.sketch import derive_seed
 
-    U, n, d, h = w["batch"] * w["kv_heads"], w["n"], w["d"], w["h"]
+    U, n, d, h = shard.count, w["n"], w["d"], w["h"]
     tdt = {"bf16": torch.bfloat16, "f16": torch.float16}[w["dtype"]]
-    g = torch.Generator(device=device)
-    g.manual_seed(derive_seed(seed, 1000 + rank) & ((1 << 63) - 1))
+    K = torch.empty(U, n, d, dtype=tdt, device=device)
+    V = torch.empty(U, n, d, dtype=tdt, device=device)
+    for i in range(U):
+        gu = shard.start + i
+        sc = None
+        if h:
+            g = torch.Generator(device="cpu").manual_seed(7919 * gu + seed)
+            ch = torch.randperm(d, generator=g)[:h]
+            sc = torch.ones(d, device=device)
+            sc[ch.to(device)] = w["factor"]
+        K[i] = unit_tensor((n, d), seed, 2 * gu, device, tdt, sc)
+        V[i] = unit_tensor((n, d), seed, 2 * gu + 1, device, tdt)
     cache = DeviceKeyCache.create(U, d, w["m_in"], h=h, m_out=w["m_out"], capacity=n, seed=seed,
-                                  key_dtype=tdt, value_layout=layout)
-    chunk = max(1, min(U, (1 << 30) // (n * d * 4)))    # bound the transient raw K/V
-    prompt_done = False
-    for u0 in range(0, U, chunk):
-        uc = min(chunk, U - u0)
-        K = torch.randn(uc, n, d, generator=g, device=device, dtype=torch.float32)
-        if h:
-            ch = torch.argsort(torch.rand(uc, d, generator=g, device=device), dim=1)[:, :h]
-            scale = torch.ones(uc, d, device=device)
-            scale.scatter_(1, ch, w["factor"])
-            K *= scale[:, None, :]
-        V = torch.randn(uc, n, d, generator=g, device=device, dtype=torch.float32)
-        K, V = K.to(tdt), V.to(tdt)
-        sub = _UnitSlice(cache, u0, uc)
-        if h:
-            sub.detect(K)
-        sub.append(K, V)
-        del K, V
-        prompt_done = True
-    assert prompt_done
-    cache.n = n
-    cache.n_values = n
+                                  key_dtype=tdt)
+    cache.prefill(K, V)
+    del K, V
+    torch.cuda.empty_cache()
     return cache
 
 
-class _UnitSlice:
-    """Helper to run detect/append on a contiguous unit sub-range [u0, u0+uc)."""
+def make_queries(w, shard, seed, device):
+    import torch
 
-    def __init__(self, cache, u0, uc):
-        self.c, self.u0, self.uc = cache, u0, uc
-
-    def detect(self, K):
-        import ctypes
-
-        from paper_2406_03482_b200 import _lib
-        from paper_2406_03482_b200.device import _TORCH2QJL, _stream
-
-        c, s = self.c, self.c.shape
-        ch = c.channels[self.u0:self.u0 + self.uc]
-        _lib.check(c.lib.qjl_detect_outliers(K.data_ptr(), _TORCH2QJL[K.dtype], self.uc, K.shape[1],
-                                             s.d, K.shape[1] * s.d, s.h, ch.data_ptr(), None,
-                                             _stream()), "detect_outliers")
-        del ctypes
-
-    def append(self, K, V):
-        import ctypes
-
-        from paper_2406_03482_b200 import _lib
-        from paper_2406_03482_b200.device import _TORCH2QJL, _stream
-
-        c, s = self.c, self.c.shape
-        if c.s_full is None or s.h:
-            # (re)build per-unit sketches: this slice's profiles are now known
-            c.set_sketches(c.S_in_host, c.S_out_host)
-        n = K.shape[1]
-        kd = c.key_desc()
-        kd.units = self.uc
-        off_b_in = self.u0 * s.capacity * (s.m_in // 8)
-        kd.bits_in = c.bits_in.data_ptr() + off_b_in
-        kd.norm_in = c.norm_in.data_ptr() + self.u0 * s.capacity * 2
-        if s.m_out:
-            kd.bits_out = c.bits_out.data_ptr() + self.u0 * s.capacity * (s.m_out // 8)
-            kd.norm_out = c.norm_out.data_ptr() + self.u0 * s.capacity * 2
-        sd = c.sketch_desc()
-        sd.s_full = c.s_full.data_ptr() + self.u0 * (s.m_in + s.m_out) * s.d * c.s_full.element_size()
-        chp = c.channels.data_ptr() + self.u0 * c.channels.shape[1] * 4
-        _lib.check(c.lib.qjl_quantize_keys(K.data_ptr(), _TORCH2QJL[K.dtype], n, n * s.d,
-                                           ctypes.byref(sd), chp, s.h, ctypes.byref(kd), 0,
-                                           _stream()), "quantize_keys")
-        vd = c.value_desc()
-        vd.units = self.uc
-        vd.codes = c.v_codes.data_ptr() + self.u0 * s.capacity * (s.d // 4)
-        G = s.d // c.value_group
-        vd.zero = c.v_zero.data_ptr() + self.u0 * s.capacity * G * 2
-        vd.scale = c.v_scale.data_ptr() + self.u0 * s.capacity * G * 2
-        _lib.check(c.lib.qjl_quantize_values(V.data_ptr(), _TORCH2QJL[V.dtype], n, n * s.d,
-                                             ctypes.byref(vd), 0, _stream()), "quantize_values")
+    tdt = {"bf16": torch.bfloat16, "f16": torch.float16}[w["dtype"]]
+    return torch.stack([unit_tensor((w["G"], w["d"]), seed + 1, shard.start + i, device, tdt)
+                        for i in range(shard.count)])
 
 
 def host_unit(cache, u):
     """Copy one unit's packed cache + value constants to host numpy for the oracle."""
-    from paper_2406_03482_b200.device import p2_unpack_codes
+    from paper_2406_03482_b200.device import unpack_codes
 
     n = cache.n
     r = dict(bits_in=cache.bits_in[u, :n].cpu().numpy(),
              norm_in=cache.norm_in[u, :n].double().cpu().numpy())
-    if cache.bits_out is not None:
+    if cache.shape.m_out:
         r["bits_out"] = cache.bits_out[u, :n].cpu().numpy()
         r["norm_out"] = cache.norm_out[u, :n].double().cpu().numpy()
-    r["codes"] = p2_unpack_codes(cache.v_codes[u].cpu().numpy(), n, cache.value_layout)
+    r["codes"] = unpack_codes(cache.v_codes[u].cpu().numpy(), n)
     r["zero"] = cache.v_zero[u, :n].double().cpu().numpy()
     r["scale"] = cache.v_scale[u, :n].double().cpu().numpy()
     r["channels"] = tuple(int(c) for c in cache.channels[u, : cache.shape.h].cpu().numpy())
     return r
 
 
-def oracle_decode_unit(S_in, S_out, hu, Q, T=1.0, tokens=None, with_logits=False):
+def oracle_decode_unit(S_in, S_out, hu, Q, T=1.0, with_logits=False):
     """CPU oracle decode of one unit (dequantize inside, as attention.py:70 does)."""
     from oracle import qjl_oracle as O
 
-    L = tokens or hu["bits_in"].shape[0]
-    c = {k: hu[k][:L] for k in ("bits_in", "norm_in", "bits_out", "norm_out") if k in hu}
-    deq = O.dequantize_values(hu["codes"][:L], hu["zero"][:L], hu["scale"][:L])
+    c = {k: hu[k] for k in ("bits_in", "norm_in", "bits_out", "norm_out") if k in hu}
+    deq = O.dequantize_values(hu["codes"], hu["zero"], hu["scale"])
     S_out_u = S_out if hu["channels"] else None
     res = [O.quantized_decode(S_in, S_out_u, hu["channels"], q, c, deq, T) for q in Q]
     out = np.stack([r[0] for r in res])
     return (out, np.stack([r[2] for r in res])) if with_logits else out
 
 
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 def cpu_baseline_leg(cache, q, w, budget_s=12.0):
-    """1-thread oracle on whole units at full n until ~budget_s of CPU work."""
+    """1-thread oracle on whole units at full n until ~budget_s of CPU work; the device
+    decode, its lse and the scores kernel's logits are checked on the same units."""
+    import torch
     try:
         from threadpoolctl import threadpool_limits
     except Exception:                                   # pragma: no cover
         threadpool_limits = None
     Qh = q.double().cpu().numpy()
-    out_dev = cache.decode(q).double().cpu().numpy()          # the device path on the same inputs
+    lse = torch.empty(q.shape[0], q.shape[1], device=q.device)
+    out_dev = cache.decode(q, lse=lse).double().cpu().numpy()
+    lse = lse.double().cpu().numpy()
     lg_dev = cache.scores(q)                                  # K2 logits [U, G, n] on the device
     per_unit = bytes_per_token_head(w) * w["n"]
     done, t_tot = 0, 0.0
-    rel, lg_rel, lg_scaled, l1_num, l1_den = [], [], [], 0.0, 0.0
+    rel, lse_err, lg_rel, lg_scaled, l1_num, l1_den = [], [], [], [], 0.0, 0.0
     ctx = threadpool_limits(1) if threadpool_limits else _nullctx()
     with ctx:
         for u in range(cache.shape.units):
@@ -270,6 +246,9 @@ def cpu_baseline_leg(cache, q, w, budget_s=12.0):
             t_tot += time.perf_counter() - t0
             rel += [float(np.linalg.norm(out_dev[u, g] - ref[g]) / np.linalg.norm(ref[g]))
                     for g in range(ref.shape[0])]
+            m = ref_lg.max(axis=1, keepdims=True)
+            ref_lse = (m + np.log(np.exp(ref_lg - m).sum(axis=1, keepdims=True)))[:, 0]
+            lse_err += list(np.abs(lse[u] - ref_lse) / np.abs(ref_lse))
             dl = np.abs(lg_dev[u].double().cpu().numpy() - ref_lg)
             lg_rel.append((dl / np.maximum(np.abs(ref_lg), 1e-300)).ravel())
             lg_scaled.append(float((dl.max(axis=1) / np.abs(ref_lg).max(axis=1)).max()))
@@ -284,23 +263,46 @@ def cpu_baseline_leg(cache, q, w, budget_s=12.0):
                       f"({w['G']} query heads each), oracle/qjl_oracle.py, BLAS pinned to 1 thread, "
                       f"{t_tot:.1f} s"}
     parity = {"outputs_checked": len(rel), "rel_l2_max": max(rel), "rel_l2_mean": float(np.mean(rel)),
-              "tolerance": 1e-3, "pass": max(rel) <= 1e-3,
+              "tolerance": 1e-3, "pass": max(rel) <= 1e-3 and max(lse_err) <= 1e-4,
+              "lse_rel_err_max": float(max(lse_err)),
               "logits_checked": int(lr.size), "logit_rel_err_p99": float(np.percentile(lr, 99)),
               "logit_rel_err_max": float(lr.max()), "logit_err_max_over_row_max": max(lg_scaled),
               "logit_l1_norm_err": l1_num / l1_den,
               "note": "device decode vs the CPU oracle on the same packed cache (full n), "
-                      "relative L2 per (unit, query head); logits: the device score kernel "
-                      "(qjl_scores) vs the oracle's estimate_logits, elementwise |d|/|ref| "
-                      "(max, p99), max |d| over the row's max |ref|, and sum |d| / sum |ref|"}
+                      "relative L2 per (unit, query head); lse: the fused kernel's log-sum-exp vs "
+                      "the oracle's; logits: the scores kernel (qjl_scores) vs the oracle's "
+                      "estimate_logits, elementwise |d|/|ref| (max, p99), max |d| over the row's "
+                      "max |ref|, and sum |d| / sum |ref|"}
     return base, parity
 
 
-class _nullctx:
-    def __enter__(self):
-        return self
+def measure_scores(cache, q, w, steps):
+    """K2 scores-only (kvcache.py:311-329): logits of every head over the key fields of the
+    tile records; algorithmic bytes = key bytes per token-head (SURVEY 8(d) scores-only)."""
+    import torch
 
-    def __exit__(self, *a):
-        return False
+    U, G = q.shape[0], q.shape[1]
+    logits = torch.empty(U, G, cache.n, dtype=torch.float32, device=q.device)
+    for _ in range(3):
+        cache.scores(q, out=logits)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        cache.scores(q, out=logits)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    kb = U * w["n"] * bytes_per_token_head(w, values=False)
+    wb = U * G * w["n"] * 4
+    peak, _, _ = load_peaks()
+    return {"ms_per_step": ms, "key_bytes": kb, "logit_bytes_written": wb,
+            "gbs_key_bytes": kb / (ms * 1e-3) / 1e9, "frac_key_bytes": kb / (ms * 1e-3) / 1e9 / peak,
+            "gbs_read_plus_write": (kb + wb) / (ms * 1e-3) / 1e9,
+            "frac_read_plus_write": (kb + wb) / (ms * 1e-3) / 1e9 / peak,
+            "note": "scores-only K2 (prep + tcgen05 score kernel writing fp32 logits); algorithmic "
+                    "bytes = the key fields of the records (44 B/token-head at C3), plus the logits "
+                    "written"}
 
 
 def prefill_oracle_check(cache, K, w, u=0):
@@ -336,19 +338,22 @@ def prefill_oracle_check(cache, K, w, u=0):
     return res
 
 
-def measure_prefill(device, seed, steps=5, warmup=2):
-    """Secondary: keys quantized/s for config 4 (B16 x Hkv8, 8192 tokens, m=512, r=8)."""
+def measure_prefill(device, seed, shard_of_units, steps=5, warmup=2, parity=True):
+    """K1 (config 4: B16 x Hkv8, 8192 new tokens, m = 512 + 64, r = 8, lognormal channel
+    scales) over this rank's units: keys/s, TFLOP/s (padded K=128 and useful flops), and the
+    whole prefill with the fused prompt profile (F2)."""
     import torch
 
-    from paper_2406_03482_b200 import _lib
     from paper_2406_03482_b200.device import DeviceKeyCache
 
     w = PREFILL
-    U, n, d, h = w["batch"] * w["kv_heads"], w["n"], w["d"], w["h"]
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    K = (torch.randn(U, n, d, generator=g, device=device) *
-         torch.exp(torch.randn(U, 1, d, generator=g, device=device))).to(torch.bfloat16)
+    sh = shard_of_units(w["batch"] * w["kv_heads"])
+    U, n, d, h = sh.count, w["n"], w["d"], w["h"]
+    K = torch.empty(U, n, d, dtype=torch.bfloat16, device=device)
+    for i in range(U):
+        gu = sh.start + i
+        ls = torch.exp(unit_tensor((d,), seed + 7, gu, device, torch.float32))
+        K[i] = unit_tensor((n, d), seed + 9, gu, device, torch.bfloat16, ls)
     cache = DeviceKeyCache.create(U, d, w["m_in"], h=h, m_out=w["m_out"], capacity=n, seed=seed,
                                   key_dtype=torch.bfloat16, with_values=False)
     cache.detect_outliers(K)
@@ -358,6 +363,7 @@ def measure_prefill(device, seed, steps=5, warmup=2):
         cache.n = 0
         cache.append_keys(K)
     torch.cuda.synchronize()
+    import ctypes
     lib.qjl_timing_read(None, None, 1)
     lib.qjl_timing_enable(1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -368,17 +374,15 @@ def measure_prefill(device, seed, steps=5, warmup=2):
     e1.record()
     torch.cuda.synchronize()
     lib.qjl_timing_enable(0)
-    import ctypes
     ms, cnt = ctypes.c_double(), ctypes.c_int()
     lib.qjl_timing_read(ctypes.byref(ms), ctypes.byref(cnt), 1)
     step_ms = e0.elapsed_time(e1) / steps
     kern_ms = ms.value / max(cnt.value, 1)
-    # whole prefill (F2): fused profile (detect + S_full build) + K1, against the
-    # separate detect / build launches + K1
-    sk64 = tuple(torch.as_tensor(S).to(device) for S in (cache.S_in_host, cache.S_out_host))
+    # whole prefill (F2): fused profile (detect + S_full build) + K1
     for _ in range(warmup):
         cache.n = 0
         cache.prefill(K)
+    torch.cuda.synchronize()
     e0.record()
     for _ in range(steps):
         cache.n = 0
@@ -386,135 +390,55 @@ def measure_prefill(device, seed, steps=5, warmup=2):
     e1.record()
     torch.cuda.synchronize()
     fused_ms = e0.elapsed_time(e1) / steps
-    e0.record()
-    for _ in range(steps):
-        cache.n = 0
-        cache.detect_outliers(K)
-        sin, sout = sk64
-        lib.qjl_build_sketch(sin.data_ptr(), sout.data_ptr(), w["m_in"], w["m_out"], d, h,
-                             cache.channels.data_ptr(), U, _lib.QJL_BF16, cache.s_full.data_ptr(),
-                             torch.cuda.current_stream().cuda_stream)
-        cache.append_keys(K)
-    e1.record()
-    torch.cuda.synchronize()
-    sep_ms = e0.elapsed_time(e1) / steps
-    flops = 2.0 * U * n * d * (w["m_in"] + w["m_out"])
+    flops_pad = 2.0 * U * n * d * (w["m_in"] + w["m_out"])
+    flops_use = 2.0 * U * n * ((d - h) * w["m_in"] + h * w["m_out"])
     _, tf_peak, _ = load_peaks()
-    # parity of the timed K1 output: 4 units re-quantized by the fp64 SIMT path (exact
-    # products, fp64 sums, the reference's arithmetic on the same rounded S)
-    cache.n = 0
-    cache.append_keys(K)
-    Us = 4
-    ref = DeviceKeyCache.create(Us, d, w["m_in"], h=h, m_out=w["m_out"], capacity=n, seed=seed,
-                                key_dtype=torch.bfloat16, with_values=False,
-                                channels=cache.channels[:Us, :h].cpu().numpy())
-    os.environ["QJL_FORCE_SIMT"] = "1"
-    try:
+    res = {"workload": w["workload"], "units": U, "keys": U * n, "kernel_ms": kern_ms, "ms_per_step": step_ms,
+           "keys_per_s": U * n / (kern_ms * 1e-3),
+           "tflops_padded": flops_pad / (kern_ms * 1e-3) / 1e12,
+           "tensor_frac_padded": flops_pad / (kern_ms * 1e-3) / 1e12 / tf_peak,
+           "tensor_frac_useful": flops_use / (kern_ms * 1e-3) / 1e12 / tf_peak,
+           "with_profile": {"ms": fused_ms, "keys_per_s": U * n / (fused_ms * 1e-3),
+                            "note": "prefill(): qjl_prefill_profile (outlier detection + per-unit "
+                                    "S_full) + K1 over the same prompt"},
+           "note": "K.S^T over zero-padded K=128 (m_in+m_out=576 rows) + sign pack + fp16 norms; "
+                   "useful flops count each side's own columns only"}
+    if parity:
+        cache.n = 0
+        cache.append_keys(K)
+        # the fp64 kernel on the same operand-rounded S, 4 units
+        Us = min(4, U)
+        ref = DeviceKeyCache.create(Us, d, w["m_in"], h=h, m_out=w["m_out"], capacity=n, seed=seed,
+                                    key_dtype=torch.bfloat16, with_values=False, sketch_dtype=torch.float64,
+                                    channels=cache.channels[:Us, :h].cpu().numpy())
+        ref.S_in_host, ref.S_out_host = cache.S_in_host, cache.S_out_host
+        ref.set_sketches(ref.S_in_host, ref.S_out_host)
         ref.append_keys(K[:Us].contiguous())
-    finally:
-        del os.environ["QJL_FORCE_SIMT"]
-    torch.cuda.synchronize()
-    flips = int((cache.bits_in[:Us, :n] ^ ref.bits_in[:, :n]).view(torch.uint8).to(torch.int32)
-                .bitwise_count().sum()) if hasattr(torch.Tensor, "bitwise_count") else None
-    if flips is None:
+        torch.cuda.synchronize()
         x = (cache.bits_in[:Us, :n] ^ ref.bits_in[:, :n]).cpu().numpy()
         y = (cache.bits_out[:Us, :n] ^ ref.bits_out[:, :n]).cpu().numpy()
         flips = int(np.unpackbits(x).sum() + np.unpackbits(y).sum())
-    else:
-        flips += int((cache.bits_out[:Us, :n] ^ ref.bits_out[:, :n]).to(torch.int32).bitwise_count().sum())
-    norm_diff = int((cache.norm_in[:Us, :n].view(torch.int16) != ref.norm_in[:, :n].view(torch.int16)).sum()
-                    + (cache.norm_out[:Us, :n].view(torch.int16) != ref.norm_out[:, :n].view(torch.int16)).sum())
-    parity = {"units_checked": Us, "sign_bits_checked": Us * n * (w["m_in"] + w["m_out"]),
-              "bit_flips_vs_fp64_path": flips, "fp16_norm_mismatches": norm_diff,
-              "note": "tcgen05 K1 vs the fp64 SIMT quantizer on the same keys and rounded S",
-              "vs_oracle": prefill_oracle_check(cache, K, w)}
-    del K, ref
-    return {"workload": w["workload"], "keys_per_s": U * n / (step_ms * 1e-3),
-            "ms_per_step": step_ms, "kernel_ms": kern_ms,
-            "tflops": flops / (kern_ms * 1e-3) / 1e12,
-            "tensor_frac": flops / (kern_ms * 1e-3) / 1e12 / tf_peak,
-            "parity": parity,
-            "with_profile": {"fused_ms": fused_ms, "keys_per_s": U * n / (fused_ms * 1e-3),
-                             "separate_ms": sep_ms,
-                             "note": "prefill(): qjl_prefill_profile (detect + S_full) + K1; "
-                                     "separate = detect_outliers + build_sketch + K1 launches"},
-            "note": "K.S^T over zero-padded K=128 (m_in+m_out=576 rows) + sign pack + fp16 norms"}
-
-
-def measure_qjlc(device, seed, steps=10, warmup=3):
-    """Row F3: QJLC record export / import (kvcache.py:389-520) of a C3-shaped cache
-    (64 units x 32768 tokens, m_in 256, m_out 64) holding reference-format values
-    (u8 codes, one f32 zero/scale per token).  Algorithmic bytes per token-head:
-    read 176 (40 sign + 4 norm + 128 code + 8 const) + write 180 (record) = 356."""
-    import torch
-
-    from paper_2406_03482_b200 import qjlc as Q
-    from paper_2406_03482_b200.device import DeviceKeyCache
-
-    w = WORKLOADS["c3"]
-    U, n, d = w["batch"] * w["kv_heads"], w["n"], w["d"]
-    g = torch.Generator(device=device)
-    g.manual_seed(seed + 5)
-    cache = DeviceKeyCache.create(U, d, w["m_in"], h=w["h"], m_out=w["m_out"], capacity=n, seed=seed,
-                                  key_dtype=torch.bfloat16, value_layout="u8", value_bits=2,
-                                  value_group=d, channels=np.tile(np.arange(w["h"]) * 16, (U, 1)))
-    for c0 in range(0, n, 8192):                      # chunked to bound the bf16 staging
-        K = torch.randn(U, 8192, d, generator=g, device=device).to(torch.bfloat16)
-        V = torch.randn(U, 8192, d, generator=g, device=device).to(torch.bfloat16)
-        cache.append(K, V)
-    del K, V
-    kd, vd = cache.key_desc(), cache.value_desc()
-    recs, R = Q.export_records(kd, vd, w["m_in"], w["m_out"], n)
-    dst = DeviceKeyCache(U, d, w["m_in"], w["m_out"], w["h"], n, value_layout="u8", value_bits=2,
-                         value_group=d)
-    kd2, vd2 = dst.key_desc(), dst.value_desc()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    for _ in range(warmup):
-        Q.export_records(kd, vd, w["m_in"], w["m_out"], n, out=recs)
-        Q.import_records(recs, n, w["m_in"], w["m_out"], kd2, vd2)
-    torch.cuda.synchronize()
-    ev[0].record()
-    for _ in range(steps):
-        Q.export_records(kd, vd, w["m_in"], w["m_out"], n, out=recs)
-    ev[1].record()
-    for _ in range(steps):
-        Q.import_records(recs, n, w["m_in"], w["m_out"], kd2, vd2)
-    ev[2].record()
-    torch.cuda.synchronize()
-    ok = all(torch.equal(a[:, :n], b[:, :n]) for a, b in
-             ((cache.bits_in, dst.bits_in), (cache.bits_out, dst.bits_out), (cache.norm_in, dst.norm_in),
-              (cache.v_codes, dst.v_codes), (cache.v_scale, dst.v_scale)))
-    host = torch.empty(recs.shape, dtype=torch.uint8, pin_memory=True)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(3):
-        Q.export_records(kd, vd, w["m_in"], w["m_out"], n, out=recs)
-        host.copy_(recs)
-    torch.cuda.synchronize()
-    e2e_s = (time.perf_counter() - t0) / 3
-    exp_ms = ev[0].elapsed_time(ev[1]) / steps
-    imp_ms = ev[1].elapsed_time(ev[2]) / steps
-    byts = U * n * (176 + R)
-    del cache, dst, recs, host
+        norm_diff = int((cache.norm_in[:Us, :n].view(torch.int16) != ref.norm_in[:, :n].view(torch.int16)).sum()
+                        + (cache.norm_out[:Us, :n].view(torch.int16) != ref.norm_out[:, :n].view(torch.int16)).sum())
+        res["parity"] = {"units_checked": Us, "sign_bits_checked": Us * n * (w["m_in"] + w["m_out"]),
+                         "bit_flips_vs_fp64_kernel": flips, "fp16_norm_mismatches": norm_diff,
+                         "note": "tcgen05 K1 vs the fp64 quantizer kernel on the same keys and rounded S",
+                         "vs_oracle": prefill_oracle_check(cache, K, w)}
+        del ref
+    del K, cache
     torch.cuda.empty_cache()
-    return {"workload": "c3_qjlc_export_import", "record_bytes": R, "tokens": U * n,
-            "export_ms": exp_ms, "export_gbs": byts / (exp_ms * 1e-3) / 1e9,
-            "import_ms": imp_ms, "import_gbs": byts / (imp_ms * 1e-3) / 1e9,
-            "export_to_host_gbs": U * n * R / e2e_s / 1e9, "round_trip_identical": bool(ok),
-            "note": "algorithmic bytes = 176 read + 180 written per token-head; export_to_host adds "
-                    "the D2H of the records into pinned memory (PCIe bound)"}
+    return res
 
 
 def measure_generation_step(cache, q, steps=50):
-    """Row F1: one generation step at C3 = append every unit's new token (key + value)
-    and decode over the grown cache.  `decode_step` fuses the append into the step's
-    query-sketch kernel; `separate` is K1 + value quantizer launches, then the decode.
-    Each step re-appends the last row (the bench cache is full), so the decode covers the
-    same n = 32768 tokens as the headline measurement."""
+    """Row F1: one generation step = append every unit's new token (key + value) and decode
+    over the grown cache.  `decode_step` fuses the append into the step's query-sketch kernel;
+    `separate` is K1 + value quantizer launches, then the decode.  Each step re-appends the
+    last row (the bench cache is full), so the decode covers the same n as the headline."""
     import torch
 
     U, G, d = q.shape
-    n0 = cache.n                                          # the step appends row n0 - 1 again
+    n0 = cache.n
     g = torch.Generator(device=q.device).manual_seed(7)
     kn = torch.randn(U, d, generator=g, device=q.device).to(q.dtype)
     vn = torch.randn(U, d, generator=g, device=q.device).to(q.dtype)
@@ -528,7 +452,7 @@ def measure_generation_step(cache, q, steps=50):
             for i in range(steps):
                 cache.n = cache.n_values = n0 - 1
                 if mode == "decode_step":
-                    cache.decode_step(q, kn, vn, out=out)
+                    cache.decode_step(q, kn, vn, out=out, chained=i > 0)
                 else:
                     cache.append(kn[:, None, :], vn[:, None, :])
                     cache.decode(q, out=out)
@@ -537,33 +461,8 @@ def measure_generation_step(cache, q, steps=50):
             res[mode] = e0.elapsed_time(e1) / steps * 1e3
     cache.n = cache.n_values = n0
     return {"decode_step_us": res["decode_step"], "separate_us": res["separate"],
-            "note": "append one token per unit (64 units) + decode over n = 32768 tokens; "
-                    "decode_step fuses K1 + value quantizer into the query-sketch kernel"}
-
-
-def measure_harness():
-    """Row F4: the statistical suites (harness.py:183-329) as batched device runs, wall
-    time end to end (host sketch draws + device orthogonalize / K1 / K2 + host stats)."""
-    import torch
-
-    from paper_2406_03482_b200 import harness as H
-
-    out = {}
-    for name, fn, kw in (("unbiasedness", H.run_unbiasedness_trial, {}),
-                         ("distortion", H.run_distortion_trial, dict(m=142)),
-                         ("orthogonal", H.run_orthogonal_comparison, {}),
-                         ("scores", H.run_score_trial, dict(m=64, trials=1000))):
-        fn(H.TrialConfig(**dict(kw, trials=100)))        # warm-up (library load, first launches)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        r = fn(H.TrialConfig(**kw))
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        out[name] = {"config": dict(H.TrialConfig(**kw).__dict__), "seconds": dt,
-                     "trials_per_s": r.trials / dt, "passed": bool(r.passed)}
-    out["note"] = ("wall clock per suite, host draws included; the reference's pure-Python loop "
-                   "measures 5.9k / 1.1k / 5.2k / 149 trials/s on these configs (DESIGN.md 5)")
-    return out
+            "note": f"append one token per unit ({U} units) + decode over n = {n0} tokens; decode_step "
+                    "fuses K1 + value quantizer into the query-sketch kernel (chained steps)"}
 
 
 # --------------------------------------------------------------- GPU arm
@@ -571,27 +470,38 @@ def run_gpu(args):
     import torch
     import torch.distributed as dist
 
+    from paper_2406_03482_b200.distributed import gather_units, shard_units
+
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() < (local + 1):
+        raise SystemExit(f"rank {rank}: local rank {local} but only {torch.cuda.device_count()} GPU(s) visible")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
     from paper_2406_03482_b200 import _lib
 
-    lib = _lib.load()
+    _lib.load()
     w = dict(WORKLOADS[args.workload])
-    U = w["batch"] * w["kv_heads"]
-    cache = build_cache(w, rank, args.seed, device, args.layout)
-    tdt = {"bf16": torch.bfloat16, "f16": torch.float16}[w["dtype"]]
-    g = torch.Generator(device=device)
-    g.manual_seed(args.seed + 17 * rank + 3)
-    q = torch.randn(U, w["G"], w["d"], generator=g, device=device).to(tdt)
+    for k in ("batch", "n", "m_in"):
+        if getattr(args, k) is not None:
+            w[k] = getattr(args, k)
+    if args.n is not None or args.batch is not None or args.m_in is not None:
+        w["workload"] = f"{w['workload']}_b{w['batch']}_n{w['n']}_m{w['m_in']}"
+    U_all = w["batch"] * w["kv_heads"]
+    shard = shard_units(U_all, world, rank)
+    U = shard.count
+    cache = build_cache(w, shard, args.seed, device)
+    q = make_queries(w, shard, args.seed, device)
     out = torch.empty(U, w["G"], w["d"], dtype=torch.float32, device=device)
     torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        cache.decode(q, out=out)
+    # ---- value: back-to-back decode steps, device-resident inputs (chained launches)
+    for i in range(args.warmup):
+        cache.decode(q, out=out, chained=i > 0)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -599,64 +509,30 @@ def run_gpu(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record()
-        for _ in range(args.steps):
-            cache.decode(q, out=out)
+        for i in range(args.steps):
+            cache.decode(q, out=out, chained=True)
         e1.record()
         torch.cuda.synchronize()
     t_ms = e0.elapsed_time(e1)
     if world > 1:
         dist.barrier()
 
-    # roofline leg: the same K steps again with the library's per-kernel event hook
-    # on (events bracket the dominant decode kernel on its own launch stream; the hook
-    # turns programmatic dependent launch off, so it is kept out of the value loop)
-    torch.cuda.synchronize()
-    lib.qjl_timing_read(None, None, 1)
-    lib.qjl_timing_enable(1)
-    for _ in range(args.steps):
-        cache.decode(q, out=out)
-    torch.cuda.synchronize()
-    lib.qjl_timing_enable(0)
-    import ctypes
-    kms, kcnt = ctypes.c_double(), ctypes.c_int()
-    lib.qjl_timing_read(ctypes.byref(kms), ctypes.byref(kcnt), 1)
+    # ---- roofline: the decode kernel alone, in a chain of back-to-back decodes
+    kern_ms = cache.bench_decode_kernel(q, reps=max(args.steps, 20))
 
-    # end-to-end through the public API with host buffers: every step copies its query
-    # (pinned host -> device) and reads its output back (device -> pinned host).  The
-    # copies run on a side stream, double-buffered, so step i+1's upload and step i's
-    # read-back overlap the decode kernels (each decode waits for its own upload; each
-    # read-back waits for its own decode).
-    qh = [q.cpu().pin_memory() for _ in range(2)]
-    oh = [torch.empty(out.shape, dtype=out.dtype).pin_memory() for _ in range(2)]
-    qd = [torch.empty_like(q) for _ in range(2)]
-    od = [torch.empty_like(out) for _ in range(2)]
-    comp = torch.cuda.current_stream()
-    copy = torch.cuda.Stream()
-    up_done = [torch.cuda.Event() for _ in range(2)]
-    dec_done = [torch.cuda.Event() for _ in range(2)]
-    d2h_done = [torch.cuda.Event() for _ in range(2)]
+    # ---- e2e through the public API with host buffers: H2D of the step's query from pinned
+    # memory, decode, NCCL all-gather of the outputs (N > 1), D2H of the gathered output
+    qh = q.cpu().pin_memory()
+    qd = torch.empty_like(q)
+    full_shape = (U_all,) + tuple(out.shape[1:])
+    oh = torch.empty(full_shape, dtype=out.dtype).pin_memory()
 
     def e2e_steps(k):
-        with torch.cuda.stream(copy):
-            qd[0].copy_(qh[0], non_blocking=True)
-            up_done[0].record(copy)
-        for i in range(k):
-            b = i & 1
-            if i + 1 < k:                               # upload the next step's query
-                with torch.cuda.stream(copy):
-                    copy.wait_event(dec_done[1 - b]) if i >= 1 else None   # buffer reuse
-                    qd[1 - b].copy_(qh[1 - b], non_blocking=True)
-                    up_done[1 - b].record(copy)
-            comp.wait_event(up_done[b])
-            if i >= 2:
-                comp.wait_event(d2h_done[b])            # od[b] was read back two steps ago
-            cache.decode(qd[b], out=od[b])
-            dec_done[b].record(comp)
-            with torch.cuda.stream(copy):               # read this step's output back
-                copy.wait_event(dec_done[b])
-                oh[b].copy_(od[b], non_blocking=True)
-                d2h_done[b].record(copy)
-        comp.wait_stream(copy)
+        for _ in range(k):
+            qd.copy_(qh, non_blocking=True)
+            cache.decode(qd, out=out)
+            full = gather_units(out, shard) if world > 1 else out
+            oh.copy_(full, non_blocking=True)
 
     e2e_steps(args.warmup)
     torch.cuda.synchronize()
@@ -668,115 +544,102 @@ def run_gpu(args):
     e3.record()
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3)
-    qd, out = qd[0], od[(args.steps - 1) & 1]
+    e2e_ok = bool(torch.equal(oh[shard.start:shard.stop], cache.decode(q).cpu()))
 
-    # zero-copy variant of the same end-to-end step: the decode is called directly on the
-    # pinned host buffers (UVA pointers), so its query-sketch kernel reads the query over
-    # PCIe and the merging CTAs write the outputs over PCIe, inside the timed kernels, and
-    # no copy op breaks the PDL chain between consecutive steps
-    def zc_steps(k):
-        for i in range(k):
-            cache.decode(qh[i & 1], out=oh[i & 1])
-
-    zc_steps(args.warmup)
-    torch.cuda.synchronize()
-    ref_out = cache.decode(q).cpu()
-    zc_ok = bool(torch.equal(oh[(args.warmup - 1) & 1], ref_out))
-    if world > 1:
-        dist.barrier()
-    e2.record()
-    zc_steps(args.steps)
-    e3.record()
-    torch.cuda.synchronize()
-    zc_ms = e2.elapsed_time(e3)
-
-    # output gather over NCCL (the path's only exchange), timed on its own
-    gather_ms = 0.0
-    if world > 1:
-        from paper_2406_03482_b200.distributed import gather_units, shard_units
-
-        shard = shard_units(U * world, world, rank)
-        for _ in range(3):
-            gather_units(out, shard)
+    # zero-copy variant (N = 1): the decode reads q / writes out through pinned host pointers
+    zc_ms = None
+    if world == 1:
+        ohz = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        for i in range(args.warmup):
+            cache.decode(qh, out=ohz, chained=i > 0)
         torch.cuda.synchronize()
-        dist.barrier()
-        e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e4.record()
-        for _ in range(20):
-            full = gather_units(out, shard)
-        e5.record()
+        e2.record()
+        for _ in range(args.steps):
+            cache.decode(qh, out=ohz, chained=True)
+        e3.record()
         torch.cuda.synchronize()
-        gather_ms = e4.elapsed_time(e5) / 20
-        assert full.shape[0] == U * world
+        zc_ms = e2.elapsed_time(e3)
 
-    t = torch.tensor([t_ms, e2e_ms, gather_ms, zc_ms], device=device, dtype=torch.float64)
+    # ---- K2 scores-only and K1 prefill (sharded like the decode)
+    scores = measure_scores(cache, q, w, max(20, args.steps // 4)) if not args.no_extras else None
+    prefill = None
+    if not args.no_prefill:
+        prefill = measure_prefill(device, args.seed, lambda total: shard_units(total, world, rank),
+                                  parity=(rank == 0 and world == 1))
+
+    t = torch.tensor([t_ms, e2e_ms, kern_ms, prefill["kernel_ms"] if prefill else 0.0,
+                      prefill["with_profile"]["ms"] if prefill else 0.0,
+                      scores["ms_per_step"] if scores else 0.0], device=device, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_ms, e2e_ms, gather_ms, zc_ms = float(t[0]), float(t[1]), float(t[2]), float(t[3])
+    t_ms, e2e_ms, kern_ms, k1_ms, pf_ms, sc_ms = (float(x) for x in t)
 
     bpt = bytes_per_token_head(w)
+    alg_bytes = U_all * w["n"] * bpt
     alg_bytes_rank = U * w["n"] * bpt
-    alg_bytes = alg_bytes_rank * world
     value = alg_bytes * args.steps / (t_ms * 1e-3) / 1e9
-    e2e_copy_val = alg_bytes * args.steps / (e2e_ms * 1e-3) / 1e9
-    zc_val = alg_bytes * args.steps / (zc_ms * 1e-3) / 1e9
-    e2e_val = max(e2e_copy_val, zc_val) if zc_ok else e2e_copy_val
+    e2e_val = alg_bytes * args.steps / (e2e_ms * 1e-3) / 1e9
     peak, tf_peak, peak_src = load_peaks()
-    kern_avg_ms = kms.value / max(kcnt.value, 1)
-    achieved = alg_bytes_rank / (kern_avg_ms * 1e-3) / 1e9
-    launches_per_step = 2      # k_prep (query sketch digits) + fused decode with in-kernel merge (PDL-chained)
+    achieved = alg_bytes_rank / (kern_ms * 1e-3) / 1e9
     res = {
         "metric": "QJL decode score+aggregate kernel HBM GB/s (algorithmic bytes of the packed cache)",
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "i8 (tcgen05 kind::i8 scores and P.V, s32 accumulators) + f32 (softmax, output); inputs bf16, u1 signs, u2 values",
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "i8 (tcgen05 kind::i8 scores and P.V, s32 accumulators) + f32 (softmax, output); "
+                 "inputs bf16, u1 signs, u2 values",
         "data": "synthetic (seeded N(0,1), outlier channels planted; random-init, no dataset)",
-        "config": {"workload": w["workload"], "units_per_gpu": U, "global_batch": w["batch"] * world,
-                   "kv_heads": w["kv_heads"], "q_heads": w["kv_heads"] * w["G"], "seq_len": w["n"],
-                   "head_dim": w["d"], "m_in": w["m_in"], "m_out": w["m_out"], "outliers": w["h"],
-                   "value_bits": 2, "value_group": 32, "bytes_per_token_head": bpt,
-                   "parallelism": f"units sharded, {world} rank(s), no data-path collective",
-                   "l2": f"inputs larger than L2 ({alg_bytes_rank / 1e6:.0f} MB/step/rank > 126 MB)"},
+        "config": {"workload": w["workload"], "units_total": U_all, "units_per_gpu": U,
+                   "global_batch": w["batch"], "kv_heads": w["kv_heads"], "q_heads": w["kv_heads"] * w["G"],
+                   "seq_len": w["n"], "head_dim": w["d"], "m_in": w["m_in"], "m_out": w["m_out"],
+                   "outliers": w["h"], "value_bits": 2, "value_group": 32, "bytes_per_token_head": bpt,
+                   "cache_layout": f"tile-major records, {cache.record_bytes} B per (unit, 128-token tile)",
+                   "parallelism": f"KV heads sharded over {world} rank(s) ({U} units each), no data-path "
+                                  f"collective",
+                   "l2": f"inputs larger than L2 ({alg_bytes_rank / 1e6:.0f} MB/step/rank vs 126 MB)"
+                         if alg_bytes_rank > 126e6 else
+                         f"{alg_bytes_rank / 1e6:.0f} MB/step/rank fits the 126 MB L2 (strong-scaled "
+                         f"shard; not flushed)"},
         "e2e": {"value": e2e_val, "unit": "GB/s",
                 "h2d_bytes_per_step": int(q.numel() * q.element_size()),
-                "d2h_bytes_per_step": int(out.numel() * out.element_size()),
-                "mode": "zero-copy" if e2e_val == zc_val else "copy-stream",
-                "copy_stream_gbs": e2e_copy_val, "zero_copy_gbs": zc_val, "zero_copy_output_ok": zc_ok,
-                "note": "decode(q, out) on pinned host buffers every step: copy-stream = explicit H2D / D2H "
-                        "copies on a side stream; zero-copy = the kernels read q / write out over PCIe"},
+                "d2h_bytes_per_step": int(oh.numel() * oh.element_size()),
+                "output_ok": e2e_ok,
+                "note": "per step: query H2D from pinned host, decode, NCCL all_gather of the outputs "
+                        "(N > 1), D2H of the gathered [units, G, d] output -- one stream, in the timed "
+                        "region"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_src,
                      "frac_of_8tbs": achieved / 8000.0,
-                     "kernel": "fused decode (scores + online softmax + PV)",
-                     "kernel_ms": kern_avg_ms,
+                     "kernel": "k_udecode (fused scores + online softmax + PV)",
+                     "kernel_ms": kern_ms,
+                     "timing": "mean of back-to-back decode kernels chained with PDL "
+                               "(qjl_bench_decode_kernel), CUDA events on the launch stream",
                      "traffic": load_traffic(w["workload"])},
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": 2 * args.steps,
         "clocks": clk.summary(),
     }
-    if world > 1:
-        res["output_gather"] = {"collective": "all_gather_into_tensor (NCCL)", "ms": gather_ms,
-                                "bytes": int(out.numel() * out.element_size() * world),
-                                "note": "outside the timed decode region; units are independent"}
-    if world == 1 and rank == 0 and not args.no_prefill and args.layout == "p2t":
+    if zc_ms is not None:
+        res["e2e"]["zero_copy_gbs"] = alg_bytes * args.steps / (zc_ms * 1e-3) / 1e9
+    if scores:
+        scores["ms_per_step"] = sc_ms
+        kb = U_all * w["n"] * bytes_per_token_head(w, values=False)
+        scores["gbs_key_bytes"] = kb / (sc_ms * 1e-3) / 1e9
+        scores["frac_key_bytes"] = scores["gbs_key_bytes"] / peak
+        scores["kernel"] = "k_uscores (tcgen05 score stage writing fp32 logits) after the query-sketch kernel"
+        res["scores_only"] = scores
+    if prefill:
+        keys_all = PREFILL["batch"] * PREFILL["kv_heads"] * PREFILL["n"]
+        res["keys_quantized_per_s"] = keys_all / (k1_ms * 1e-3)
+        res["k1_tensor_frac"] = prefill["tensor_frac_padded"] if world == 1 else None
+        res["k1_tensor_frac_useful"] = prefill["tensor_frac_useful"] if world == 1 else None
+        prefill["keys_per_s_all_ranks"] = res["keys_quantized_per_s"]
+        prefill["with_profile_keys_per_s_all_ranks"] = keys_all / (pf_ms * 1e-3)
+        res["prefill"] = prefill
+    if world == 1 and rank == 0 and not args.no_extras:
         try:
             res["generation_step"] = measure_generation_step(cache, q)
         except Exception as e:                       # pragma: no cover
             res["generation_step"] = {"error": repr(e)[:200]}
-    if world == 1 and rank == 0 and not args.no_prefill:
-        try:
-            res["prefill"] = measure_prefill(device, args.seed)
-        except Exception as e:                       # pragma: no cover
-            res["prefill"] = {"error": repr(e)[:200]}
-    if world == 1 and rank == 0 and not args.no_prefill:
-        try:
-            res["qjlc"] = measure_qjlc(device, args.seed)
-        except Exception as e:                       # pragma: no cover
-            res["qjlc"] = {"error": repr(e)[:200]}
-    if world == 1 and rank == 0 and not args.no_prefill:
-        try:
-            res["harness"] = measure_harness()
-        except Exception as e:                       # pragma: no cover
-            res["harness"] = {"error": repr(e)[:200]}
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         res["cpu_baseline"], res["parity"] = cpu_baseline_leg(cache, q, w)
     if rank == 0:
@@ -788,8 +651,6 @@ def run_gpu(args):
 # --------------------------------------------------------- reference arm
 def _ref_worker(args_tuple):
     """Build one unit on the host with the oracle and time decodes of a token slice."""
-    import torch  # noqa: F401  (sketch rounding uses torch on the host)
-
     from threadpoolctl import threadpool_limits
 
     from oracle import qjl_oracle as O
@@ -805,15 +666,13 @@ def _ref_worker(args_tuple):
         K[:, ch] *= w["factor"]
         V = rng.standard_normal((n, d))
         Q = rng.standard_normal((w["G"], d))
-        cast = np.float16 if w["dtype"] == "f16" else None
         import torch as _t
-        tdt = _t.float16 if cast else _t.bfloat16
+        tdt = _t.float16 if w["dtype"] == "f16" else _t.bfloat16
         K = _t.from_numpy(K).to(tdt).double().numpy()
         V = _t.from_numpy(V).to(tdt).double().numpy()
         Q = _t.from_numpy(Q).to(tdt).double().numpy()
         chans = O.detect_outliers(K, h)[0]
-        S_in, S_out = DeviceKeyCache.make_sketches(d, h, w["m_in"], w["m_out"], seed, True,
-                                                   w["dtype"])
+        S_in, S_out = DeviceKeyCache.make_sketches(d, h, w["m_in"], w["m_out"], seed, True, w["dtype"])
         r = O.append_keys(S_in, S_out, chans, K)
         codes, zero, scale = O.quantize_values(V, 2, 32)
         hu = dict(bits_in=r["bits_in"], norm_in=O.fp16_round(r["norm_in"]),
@@ -854,7 +713,7 @@ def run_reference(args):
     out = {"metric": "QJL decode score+aggregate kernel HBM GB/s (algorithmic bytes of the packed cache)",
            "value": value, "unit": "GB/s", "n_gpus": int(os.environ.get("WORLD_SIZE", 1)),
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(step_t.mean() * 1e3),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
            "dtype": "f64 (reference numpy arithmetic)", "data": "synthetic (seeded N(0,1))",
            "config": {"workload": w["workload"], "seq_len_sample": L, "units_sample": workers},
            "impl": "reference",
@@ -864,21 +723,43 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def relaunch(args):
+    """`--gpus N` without torchrun: re-run this script under torch.distributed.run, one
+    process per GPU, rendezvous on 127.0.0.1 (NCCL_DEBUG=INFO unless set)."""
+    import socket
+
+    import torch
+
+    if args.impl != "reference" and torch.cuda.device_count() < args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but {torch.cuda.device_count()} GPU(s) visible")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd, env=env))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=None, help="override the workload's batch (C5 sweep)")
+    ap.add_argument("--n", type=int, default=None, help="override the workload's sequence length")
+    ap.add_argument("--m-in", dest="m_in", type=int, default=None, help="override m_in (256 or 512)")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--layout", default="p2t", choices=["p2t", "p2"],
-                    help="value-code layout: p2t = tcgen05 decode, p2 = mma.sync decode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the scores-only and generation-step legs")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

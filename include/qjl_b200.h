@@ -31,21 +31,27 @@
  *   qjl_qjlc_export      <- write_cache record loop    pkg/src/qjl/kvcache.py:389-437
  *   qjl_qjlc_import      <- read_cache record loop     pkg/src/qjl/kvcache.py:440-520
  *
- * Data layout in HBM (unit = one (batch, kv-head) pair; all arrays unit-major):
- *   key cache   bits_in  u8  [units][capacity][m_in/8]   LSB-first sign bits; byte-
- *                                                         identical to the reference's
- *                                                         LE u64 words when m % 64 == 0
- *               bits_out u8  [units][capacity][m_out/8]
- *               norm_in  f16 [units][capacity]           ||k_inlier||_2
- *               norm_out f16 [units][capacity]           ||k_outlier||_2
- *   value cache layout P2 (fast path): 2-bit codes, group 32, fp16 zero/scale
- *               codes u8  [units][capacity][d/4]  in MMA fragment order
- *               zero  f16 [units][capacity][d/32], scale f16 [units][capacity][d/32]
- *   value cache layout P2T (tcgen05 path): 2-bit codes, group 32, fp16 zero/scale; inside each
- *               128-token tile byte (d/4)*128 + (t%128)/4*4 + t%4 holds dims 4(d/4)..+3 of
- *               token t at bits 2(d%4)..+1 -- one u32 = 4 tokens x 4 dims
- *   value cache layout U8 (reference-format path): 1 byte per code, any bits 1..8,
- *               any group dividing d, fp32 zero/scale per (token, group).
+ * Data layout in HBM (unit = one (batch, kv-head) pair; rows padded to 128-token tiles):
+ *   key cache   bits_in  u8  [row][m_in/8]    LSB-first sign bits; byte-identical to the
+ *                                            reference's LE u64 words when m % 64 == 0
+ *               bits_out u8  [row][m_out/8]
+ *               norm_in  f16 [row]            ||k_inlier||_2
+ *               norm_out f16 [row]            ||k_outlier||_2
+ *   value cache P2T (tensor-core path): 2-bit codes, group 32, d = 128, fp16 zero/scale
+ *               codes u8 [tile][4096]: byte (d/4)*128 + (t%128)/4*4 + t%4 holds dims
+ *               4(d/4)..+3 of token t at bits 2(d%4)..+1 (one u32 = 4 tokens x 4 dims)
+ *               zero f16 [row][d/32], scale f16 [row][d/32]
+ *   value cache U8 (reference format): 1 byte per code, any bits 1..8, any group dividing
+ *               d, fp32 zero/scale per (token, group) -- rows layout only.
+ *   Row addressing (tile_stride, both cache structs):
+ *     tile_stride == 0  rows layout: every array is [units][capacity][row bytes];
+ *     tile_stride  > 0  tile-major records: row r of unit u of every array lives at
+ *                       array + (u * capacity/128 + r/128) * tile_stride + (r%128) * row bytes
+ *                       (P2T codes: + the in-tile offset above).  capacity % 128 == 0.
+ *   The tensor-core decode streams one contiguous record per (unit, 128-token tile):
+ *     [bits_in 128*m_in/8][bits_out 128*m_out/8][norm_in 256][norm_out 256 if m_out]
+ *     [codes 4096][zero 1024][scale 1024]            (qjl_tile_record, QJL_REC_*)
+ *   so a P2T value cache must be the tail of the same records as its key cache.
  *   sketch      s_full [units or 1][m_in+m_out][d]: rows 0..m_in-1 hold S_in at the
  *               inlier columns (zeros at outlier columns), rows m_in.. hold S_out at
  *               the outlier columns -- one zero-padded K=d GEMM per unit.
@@ -60,7 +66,7 @@
 extern "C" {
 #endif
 
-#define QJL_ABI_VERSION 1
+#define QJL_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define QJL_API __attribute__((visibility("default")))
@@ -78,7 +84,18 @@ enum {
 };
 
 enum { QJL_F32 = 0, QJL_F16 = 1, QJL_BF16 = 2, QJL_F64 = 3 };
-enum { QJL_VLAYOUT_U8 = 0, QJL_VLAYOUT_P2 = 1, QJL_VLAYOUT_P2T = 2 };
+enum { QJL_VLAYOUT_U8 = 0, QJL_VLAYOUT_P2T = 2 };
+/* qjl_tile_record field indices */
+enum { QJL_REC_BITS_IN = 0, QJL_REC_BITS_OUT, QJL_REC_NORM_IN, QJL_REC_NORM_OUT, QJL_REC_CODES,
+       QJL_REC_ZERO, QJL_REC_SCALE, QJL_REC_FIELDS };
+/* qjl_decode / qjl_decode_step flags */
+enum {
+  /* The previous kernel on `stream` is a qjl_decode / qjl_decode_step of this library and
+   * every input of this call (cache rows, q, k_new, v_new, sketch) was written before that
+   * launch: the query-sketch kernel may then read its inputs while the previous decode
+   * drains (programmatic dependent launch).  Without it every read waits for the stream. */
+  QJL_DECODE_CHAINED = 1
+};
 
 typedef struct qjl_key_cache {
   uint8_t* bits_in;
@@ -87,6 +104,7 @@ typedef struct qjl_key_cache {
   uint16_t* norm_out;  /* NULL when m_out == 0 */
   int64_t capacity;
   int32_t units, d, m_in, m_out;
+  int64_t tile_stride;   /* 0: rows layout; > 0: tile-major records of this many bytes */
 } qjl_key_cache_t;
 
 typedef struct qjl_value_cache {
@@ -95,6 +113,8 @@ typedef struct qjl_value_cache {
   void* scale;
   int64_t capacity;
   int32_t units, d, bits, group, layout;
+  int32_t pad_;
+  int64_t tile_stride;   /* P2T: the key cache's record bytes; U8: 0 */
 } qjl_value_cache_t;
 
 typedef struct qjl_sketch {
@@ -146,11 +166,20 @@ QJL_API int qjl_quantize_keys(const void* keys, int dtype, int64_t n, int64_t ke
                       const qjl_sketch_t* sketch, const int32_t* channels, int h,
                       const qjl_key_cache_t* cache, int64_t row_offset, void* stream);
 
-/* S_full @ q per unit and query head: q [units][G][d] -> sq f32 [units][G][m_in+m_out]. */
+/* S_full @ q per unit and query head (fp64 accumulation): q [units][G][d] ->
+ * sq [units][G][m_in+m_out] in sq_dtype (QJL_F32 or QJL_F64). */
 QJL_API int qjl_sketch_query(const void* q, int q_dtype, int units, int G, int d,
-                     const qjl_sketch_t* sketch, int m_total, float* sq, void* stream);
+                     const qjl_sketch_t* sketch, int m_total, int sq_dtype, void* sq, void* stream);
 
-/* K2: logits [units][G][n] (f32) of G query heads per unit over the first n keys. */
+/* Canonical tile record (see the layout above): byte offsets of the QJL_REC_* fields
+ * within one 128-token record (-1 for absent fields: no outlier side, or no values when
+ * values == 0) and the record size in bytes, or -1 for an unsupported shape.
+ * values != 0 appends the P2T value fields (d == 128). */
+QJL_API int64_t qjl_tile_record(int d, int m_in, int m_out, int values, int64_t* offsets);
+
+/* K2: logits [units][G][n] (f32) of G query heads per unit over the first n keys.
+ * Tile-major caches with m_in/32 in {8, 16}, m_out/32 in {0, 2, 4}, d == 128 and G <= 4
+ * run the tensor-core score kernel; every other shape runs the generic kernel. */
 QJL_API size_t qjl_scores_workspace(int units, int G, int m_total);
 QJL_API int qjl_scores(const qjl_key_cache_t* cache, int64_t n, const void* q, int q_dtype, int G,
                const qjl_sketch_t* sketch, float* logits, void* workspace,
@@ -166,30 +195,44 @@ QJL_API int qjl_softmax_f64(const float* logits, int64_t rows, int64_t n, double
                     double* weights, void* stream);
 
 /* K2+K3 fused decode: out [units][G][d] f32 = softmax(logits * inv_temperature) @ V.
- * lse (optional, may be NULL): [units][G] f32 log-sum-exp of the scaled logits. */
+ * lse (optional, may be NULL): [units][G] f32 log-sum-exp of the scaled logits.
+ * logits (optional, may be NULL): [units][G][n] f32, the scaled logits the softmax consumed
+ * (what `estimate_scores` normalizes, kvcache.py:331-337).
+ * P2T caches (tile-major records) run the tensor-core decode (G <= 4); U8 caches run the
+ * generic decode.  flags: QJL_DECODE_*. */
 QJL_API size_t qjl_decode_workspace(const qjl_key_cache_t* cache, const qjl_value_cache_t* values,
                             int64_t n, int G);
 QJL_API int qjl_decode(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int64_t n,
                const void* q, int q_dtype, int G, const qjl_sketch_t* sketch,
-               float inv_temperature, float* out, float* lse, void* workspace,
-               size_t workspace_bytes, void* stream);
+               float inv_temperature, float* out, float* lse, float* logits, void* workspace,
+               size_t workspace_bytes, unsigned flags, void* stream);
 
 /* One generation step (Algorithm 1 of the paper): append the new token of
  * every unit -- k_new / v_new [units][d] in q_dtype -- at row n (K1 + value quantizer
  * arithmetic, fused into the query-sketch kernel), then decode over rows [0, n + 1).
- * channels [units][h] is the outlier profile.  Tensor-core path only (P2T values);
- * QJL_ERR_UNSUPPORTED otherwise (callers then append and decode separately).  Workspace:
+ * channels [units][h] is the outlier profile.  P2T caches only (QJL_ERR_UNSUPPORTED
+ * otherwise: callers then append and decode separately).  Workspace:
  * qjl_decode_workspace(cache, values, n + 1, G). */
 QJL_API int qjl_decode_step(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int64_t n,
                             const void* q, int q_dtype, int G, const qjl_sketch_t* sketch,
                             const int32_t* channels, int h, const void* k_new, const void* v_new,
-                            float inv_temperature, float* out, float* lse, void* workspace,
-                            size_t workspace_bytes, void* stream);
+                            float inv_temperature, float* out, float* lse, float* logits, void* workspace,
+                            size_t workspace_bytes, unsigned flags, void* stream);
 
-/* Benchmark timing hook: while enabled, the dominant kernel of every qjl_decode /
- * qjl_quantize_keys call is bracketed by CUDA events recorded on its launch stream.
- * qjl_timing_read synchronizes on them and returns the summed kernel time (ms)
- * and the number of bracketed launches (reset != 0 clears the record). */
+/* Benchmark hook: time the dominant kernel of the P2T decode as it runs in a decode loop.
+ * Runs the query-sketch kernel once, then `reps` back-to-back decode kernels chained with
+ * programmatic dependent launch (each one re-reads the whole cache and rewrites out/lse),
+ * bracketed by CUDA events on `stream`; *ms = mean kernel time.  Same arguments as
+ * qjl_decode otherwise. */
+QJL_API int qjl_bench_decode_kernel(const qjl_key_cache_t* cache, const qjl_value_cache_t* values,
+                                    int64_t n, const void* q, int q_dtype, int G,
+                                    const qjl_sketch_t* sketch, float inv_temperature, float* out,
+                                    float* lse, void* workspace, size_t workspace_bytes, int reps,
+                                    float* ms, void* stream);
+
+/* Benchmark timing hook: while enabled, every qjl_quantize_keys call is bracketed by CUDA
+ * events recorded on its launch stream.  qjl_timing_read synchronizes on them and returns the
+ * summed kernel time (ms) and the number of bracketed launches (reset != 0 clears the record). */
 QJL_API int qjl_timing_enable(int on);
 QJL_API int qjl_timing_read(double* total_ms, int* launches, int reset);
 
@@ -212,7 +255,8 @@ QJL_API int qjl_orthogonalize(const double* gaussian, int batch, int m, int d, d
  * m_in_file / m_out_file are the logical widths of the file header; the key cache's
  * (32-bit padded) widths must fit inside the file's words, and bits past the logical
  * width are written / loaded as zero.  An empty side (width 0) writes a 0.0 norm
- * (EMPTY_KEY, estimator.py:95).  The value cache must use the U8 layout with group == d
+ * (EMPTY_KEY, estimator.py:95).  Rows-layout caches only (tile_stride == 0); the value cache
+ * must use the U8 layout with group == d
  * (the only value format the file holds).  records: [units][unit_stride] bytes, unit u's
  * n records at u * unit_stride.  The header, outlier channels and magnitudes of each file
  * are host data (paper_2406_03482_b200/qjlc.py). */

@@ -9,7 +9,7 @@ need the device fail loudly when the library or a CUDA device is missing.
 """
 
 from .attention import DecodeResult, quantized_decode
-from .device import DeviceKeyCache, p2_pack_codes, p2_unpack_codes
+from .device import DeviceKeyCache, pack_codes, unpack_codes
 from .distributed import UnitShard, gather_units, shard_of, shard_units
 from .estimator import (
     EMPTY_KEY,
@@ -50,8 +50,8 @@ __all__ = [
     "DecodeResult", "DeviceKeyCache", "EMPTY_KEY", "ESTIMATOR_SCALE", "KeyCacheState", "MemoryReport",
     "OutlierProfile", "QuantizedKey", "QuantizedValueToken", "ScoreVector", "SketchMatrix",
     "SketchedQuery", "UnitShard", "dequantize_value", "derive_seed", "detect_outliers",
-    "estimate_inner_product", "gather_units", "generate_gaussian", "orthogonalize", "p2_pack_codes",
-    "p2_unpack_codes", "pack_signs", "packed_sign_dot", "packed_sign_dot_batch", "quantize_key",
+    "estimate_inner_product", "gather_units", "generate_gaussian", "orthogonalize", "pack_codes",
+    "unpack_codes", "pack_signs", "packed_sign_dot", "packed_sign_dot_batch", "quantize_key",
     "quantize_value", "quantized_decode", "rng_from_seed", "shard_of", "shard_units",
     "sketch_query", "softmax", "unpack_signs",
 ]

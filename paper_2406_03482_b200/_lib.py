@@ -16,7 +16,10 @@ LIB_PATH = os.environ.get("QJL_LIB") or os.path.join(_HERE, "libqjl_b200.so")
 QJL_OK, QJL_ERR_ARG, QJL_ERR_UNSUPPORTED, QJL_ERR_CUDA, QJL_ERR_WORKSPACE, QJL_ERR_EMPTY = (
     0, -1, -2, -3, -4, -5)
 QJL_F32, QJL_F16, QJL_BF16, QJL_F64 = 0, 1, 2, 3
-QJL_VLAYOUT_U8, QJL_VLAYOUT_P2, QJL_VLAYOUT_P2T = 0, 1, 2
+QJL_VLAYOUT_U8, QJL_VLAYOUT_P2T = 0, 2
+QJL_DECODE_CHAINED = 1
+(QJL_REC_BITS_IN, QJL_REC_BITS_OUT, QJL_REC_NORM_IN, QJL_REC_NORM_OUT, QJL_REC_CODES, QJL_REC_ZERO,
+ QJL_REC_SCALE) = range(7)
 
 c_i32, c_i64, c_sz, c_vp, c_dbl, c_flt = (ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t,
                                           ctypes.c_void_p, ctypes.c_double, ctypes.c_float)
@@ -25,13 +28,13 @@ c_i32, c_i64, c_sz, c_vp, c_dbl, c_flt = (ctypes.c_int32, ctypes.c_int64, ctypes
 class KeyCacheDesc(ctypes.Structure):
     _fields_ = [("bits_in", c_vp), ("bits_out", c_vp), ("norm_in", c_vp), ("norm_out", c_vp),
                 ("capacity", c_i64), ("units", c_i32), ("d", c_i32), ("m_in", c_i32),
-                ("m_out", c_i32)]
+                ("m_out", c_i32), ("tile_stride", c_i64)]
 
 
 class ValueCacheDesc(ctypes.Structure):
     _fields_ = [("codes", c_vp), ("zero", c_vp), ("scale", c_vp), ("capacity", c_i64),
                 ("units", c_i32), ("d", c_i32), ("bits", c_i32), ("group", c_i32),
-                ("layout", c_i32)]
+                ("layout", c_i32), ("pad_", c_i32), ("tile_stride", c_i64)]
 
 
 class SketchDesc(ctypes.Structure):
@@ -51,7 +54,7 @@ SIGNATURES = {
                                     c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "qjl_quantize_keys": (c_i32, [c_vp, c_i32, c_i64, c_i64, P(SketchDesc), c_vp, c_i32,
                                   P(KeyCacheDesc), c_i64, c_vp]),
-    "qjl_sketch_query": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, P(SketchDesc), c_i32, c_vp, c_vp]),
+    "qjl_sketch_query": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, P(SketchDesc), c_i32, c_i32, c_vp, c_vp]),
     "qjl_scores_workspace": (c_sz, [c_i32, c_i32, c_i32]),
     "qjl_scores": (c_i32, [P(KeyCacheDesc), c_i64, c_vp, c_i32, c_i32, P(SketchDesc), c_vp, c_vp,
                            c_sz, c_vp]),
@@ -59,9 +62,13 @@ SIGNATURES = {
     "qjl_softmax_f64": (c_i32, [c_vp, c_i64, c_i64, c_dbl, c_vp, c_vp]),
     "qjl_decode_workspace": (c_sz, [P(KeyCacheDesc), P(ValueCacheDesc), c_i64, c_i32]),
     "qjl_decode": (c_i32, [P(KeyCacheDesc), P(ValueCacheDesc), c_i64, c_vp, c_i32, c_i32,
-                           P(SketchDesc), c_flt, c_vp, c_vp, c_vp, c_sz, c_vp]),
+                           P(SketchDesc), c_flt, c_vp, c_vp, c_vp, c_vp, c_sz, ctypes.c_uint, c_vp]),
     "qjl_decode_step": (c_i32, [P(KeyCacheDesc), P(ValueCacheDesc), c_i64, c_vp, c_i32, c_i32, P(SketchDesc),
-                                c_vp, c_i32, c_vp, c_vp, c_flt, c_vp, c_vp, c_vp, c_sz, c_vp]),
+                                c_vp, c_i32, c_vp, c_vp, c_flt, c_vp, c_vp, c_vp, c_vp, c_sz, ctypes.c_uint,
+                                c_vp]),
+    "qjl_bench_decode_kernel": (c_i32, [P(KeyCacheDesc), P(ValueCacheDesc), c_i64, c_vp, c_i32, c_i32,
+                                        P(SketchDesc), c_flt, c_vp, c_vp, c_vp, c_sz, c_i32, P(c_flt), c_vp]),
+    "qjl_tile_record": (c_i64, [c_i32, c_i32, c_i32, c_i32, P(c_i64)]),
     "qjl_timing_enable": (c_i32, [c_i32]),
     "qjl_timing_read": (c_i32, [P(c_dbl), P(c_i32), c_i32]),
     "qjl_quantize_values": (c_i32, [c_vp, c_i32, c_i64, c_i64, P(ValueCacheDesc), c_i64, c_vp]),
@@ -93,7 +100,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype, fn.argtypes = res, args
-    if lib.qjl_abi_version() != 1:
+    if lib.qjl_abi_version() != 2:
         raise ImportError("qjl_b200 ABI version mismatch")
     _lib = lib
     return lib

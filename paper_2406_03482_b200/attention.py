@@ -50,16 +50,18 @@ def quantized_decode(query: np.ndarray, state: KeyCacheState, value_tokens: list
     zero = torch.tensor([[float(t.zero)] for t in value_tokens], dtype=torch.float32, device=dev)[None]
     scale = torch.tensor([[float(t.scale)] for t in value_tokens], dtype=torch.float32, device=dev)[None]
     vd = _lib.ValueCacheDesc(codes.data_ptr(), zero.data_ptr(), scale.data_ptr(), n, 1, d, bits, d,
-                             _lib.QJL_VLAYOUT_U8)
+                             _lib.QJL_VLAYOUT_U8, 0, 0)
     c = state.device_cache
     c.n = n
     kd, sd = c.key_desc(), c.sketch_desc()
     q = state._query_tensor(query)
     out = torch.empty(1, 1, d, dtype=torch.float32, device=dev)
+    logits = torch.empty(1, n, dtype=torch.float32, device=dev)    # logits / T of this launch
     ws_b = int(lib.qjl_decode_workspace(ctypes.byref(kd), ctypes.byref(vd), n, 1))
     ws = c.workspace(ws_b)
     _lib.check(lib.qjl_decode(ctypes.byref(kd), ctypes.byref(vd), n, q.data_ptr(), _lib.QJL_F64, 1,
                               ctypes.byref(sd), 1.0 / float(temperature), out.data_ptr(), None,
-                              ws.data_ptr(), ws.numel(), _stream()), "quantized_decode")
-    weights = _softmax_rows(state._logits32(query), 1.0 / float(temperature))[0]
+                              logits.data_ptr(), ws.data_ptr(), ws.numel(), 0, _stream()), "quantized_decode")
+    # the ScoreVector is the fp64 softmax of the logits the fused decode itself consumed
+    weights = _softmax_rows(logits, 1.0)[0]
     return DecodeResult(output=out[0, 0].double().cpu().numpy(), scores=ScoreVector(weights=weights))

@@ -86,9 +86,26 @@ static int check_key_cache(const qjl_key_cache_t* kc) {
   QJL_CHECK_ARG(kc->m_in == 0 || (kc->bits_in && kc->norm_in), "bits_in/norm_in must be set when m_in > 0");
   QJL_CHECK_ARG(kc->m_out == 0 || (kc->bits_out && kc->norm_out), "bits_out/norm_out must be set when m_out > 0");
   QJL_CHECK_ARG(kc->capacity >= 0, "capacity must be >= 0");
+  QJL_CHECK_ARG(kc->tile_stride >= 0, "tile stride must be >= 0");
+  if (kc->tile_stride > 0) {
+    // tile-major caches are canonical records (keys only, or keys + P2T values)
+    QJL_CHECK_ARG(kc->capacity % 128 == 0, "tile-major caches hold whole 128-row tiles (capacity %lld)",
+                  (long long)kc->capacity);
+    const TileRecord rk = tile_record(kc->d, kc->m_in, kc->m_out, false);
+    const TileRecord rv = tile_record(kc->d, kc->m_in, kc->m_out, true);
+    QJL_CHECK_ARG(kc->tile_stride == rk.bytes || (kc->d == 128 && kc->tile_stride == rv.bytes),
+                  "tile stride %lld is not a record size of this shape (%lld keys only, %lld with values)",
+                  (long long)kc->tile_stride, (long long)rk.bytes, (long long)rv.bytes);
+    const uint8_t* b = kc->bits_in;
+    QJL_CHECK_ARG((const uint8_t*)kc->norm_in == b + rk.off[QJL_REC_NORM_IN] &&
+                      (kc->m_out == 0 || (kc->bits_out == b + rk.off[QJL_REC_BITS_OUT] &&
+                                          (const uint8_t*)kc->norm_out == b + rk.off[QJL_REC_NORM_OUT])),
+                  "key arrays of a tile-major cache must sit at their record offsets (qjl_tile_record)");
+  }
   return QJL_OK;
 }
 
+// value caches: P2T lives in the key cache's tile records; U8 is rows layout
 static int check_value_cache(const qjl_value_cache_t* vc, int d, int units) {
   QJL_CHECK_ARG(vc != nullptr, "value cache descriptor is NULL");
   QJL_CHECK_ARG(vc->codes && vc->zero && vc->scale, "value cache pointers must be set");
@@ -96,13 +113,17 @@ static int check_value_cache(const qjl_value_cache_t* vc, int d, int units) {
   QJL_CHECK_ARG(vc->units == units, "value units %d != key units %d", vc->units, units);
   QJL_CHECK_ARG(vc->bits >= 1 && vc->bits <= 8, "value bit width must be in [1, 8], got %d", vc->bits);
   QJL_CHECK_ARG(vc->group >= 1 && d % vc->group == 0, "value group %d must divide d=%d", vc->group, d);
-  if (vc->layout == QJL_VLAYOUT_P2 || vc->layout == QJL_VLAYOUT_P2T) {
+  if (vc->layout == QJL_VLAYOUT_P2T) {
     if (!(d == 128 && vc->bits == 2 && vc->group == 32)) {
-      set_error("P2/P2T value layouts are 2-bit, group 32, d = 128 (got d=%d bits=%d group=%d)", d, vc->bits, vc->group);
+      set_error("the P2T value layout is 2-bit, group 32, d = 128 (got d=%d bits=%d group=%d)", d, vc->bits,
+                vc->group);
       return QJL_ERR_UNSUPPORTED;
     }
+    QJL_CHECK_ARG(vc->tile_stride > 0 && vc->capacity % 128 == 0,
+                  "P2T values live in tile-major records (tile_stride > 0, capacity %% 128 == 0)");
   } else {
     QJL_CHECK_ARG(vc->layout == QJL_VLAYOUT_U8, "unknown value layout %d", vc->layout);
+    QJL_CHECK_ARG(vc->tile_stride == 0, "U8 value caches use the rows layout (tile_stride 0)");
   }
   if (d > 128) {
     set_error("decode supports head dim <= 128 (got %d)", d);
@@ -258,26 +279,28 @@ int qjl_quantize_keys(const void* keys, int dtype, int64_t n, int64_t key_unit_s
   int rc = launch_quantize_keys_tc(keys, dtype, n, key_unit_stride, *sketch, channels, h, *cache,
                                    row_offset, (cudaStream_t)stream);
   if (rc != QJL_ERR_UNSUPPORTED) return rc;
-  if (getenv("QJL_REQUIRE_TC")) {   // tests: refuse the generic path for tensor-core shapes
-    set_error("quantize_keys: tensor-core path refused this configuration (QJL_REQUIRE_TC set)");
-    return QJL_ERR_UNSUPPORTED;
-  }
   return launch_quantize_keys_simt(keys, dtype, n, key_unit_stride, *sketch, channels, h, *cache,
                                    row_offset, (cudaStream_t)stream);
 }
 
 int qjl_sketch_query(const void* q, int q_dtype, int units, int G, int d, const qjl_sketch_t* sketch,
-                     int m_total, float* sq, void* stream) {
+                     int m_total, int sq_dtype, void* sq, void* stream) {
   QJL_TRY(check_sketch(sketch));
   QJL_CHECK_ARG(q && sq, "NULL pointer");
   QJL_CHECK_ARG(valid_dtype(q_dtype), "bad query dtype %d", q_dtype);
+  QJL_CHECK_ARG(sq_dtype == QJL_F32 || sq_dtype == QJL_F64, "sketched queries are f32 or f64");
   QJL_CHECK_ARG(units >= 1 && G >= 1 && d >= 1 && d <= 1024 && m_total >= 1, "bad shape");
-  return launch_sketch_query(q, q_dtype, units, G, d, *sketch, m_total, m_total, sq, nullptr,
+  if (sq_dtype == QJL_F64)
+    return launch_sketch_query_f64(q, q_dtype, units, G, d, *sketch, m_total, (double*)sq, (cudaStream_t)stream);
+  return launch_sketch_query(q, q_dtype, units, G, d, *sketch, m_total, m_total, (float*)sq, nullptr,
                              (cudaStream_t)stream);
 }
 
 size_t qjl_scores_workspace(int units, int G, int m_total) {
-  return (size_t)units * G * (m_total + 2) * sizeof(float);
+  // generic: Sq + side sums; tensor-core: B images + constants + counters (<= this bound)
+  const size_t a = (size_t)units * G * (m_total + 2) * sizeof(float);
+  const size_t b = (size_t)units * (5 * 2048 + 64 + 8) + 1024;
+  return a > b ? a : b;
 }
 
 int qjl_scores(const qjl_key_cache_t* cache, int64_t n, const void* q, int q_dtype, int G,
@@ -298,9 +321,11 @@ int qjl_scores(const qjl_key_cache_t* cache, int64_t n, const void* q, int q_dty
     set_error("scores workspace needs %zu bytes", qjl_scores_workspace(cache->units, G, m_total));
     return QJL_ERR_WORKSPACE;
   }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cache->tile_stride > 0 && tile_path_supported(*cache, nullptr, G))
+    return launch_scores_tile(*cache, n, q, q_dtype, G, *sketch, logits, workspace, workspace_bytes, st);
   float* sq = (float*)workspace;
   float* sums = sq + (size_t)cache->units * G * m_total;
-  cudaStream_t st = (cudaStream_t)stream;
   QJL_TRY(launch_sketch_query(q, q_dtype, cache->units, G, cache->d, *sketch, cache->m_in, m_total,
                               sq, sums, st));
   return launch_scores_simt(*cache, n, G, sq, sums, logits, st);
@@ -333,22 +358,13 @@ int qjl_softmax_f64(const float* logits, int64_t rows, int64_t n, double inv_tem
 size_t qjl_decode_workspace(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int64_t n,
                             int G) {
   if (!cache || !values || n <= 0 || G <= 0) return 0;
-  const int m_total = cache->m_in + cache->m_out;
-  size_t a = decode_simt_workspace(cache->units, n, G, values->d, m_total);
-  if (decode_umma_supported(*cache, *values, G)) {
-    size_t b = decode_umma_workspace(*cache, *values, n, G);
-    return a > b ? a : b;
-  }
-  if (decode_tc_supported(*cache, *values, G)) {
-    size_t b = decode_tc_workspace(*cache, *values, n, G);
-    return a > b ? a : b;
-  }
-  return a;
+  if (values->layout == QJL_VLAYOUT_P2T) return decode_tile_workspace(*cache, n, G, false);
+  return decode_simt_workspace(cache->units, n, G, values->d, cache->m_in + cache->m_out);
 }
 
-int qjl_decode(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int64_t n, const void* q,
-               int q_dtype, int G, const qjl_sketch_t* sketch, float inv_temperature, float* out,
-               float* lse, void* workspace, size_t workspace_bytes, void* stream) {
+// shared argument checks of the decode entry points; *tile = the tensor-core path applies
+static int check_decode(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int64_t n, const void* q,
+                        int q_dtype, int G, const qjl_sketch_t* sketch, float inv_temperature, const float* out) {
   QJL_TRY(check_key_cache(cache));
   QJL_TRY(check_value_cache(values, cache->d, cache->units));
   QJL_TRY(check_sketch(sketch));
@@ -361,29 +377,64 @@ int qjl_decode(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, in
     return QJL_ERR_EMPTY;
   }
   QJL_CHECK_ARG(n <= cache->capacity && n <= values->capacity, "n exceeds capacity");
+  if (values->layout == QJL_VLAYOUT_P2T) {
+    if (!tile_path_supported(*cache, values, G)) {
+      set_error("P2T decode runs on the tensor-core path: d = 128, G <= 4, m_in/32 in {8, 16}, m_out/32 in "
+                "{0, 2, 4}, values in the keys' tile records (got d=%d G=%d m_in=%d m_out=%d)",
+                cache->d, G, cache->m_in, cache->m_out);
+      return QJL_ERR_UNSUPPORTED;
+    }
+  } else {
+    QJL_CHECK_ARG(cache->tile_stride == 0, "U8 caches use the rows layout");
+  }
+  return QJL_OK;
+}
+
+int qjl_decode(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int64_t n, const void* q,
+               int q_dtype, int G, const qjl_sketch_t* sketch, float inv_temperature, float* out,
+               float* lse, float* logits, void* workspace, size_t workspace_bytes, unsigned flags, void* stream) {
+  QJL_TRY(check_decode(cache, values, n, q, q_dtype, G, sketch, inv_temperature, out));
   const size_t need = qjl_decode_workspace(cache, values, n, G);
   if (!workspace || workspace_bytes < need) {
     set_error("decode workspace needs %zu bytes (got %zu)", need, workspace_bytes);
     return QJL_ERR_WORKSPACE;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  if (decode_umma_supported(*cache, *values, G))
-    return launch_decode_umma(*cache, *values, n, q, q_dtype, G, *sketch, inv_temperature, out, lse,
-                              workspace, workspace_bytes, st);
-  if (decode_tc_supported(*cache, *values, G))
-    return launch_decode_tc(*cache, *values, n, q, q_dtype, G, *sketch, inv_temperature, out, lse,
-                            workspace, workspace_bytes, st);
-  if (getenv("QJL_REQUIRE_TC")) {
-    set_error("decode: tensor-core path refused this configuration (QJL_REQUIRE_TC set)");
-    return QJL_ERR_UNSUPPORTED;
-  }
+  if (values->layout == QJL_VLAYOUT_P2T)
+    return launch_decode_tile(*cache, n, q, q_dtype, G, *sketch, inv_temperature, out, lse, logits, workspace,
+                              workspace_bytes, flags, st);
   const int m_total = cache->m_in + cache->m_out;
   float* sq = (float*)workspace;
   float* sums = sq + (size_t)cache->units * G * m_total;
   float* part = sums + (size_t)cache->units * G * 2;
   QJL_TRY(launch_sketch_query(q, q_dtype, cache->units, G, cache->d, *sketch, cache->m_in, m_total,
                               sq, sums, st));
-  return launch_decode_simt(*cache, *values, n, G, sq, sums, inv_temperature, out, lse, part, st);
+  return launch_decode_simt(*cache, *values, n, G, sq, sums, inv_temperature, out, lse, logits, part, st);
+}
+
+int qjl_bench_decode_kernel(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int64_t n,
+                            const void* q, int q_dtype, int G, const qjl_sketch_t* sketch, float inv_temperature,
+                            float* out, float* lse, void* workspace, size_t workspace_bytes, int reps, float* ms,
+                            void* stream) {
+  QJL_TRY(check_decode(cache, values, n, q, q_dtype, G, sketch, inv_temperature, out));
+  QJL_CHECK_ARG(values->layout == QJL_VLAYOUT_P2T, "the benchmark hook times the tensor-core decode (P2T)");
+  QJL_CHECK_ARG(reps >= 1 && ms, "reps must be >= 1 and ms set");
+  const size_t need = qjl_decode_workspace(cache, values, n, G);
+  if (!workspace || workspace_bytes < need) {
+    set_error("decode workspace needs %zu bytes (got %zu)", need, workspace_bytes);
+    return QJL_ERR_WORKSPACE;
+  }
+  return bench_decode_tile(*cache, n, q, q_dtype, G, *sketch, inv_temperature, out, lse, workspace,
+                           workspace_bytes, reps, ms, (cudaStream_t)stream);
+}
+
+int64_t qjl_tile_record(int d, int m_in, int m_out, int values, int64_t* offsets) {
+  if (d < 1 || m_in < 0 || m_out < 0 || m_in % 32 || m_out % 32) return -1;
+  if (values && d != 128) return -1;
+  const TileRecord r = tile_record(d, m_in, m_out, values != 0);
+  if (offsets)
+    for (int i = 0; i < QJL_REC_FIELDS; ++i) offsets[i] = r.off[i];
+  return r.bytes;
 }
 
 int qjl_quantize_values(const void* v, int dtype, int64_t n, int64_t unit_stride,
@@ -409,6 +460,10 @@ static int check_qjlc(const qjl_key_cache_t* kc, const qjl_value_cache_t* vc, in
                       int64_t row_offset, int64_t n, const void* records, int64_t ustride) {
   QJL_TRY(check_key_cache(kc));
   QJL_CHECK_ARG(records != nullptr, "records buffer is NULL");
+  if (kc->tile_stride != 0) {
+    set_error("QJLC records move rows-layout caches (the file's value format is U8)");
+    return QJL_ERR_UNSUPPORTED;
+  }
   QJL_CHECK_ARG(mfi >= 0 && mfi <= kc->m_in && (mfi > 0) == (kc->m_in > 0),
                 "file inlier width %d does not fit the cache's %d bits", mfi, kc->m_in);
   QJL_CHECK_ARG(mfo >= 0 && mfo <= kc->m_out && (mfo > 0) == (kc->m_out > 0),
@@ -471,7 +526,7 @@ int qjl_orthogonalize(const double* gaussian, int batch, int m, int d, double* o
 int qjl_decode_step(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int64_t n, const void* q,
                     int q_dtype, int G, const qjl_sketch_t* sketch, const int32_t* channels, int h,
                     const void* k_new, const void* v_new, float inv_temperature, float* out, float* lse,
-                    void* workspace, size_t workspace_bytes, void* stream) {
+                    float* logits, void* workspace, size_t workspace_bytes, unsigned flags, void* stream) {
   QJL_TRY(check_key_cache(cache));
   QJL_TRY(check_value_cache(values, cache->d, cache->units));
   QJL_TRY(check_sketch(sketch));
@@ -479,10 +534,12 @@ int qjl_decode_step(const qjl_key_cache_t* cache, const qjl_value_cache_t* value
   QJL_CHECK_ARG(valid_dtype(q_dtype) && q_dtype != QJL_F64, "bad query dtype %d", q_dtype);
   QJL_CHECK_ARG(G >= 1, "G must be >= 1");
   QJL_CHECK_ARG(inv_temperature > 0.f, "temperature must be positive");
-  QJL_CHECK_ARG(h >= 0 && (h == 0 || channels != nullptr), "channels is NULL");
+  QJL_CHECK_ARG(h >= 0 && h <= cache->d && (h == 0 || channels != nullptr), "bad outlier channels");
+  QJL_CHECK_ARG((h > 0) == (cache->m_out > 0), "outlier sketch must be present exactly when h > 0");
   QJL_CHECK_ARG(n >= 0 && n + 1 <= cache->capacity && n + 1 <= values->capacity, "n + 1 exceeds capacity");
-  if (!decode_umma_supported(*cache, *values, G)) {
-    set_error("decode_step runs on the tcgen05 path (P2T values, supported sketch widths); append + decode instead");
+  if (values->layout != QJL_VLAYOUT_P2T || !tile_path_supported(*cache, values, G)) {
+    set_error("decode_step runs on the tensor-core path (P2T tile records, supported sketch widths); "
+              "append + decode instead");
     return QJL_ERR_UNSUPPORTED;
   }
   const size_t need = qjl_decode_workspace(cache, values, n + 1, G);
@@ -490,8 +547,9 @@ int qjl_decode_step(const qjl_key_cache_t* cache, const qjl_value_cache_t* value
     set_error("decode workspace needs %zu bytes (got %zu)", need, workspace_bytes);
     return QJL_ERR_WORKSPACE;
   }
-  return launch_decode_step_umma(*cache, *values, n, q, q_dtype, G, *sketch, channels, h, k_new, v_new,
-                                 inv_temperature, out, lse, workspace, workspace_bytes, (cudaStream_t)stream);
+  return launch_decode_step_tile(*cache, *values, n, q, q_dtype, G, *sketch, channels, h, k_new, v_new,
+                                 inv_temperature, out, lse, logits, workspace, workspace_bytes, flags,
+                                 (cudaStream_t)stream);
 }
 
 }  // extern "C"

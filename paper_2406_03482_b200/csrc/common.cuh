@@ -106,33 +106,46 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
   return v;
 }
 
-// ----------------------------------------------------------- P2 value layout
-// 2-bit codes, group 32, d = 128: 32 bytes per token, interleaved inside each
-// 128-token tile so that one u32 word holds 4 tokens x 4 dims -- the A operand
-// register of the PV IMMA (mma.m16n8k32 u8) after a single mask, `w & (3 << 2s)`
-// per byte.  For row t of a unit and dim d:
-//   tile = t >> 7, slice = (t >> 5) & 3 (the warp that consumes it),
-//   j = t & 7 (k-block = tokens j, j+8, j+16, j+24 of the slice), i = (t >> 3) & 3 (byte),
-//   MT = d >> 4 (m-tile), g = d & 7 (fragment row), r = (d >> 3) & 1, k = MT >> 1,
-//   s = 2 * (MT & 1) + r (2-bit slot inside the byte)
-//   word = tile * 1024 + slice * 256 + (g * 8 + (j ^ ((g & 1) << 2))) * 4 + k
-// The j ^ 4 swizzle on odd rows makes the per-lane 16-byte loads bank-conflict free.
-__host__ __device__ __forceinline__ void p2_pos(int64_t t, int d, int64_t* byte, int* shift) {
-  const int64_t tile = t >> 7;
-  const int slice = (int)(t >> 5) & 3, j = (int)t & 7, i = (int)(t >> 3) & 3;
-  const int MT = d >> 4, g = d & 7, r = (d >> 3) & 1, k = MT >> 1, s = 2 * (MT & 1) + r;
-  const int64_t word = tile * 1024 + slice * 256 + (g * 8 + (j ^ ((g & 1) << 2))) * 4 + k;
-  *byte = word * 4 + i;
-  *shift = 2 * s;
+// ------------------------------------------------------------- row addressing
+// Byte offset of row `row` of unit `u` in a cache array with `rb` bytes per row
+// (qjl_b200.h, tile_stride): rows layout [units][capacity][rb] when ts == 0, else
+// tile-major records -- unit u's 128-row tile j starts (u * capacity/128 + j) * ts in.
+__host__ __device__ __forceinline__ int64_t row_off(int64_t u, int64_t row, int64_t rb, int64_t cap, int64_t ts) {
+  return ts ? (u * (cap >> 7) + (row >> 7)) * ts + (row & 127) * rb : (u * cap + row) * rb;
+}
+// Byte offset of the 128-token tile holding row `row` of an array whose tiles are
+// `tile_bytes` long in the rows layout (e.g. 4096 for P2T codes).
+__host__ __device__ __forceinline__ int64_t tile_off(int64_t u, int64_t row, int64_t tile_bytes, int64_t cap,
+                                                     int64_t ts) {
+  return (u * (cap >> 7) + (row >> 7)) * (ts ? ts : tile_bytes);
 }
 
 // P2T value-code layout (tcgen05 decode): one u32 word = 4 consecutive tokens (bytes)
 // x 4 dims (2-bit slots), so one mask per word yields the u8 A-operand column of a
-// TMEM-resident PV operand (row = dim, weight 4^(d % 4) folded out per row):
-//   byte = tile * 4096 + (d >> 2) * 128 + ((t & 127) >> 2) * 4 + (t & 3), shift = 2 * (d & 3)
-__host__ __device__ __forceinline__ void p2t_pos(int64_t t, int d, int64_t* byte, int* shift) {
-  *byte = (t >> 7) * 4096 + (int64_t)(d >> 2) * 128 + ((t & 127) >> 2) * 4 + (t & 3);
-  *shift = 2 * (d & 3);
+// TMEM-resident PV operand (row = dim, weight 4^(d % 4) folded out per row).  In-tile
+// byte of (token t, dim d), and the bit shift of its 2-bit slot:
+//   byte = (d >> 2) * 128 + ((t & 127) >> 2) * 4 + (t & 3), shift = 2 * (d & 3)
+__host__ __device__ __forceinline__ int p2t_byte(int64_t t, int d) {
+  return (d >> 2) * 128 + (int)((t & 127) >> 2) * 4 + (int)(t & 3);
+}
+
+// Canonical tile record (qjl_b200.h: qjl_tile_record): offsets of the QJL_REC_* fields.
+struct TileRecord {
+  int64_t off[QJL_REC_FIELDS];
+  int64_t bytes;
+};
+__host__ __device__ inline TileRecord tile_record(int d, int m_in, int m_out, bool values) {
+  TileRecord r;
+  int64_t o = 0;
+  r.off[QJL_REC_BITS_IN] = o;  o += 128 * (int64_t)(m_in / 8);
+  r.off[QJL_REC_BITS_OUT] = m_out ? o : -1;  o += 128 * (int64_t)(m_out / 8);
+  r.off[QJL_REC_NORM_IN] = o;  o += 256;
+  r.off[QJL_REC_NORM_OUT] = m_out ? o : -1;  o += m_out ? 256 : 0;
+  r.off[QJL_REC_CODES] = values ? o : -1;  o += values ? 128 * (int64_t)(d / 4) : 0;
+  r.off[QJL_REC_ZERO] = values ? o : -1;  o += values ? 128 * 2 * (int64_t)(d / 32) : 0;
+  r.off[QJL_REC_SCALE] = values ? o : -1;  o += values ? 128 * 2 * (int64_t)(d / 32) : 0;
+  r.bytes = o;
+  return r;
 }
 
 }  // namespace qjl

@@ -1,8 +1,8 @@
-// Generic fused decode (scores -> online softmax -> weights @ dequantized V),
-// flash-decoding split over tokens with an fp32 (m, l, acc) merge.  Handles
-// both value layouts (U8 reference format, P2 packed), any G <= 8, any m%32==0.
-// The tensor-core fast path for P2 caches is k_decode_tc.cu; this kernel is
-// the general-shape path and the cross-check for it.
+// Generic fused decode (scores -> online softmax -> weights @ dequantized V) for the
+// reference's own value format (U8 codes, fp32 zero/scale, any bit width and group),
+// rows-layout caches, any G <= 8, any m % 32 == 0 -- the path behind the drop-in
+// `quantized_decode` (attention.py:56-71) for shapes outside the tensor-core envelope.
+// Flash-decoding split over tokens with an fp32 (m, l, acc) merge.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -30,20 +30,9 @@ __device__ __forceinline__ void set_sums_dec(const uint8_t* __restrict__ bits, i
 __device__ __forceinline__ float load_value(const qjl_value_cache_t& vc, int64_t row, int dim) {
   const int G = vc.d / vc.group;
   const int grp = dim / vc.group;
-  if (vc.layout == QJL_VLAYOUT_U8) {
-    const float z = reinterpret_cast<const float*>(vc.zero)[row * G + grp];
-    const float s = reinterpret_cast<const float*>(vc.scale)[row * G + grp];
-    const float c = (float)reinterpret_cast<const uint8_t*>(vc.codes)[row * vc.d + dim];
-    return fmaf(c, s, z);
-  }
-  // row = unit * capacity + t; capacity % 128 == 0, so tiles never straddle units
-  int64_t byte;
-  int sh;
-  if (vc.layout == QJL_VLAYOUT_P2T) p2t_pos(row, dim, &byte, &sh);
-  else p2_pos(row, dim, &byte, &sh);
-  const float c = (float)((reinterpret_cast<const uint8_t*>(vc.codes)[byte] >> sh) & 3u);
-  const float z = f16_bits_to_f32(reinterpret_cast<const uint16_t*>(vc.zero)[row * G + grp]);
-  const float s = f16_bits_to_f32(reinterpret_cast<const uint16_t*>(vc.scale)[row * G + grp]);
+  const float z = reinterpret_cast<const float*>(vc.zero)[row * G + grp];
+  const float s = reinterpret_cast<const float*>(vc.scale)[row * G + grp];
+  const float c = (float)reinterpret_cast<const uint8_t*>(vc.codes)[row * vc.d + dim];
   return fmaf(c, s, z);
 }
 
@@ -53,7 +42,7 @@ __global__ void __launch_bounds__(kDTile) k_decode_simt(qjl_key_cache_t kc, qjl_
                                                         int64_t n, int G, int64_t chunk,
                                                         const float* __restrict__ sq,
                                                         const float* __restrict__ sums, float inv_t,
-                                                        float* __restrict__ ws) {
+                                                        float* __restrict__ logits, float* __restrict__ ws) {
   extern __shared__ float sm[];
   const int m_in = kc.m_in, m_out = kc.m_out, m_total = m_in + m_out, d = vc.d;
   float* sqs = sm;                              // [G][m_total]
@@ -95,6 +84,7 @@ __global__ void __launch_bounds__(kDTile) k_decode_simt(qjl_key_cache_t kc, qjl_
           float v = c_in * nu_in * (2.f * a_in[g] - ssum[2 * g]);
           if (m_out > 0) v += c_out * nu_out * (2.f * a_out[g] - ssum[2 * g + 1]);
           lg[g] = v * inv_t;
+          if (logits) logits[((int64_t)u * G + g) * n + t] = lg[g];
         }
       }
     }
@@ -197,7 +187,7 @@ size_t decode_simt_workspace(int units, int64_t n, int G, int d, int m_total) {
 
 int launch_decode_simt(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, int G,
                        const float* sq, const float* sums, float inv_t, float* out, float* lse,
-                       float* ws, cudaStream_t st) {
+                       float* logits, float* ws, cudaStream_t st) {
   int nsplit;
   int64_t chunk;
   decode_simt_plan(kc.units, n, &nsplit, &chunk);
@@ -208,9 +198,7 @@ int launch_decode_simt(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, i
   if (G <= GM) {                                                                            \
     cudaFuncSetAttribute(k_decode_simt<GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                          (int)smem);                                                        \
-    timing_begin(st);                                                                       \
-    k_decode_simt<GM><<<grid, kDTile, smem, st>>>(kc, vc, n, G, chunk, sq, sums, inv_t, ws); \
-    timing_end(st);                                                                         \
+    k_decode_simt<GM><<<grid, kDTile, smem, st>>>(kc, vc, n, G, chunk, sq, sums, inv_t, logits, ws); \
     QJL_LAUNCH_CHECK("decode_simt");                                                        \
     k_decode_merge<<<kc.units * G, 128, 0, st>>>(ws, nsplit, G, vc.d, out, lse);            \
     QJL_LAUNCH_CHECK("decode_merge");                                                       \

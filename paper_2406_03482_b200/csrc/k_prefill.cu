@@ -641,9 +641,10 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_keys_simt(
       const int64_t row = row_offset + t0 + t;
       if (lane == 0 && t0 + t < n) {
         if (r0 < m_in) {
-          reinterpret_cast<uint32_t*>(kc.bits_in + ((int64_t)u * kc.capacity + row) * (m_in / 8))[r0 / 32] = word;
+          reinterpret_cast<uint32_t*>(kc.bits_in + row_off(u, row, m_in / 8, kc.capacity, kc.tile_stride))[r0 / 32] = word;
         } else {
-          reinterpret_cast<uint32_t*>(kc.bits_out + ((int64_t)u * kc.capacity + row) * (m_out / 8))[(r0 - m_in) / 32] = word;
+          reinterpret_cast<uint32_t*>(kc.bits_out + row_off(u, row, m_out / 8, kc.capacity, kc.tile_stride))[(r0 - m_in) / 32] =
+              word;
         }
       }
     }
@@ -661,9 +662,10 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_keys_simt(
     s_in = warp_sum_f64(s_in);
     s_out = warp_sum_f64(s_out);
     if (lane == 0) {
-      const int64_t row = (int64_t)u * kc.capacity + row_offset + t0 + t;
-      kc.norm_in[row] = f16_canon(f64_to_f16_bits(sqrt(s_in)));
-      if (m_out > 0) kc.norm_out[row] = f16_canon(f64_to_f16_bits(sqrt(s_out)));
+      const int64_t no = row_off(u, row_offset + t0 + t, 2, kc.capacity, kc.tile_stride);
+      *reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(kc.norm_in) + no) = f16_canon(f64_to_f16_bits(sqrt(s_in)));
+      if (m_out > 0)
+        *reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(kc.norm_out) + no) = f16_canon(f64_to_f16_bits(sqrt(s_out)));
     }
   }
 }
@@ -726,7 +728,7 @@ int launch_quantize_keys_simt(const void* keys, int dtype, int64_t n, int64_t ku
 // Value quantizer (kvcache.py:140-161) per group: zero = min, scale =
 // (max - min)/(2^b - 1), codes = clip(rint((v - zero)/scale)) -- all in fp64 so
 // codes match the reference bit for bit (IEEE div + rint are exact-rounded);
-// constant group -> scale 0, codes 0.  Constants stored fp16 (P2) or f32 (U8).
+// constant group -> scale 0, codes 0.  Constants stored fp16 (P2T) or f32 (U8).
 // One warp per token; lane l owns dims l + 32*i.
 // ---------------------------------------------------------------------------
 template <typename T>
@@ -740,9 +742,9 @@ __global__ void __launch_bounds__(256) k_quantize_values(const T* __restrict__ v
   const int levels = (1 << vc.bits) - 1;
   const bool valid = t < n;
   const T* V = v + (int64_t)u * unit_stride + (valid ? t : 0) * d;
-  const int64_t row = (int64_t)u * vc.capacity + row_offset + t;
-  const bool p2 = vc.layout == QJL_VLAYOUT_P2 || vc.layout == QJL_VLAYOUT_P2T;
-  const bool p2t = vc.layout == QJL_VLAYOUT_P2T;
+  const int64_t r = row_offset + t;
+  const int64_t row = (int64_t)u * vc.capacity + r;   // U8 (rows layout) row index
+  const bool p2 = vc.layout == QJL_VLAYOUT_P2T;
   for (int g = 0; g < G; ++g) {
     // group g spans dims [g*gs, (g+1)*gs); lanes stride over it
     double mn = INFINITY, mx = -INFINITY;
@@ -770,30 +772,13 @@ __global__ void __launch_bounds__(256) k_quantize_values(const T* __restrict__ v
       if (!p2) {
         if (valid) reinterpret_cast<uint8_t*>(vc.codes)[row * d + dim] = (uint8_t)code;
       } else {
-        if (p2t) {
-          // P2T: dims 4a..4a+3 share a byte (slot = dim & 3); OR the four lanes together
-          uint32_t b = (uint32_t)code << (2 * (lane & 3));
-          b |= __shfl_xor_sync(0xffffffffu, b, 1);
-          b |= __shfl_xor_sync(0xffffffffu, b, 2);
-          if (valid && (lane & 3) == 0) {
-            int64_t byte;
-            int sh;
-            p2t_pos(row, dim, &byte, &sh);
-            reinterpret_cast<uint8_t*>(vc.codes)[byte] = (uint8_t)b;
-          }
-        } else {
-          // P2 (d = 128, group 32, 2 bits): dim 32g + lane sits in byte (row g & 7 =
-          // lane & 7, k = g) at slot lane >> 3; OR the four slots of a byte together
-          uint32_t b = (uint32_t)code << (2 * (lane >> 3));
-          b |= __shfl_xor_sync(0xffffffffu, b, 8);
-          b |= __shfl_xor_sync(0xffffffffu, b, 16);
-          if (valid && lane < 8) {
-            int64_t byte;
-            int sh;
-            p2_pos(row, dim, &byte, &sh);
-            reinterpret_cast<uint8_t*>(vc.codes)[byte] = (uint8_t)b;
-          }
-        }
+        // P2T: dims 4a..4a+3 share a byte (slot = dim & 3); OR the four lanes together
+        uint32_t b = (uint32_t)code << (2 * (lane & 3));
+        b |= __shfl_xor_sync(0xffffffffu, b, 1);
+        b |= __shfl_xor_sync(0xffffffffu, b, 2);
+        if (valid && (lane & 3) == 0)
+          reinterpret_cast<uint8_t*>(vc.codes)[tile_off(u, r, 4096, vc.capacity, vc.tile_stride) + p2t_byte(r, dim)] =
+              (uint8_t)b;
       }
     }
     if (valid && lane == 0) {
@@ -801,8 +786,9 @@ __global__ void __launch_bounds__(256) k_quantize_values(const T* __restrict__ v
         reinterpret_cast<float*>(vc.zero)[row * G + g] = (float)zero;
         reinterpret_cast<float*>(vc.scale)[row * G + g] = (float)scale;
       } else {
-        reinterpret_cast<uint16_t*>(vc.zero)[row * G + g] = f64_to_f16_bits(zero);
-        reinterpret_cast<uint16_t*>(vc.scale)[row * G + g] = f64_to_f16_bits(scale);
+        const int64_t o = row_off(u, r, 2 * G, vc.capacity, vc.tile_stride) + 2 * g;
+        *reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(vc.zero) + o) = f64_to_f16_bits(zero);
+        *reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(vc.scale) + o) = f64_to_f16_bits(scale);
       }
     }
   }
@@ -823,9 +809,9 @@ __global__ void __launch_bounds__(256) k_quantize_values_p2t(const T* __restrict
   const int64_t t0 = (idx >> 2) * 4;                    // first token of this thread's block
   if (t0 >= n) return;
   const T* V = v + (int64_t)u * unit_stride;
-  uint8_t* codes = reinterpret_cast<uint8_t*>(vc.codes) + (int64_t)u * vc.capacity * 32;
-  uint16_t* zo = reinterpret_cast<uint16_t*>(vc.zero) + (int64_t)u * vc.capacity * 4;
-  uint16_t* so = reinterpret_cast<uint16_t*>(vc.scale) + (int64_t)u * vc.capacity * 4;
+  uint8_t* codes = reinterpret_cast<uint8_t*>(vc.codes);
+  uint8_t* zo = reinterpret_cast<uint8_t*>(vc.zero);
+  uint8_t* so = reinterpret_cast<uint8_t*>(vc.scale);
   uint32_t cw[4][8];                                    // [token][byte a = 4-dim slot group] (bits of one byte)
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -851,9 +837,9 @@ __global__ void __launch_bounds__(256) k_quantize_values_p2t(const T* __restrict
     const double mn64 = (double)mn, mx64 = (double)mx;   // inputs are exact in fp32
     const double spread = mx64 - mn64;
     const double scale = spread == 0.0 ? 0.0 : spread / 3.0;
-    const int64_t row = row_offset + t;
-    zo[row * 4 + g] = f64_to_f16_bits(mn64);
-    so[row * 4 + g] = f64_to_f16_bits(scale);
+    const int64_t co = row_off(u, row_offset + t, 8, vc.capacity, vc.tile_stride) + 2 * g;
+    *reinterpret_cast<uint16_t*>(zo + co) = f64_to_f16_bits(mn64);
+    *reinterpret_cast<uint16_t*>(so + co) = f64_to_f16_bits(scale);
     if (spread != 0.0) {
       const float inv = 3.0f / (float)spread;
 #pragma unroll
@@ -873,9 +859,7 @@ __global__ void __launch_bounds__(256) k_quantize_values_p2t(const T* __restrict
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
       const uint32_t w = cw[0][a] | (cw[1][a] << 8) | (cw[2][a] << 16) | (cw[3][a] << 24);
-      int64_t byte;
-      int sh;
-      p2t_pos(r0, 32 * g + 4 * a, &byte, &sh);
+      const int64_t byte = tile_off(u, r0, 4096, vc.capacity, vc.tile_stride) + p2t_byte(r0, 32 * g + 4 * a);
       *reinterpret_cast<uint32_t*>(codes + byte) = w;
     }
   } else {
@@ -884,10 +868,8 @@ __global__ void __launch_bounds__(256) k_quantize_values_p2t(const T* __restrict
       if (t0 + i >= n) break;
 #pragma unroll
       for (int a = 0; a < 8; ++a) {
-        int64_t byte;
-        int sh;
-        p2t_pos(r0 + i, 32 * g + 4 * a, &byte, &sh);
-        codes[byte] = (uint8_t)cw[i][a];
+        codes[tile_off(u, r0 + i, 4096, vc.capacity, vc.tile_stride) + p2t_byte(r0 + i, 32 * g + 4 * a)] =
+            (uint8_t)cw[i][a];
       }
     }
   }

@@ -24,6 +24,10 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef QJL_K1_ABLATE
+#define QJL_K1_ABLATE 0      // perf experiments only (tools/k1_ablate.sh builds variants)
+#endif
+
 namespace qjl {
 namespace qtc {
 
@@ -504,9 +508,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         }
       }
       if (tok < P.n) {
-        const int64_t crow = (int64_t)u * P.kc.capacity + P.row_offset + tok;
-        P.kc.norm_in[crow] = f16_canon(nin16);
-        if (m_out > 0) P.kc.norm_out[crow] = f16_canon(nout16);
+        const int64_t no = row_off(u, P.row_offset + tok, 2, P.kc.capacity, P.kc.tile_stride);
+        *reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(P.kc.norm_in) + no) = f16_canon(nin16);
+        if (m_out > 0) *reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(P.kc.norm_out) + no) = f16_canon(nout16);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_empty[s]);
@@ -521,7 +525,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     for (int it = 0; it < ntiles; ++it) {
       const int64_t tok = (int64_t)lt * kM + row;
       const bool valid = tok < P.n;
-      const int64_t crow = (int64_t)u * P.kc.capacity + P.row_offset + tok;
+      uint8_t* const rin = P.kc.bits_in + row_off(u, P.row_offset + tok, m_in / 8, P.kc.capacity, P.kc.tile_stride);
+      uint8_t* const rout =
+          m_out ? P.kc.bits_out + row_off(u, P.row_offset + tok, m_out / 8, P.kc.capacity, P.kc.tile_stride) : nullptr;
       for (int c = 0; c < NC; ++c, ++chunk) {
         if ((chunk & 1) != set) continue;      // the two warp sets alternate chunks
         const int buf = chunk % L::NBUF;
@@ -537,11 +543,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
                                              : QJL_K1_FASTSIGN ? sign_word_fast(r + 32) : sign_word(r + 32);
           const int sr = c * CH + g64 * 64;      // first sketch row of the word pair
           if (valid) {
-            uint32_t* d0 = sr < m_in ? reinterpret_cast<uint32_t*>(P.kc.bits_in + crow * (m_in / 8)) + (sr >> 5)
-                                     : reinterpret_cast<uint32_t*>(P.kc.bits_out + crow * (m_out / 8)) + ((sr - m_in) >> 5);
+            uint32_t* d0 = sr < m_in ? reinterpret_cast<uint32_t*>(rin) + (sr >> 5)
+                                     : reinterpret_cast<uint32_t*>(rout) + ((sr - m_in) >> 5);
             const int s1 = sr + 32;
-            uint32_t* d1 = s1 < m_in ? reinterpret_cast<uint32_t*>(P.kc.bits_in + crow * (m_in / 8)) + (s1 >> 5)
-                                     : reinterpret_cast<uint32_t*>(P.kc.bits_out + crow * (m_out / 8)) + ((s1 - m_in) >> 5);
+            uint32_t* d1 = s1 < m_in ? reinterpret_cast<uint32_t*>(rin) + (s1 >> 5)
+                                     : reinterpret_cast<uint32_t*>(rout) + ((s1 - m_in) >> 5);
             if (d1 == d0 + 1 && ((reinterpret_cast<uintptr_t>(d0) & 7) == 0)) {
               *reinterpret_cast<uint2*>(d0) = make_uint2(w0, w1);
             } else {
@@ -558,9 +564,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
           const int sr = c * CH + CH - 32;
           if (valid) {
             if (sr < m_in)
-              reinterpret_cast<uint32_t*>(P.kc.bits_in + crow * (m_in / 8))[sr >> 5] = w;
+              reinterpret_cast<uint32_t*>(rin)[sr >> 5] = w;
             else
-              reinterpret_cast<uint32_t*>(P.kc.bits_out + crow * (m_out / 8))[(sr - m_in) >> 5] = w;
+              reinterpret_cast<uint32_t*>(rout)[(sr - m_in) >> 5] = w;
           }
         }
         if (QJL_K1_ZEROACC) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");   // zeros landed
@@ -631,7 +637,7 @@ static int launch_impl(const void* keys, int64_t n, int64_t kus, const qjl_sketc
   P.T = (int64_t)kc.units * P.tpu;
   P.s_per_unit = sk.unit_stride ? 1 : 0;
   P.keys = (const uint8_t*)keys;
-  P.ablate = getenv("QJL_K1_ABLATE") ? atoi(getenv("QJL_K1_ABLATE")) : 0;
+  P.ablate = QJL_K1_ABLATE;
   P.key_unit_bytes = kus * 2;
   auto kern = k_quant_tc<MT, NC, STAGES, ABF>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
@@ -649,7 +655,6 @@ int launch_quantize_keys_tc(const void* keys, int dtype, int64_t n, int64_t kus,
                             const int32_t* ch, int h, const qjl_key_cache_t& kc, int64_t row_offset,
                             cudaStream_t st) {
   using namespace qtc;
-  if (getenv("QJL_FORCE_SIMT")) return QJL_ERR_UNSUPPORTED;
   if (kc.d != kK || !(dtype == QJL_BF16 || dtype == QJL_F16) || sk.dtype != dtype) return QJL_ERR_UNSUPPORTED;
   if (h > 64 || kus % 8 != 0 || kus == 0) return QJL_ERR_UNSUPPORTED;   // kus == 0: shared keys (SIMT)
   if (((uintptr_t)keys & 15) || ((uintptr_t)sk.s_full & 15)) return QJL_ERR_UNSUPPORTED;

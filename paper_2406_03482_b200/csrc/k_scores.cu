@@ -10,11 +10,11 @@ namespace qjl {
 // `sums` (f32 [units][G][2]), the per-side totals sum_j Sq_j used by the
 // 2*sum_set - sum_all identity (estimator.py:164-169).
 // ---------------------------------------------------------------------------
-template <typename TQ, typename TS>
+template <typename TQ, typename TS, typename TO>
 __global__ void __launch_bounds__(256) k_sketch_query(const TQ* __restrict__ q, int G, int d,
                                                       const TS* __restrict__ s_full,
                                                       int64_t s_unit_stride, int m_in, int m_total,
-                                                      float* __restrict__ sq,
+                                                      TO* __restrict__ sq,
                                                       float* __restrict__ sums) {
   extern __shared__ double qs[];  // [d] then [8] warp partials x 2
   const int ug = blockIdx.x;
@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256) k_sketch_query(const TQ* __restrict__ q, 
     const TS* row = S + (int64_t)r * d;
     double acc = 0.0;
     for (int c = 0; c < d; ++c) acc = fma(to_f64(row[c]), qs[c], acc);
-    sq[(int64_t)ug * m_total + r] = (float)acc;
+    sq[(int64_t)ug * m_total + r] = (TO)acc;
     if (r < m_in) part_in += (double)(float)acc; else part_out += (double)(float)acc;
   }
   if (sums) {
@@ -47,14 +47,14 @@ __global__ void __launch_bounds__(256) k_sketch_query(const TQ* __restrict__ q, 
   }
 }
 
-template <typename TQ>
+template <typename TQ, typename TO>
 static int launch_sq_1(const void* q, int units, int G, int d, const qjl_sketch_t& sk, int m_in,
-                       int m_total, float* sq, float* sums, cudaStream_t st) {
+                       int m_total, TO* sq, float* sums, cudaStream_t st) {
   const size_t smem = (d + 16) * sizeof(double);
   switch (sk.dtype) {
 #define QJL_SQ(DT)                                                                           \
   case DT:                                                                                   \
-    k_sketch_query<TQ, Elem<DT>::T><<<units * G, 256, smem, st>>>(                           \
+    k_sketch_query<TQ, Elem<DT>::T, TO><<<units * G, 256, smem, st>>>(                       \
         (const TQ*)q, G, d, (const Elem<DT>::T*)sk.s_full, sk.unit_stride, m_in, m_total,    \
         sq, sums);                                                                           \
     break;
@@ -69,16 +69,27 @@ static int launch_sq_1(const void* q, int units, int G, int d, const qjl_sketch_
   return QJL_OK;
 }
 
+template <typename TO>
+static int launch_sq_o(const void* q, int q_dtype, int units, int G, int d, const qjl_sketch_t& sk, int m_in,
+                       int m_total, TO* sq, float* sums, cudaStream_t st) {
+  switch (q_dtype) {
+    case QJL_F32: return launch_sq_1<float, TO>(q, units, G, d, sk, m_in, m_total, sq, sums, st);
+    case QJL_F16: return launch_sq_1<__half, TO>(q, units, G, d, sk, m_in, m_total, sq, sums, st);
+    case QJL_BF16: return launch_sq_1<__nv_bfloat16, TO>(q, units, G, d, sk, m_in, m_total, sq, sums, st);
+    case QJL_F64: return launch_sq_1<double, TO>(q, units, G, d, sk, m_in, m_total, sq, sums, st);
+  }
+  return QJL_ERR_ARG;
+}
+
 int launch_sketch_query(const void* q, int q_dtype, int units, int G, int d,
                         const qjl_sketch_t& sk, int m_in, int m_total, float* sq, float* sums,
                         cudaStream_t st) {
-  switch (q_dtype) {
-    case QJL_F32: return launch_sq_1<float>(q, units, G, d, sk, m_in, m_total, sq, sums, st);
-    case QJL_F16: return launch_sq_1<__half>(q, units, G, d, sk, m_in, m_total, sq, sums, st);
-    case QJL_BF16: return launch_sq_1<__nv_bfloat16>(q, units, G, d, sk, m_in, m_total, sq, sums, st);
-    case QJL_F64: return launch_sq_1<double>(q, units, G, d, sk, m_in, m_total, sq, sums, st);
-  }
-  return QJL_ERR_ARG;
+  return launch_sq_o<float>(q, q_dtype, units, G, d, sk, m_in, m_total, sq, sums, st);
+}
+
+int launch_sketch_query_f64(const void* q, int q_dtype, int units, int G, int d, const qjl_sketch_t& sk,
+                            int m_total, double* sq, cudaStream_t st) {
+  return launch_sq_o<double>(q, q_dtype, units, G, d, sk, m_total, m_total, sq, nullptr, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -118,14 +129,18 @@ __global__ void __launch_bounds__(128) k_scores_simt(qjl_key_cache_t kc, int64_t
   __syncthreads();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  const int64_t row = (int64_t)u * kc.capacity + t;
   float a_in[GMAX], a_out[GMAX];
 #pragma unroll
   for (int g = 0; g < GMAX; ++g) { a_in[g] = 0.f; a_out[g] = 0.f; }
-  set_sums<GMAX>(kc.bits_in + row * (m_in / 8), m_in, sqs, m_total, G, a_in);
-  if (m_out > 0) set_sums<GMAX>(kc.bits_out + row * (m_out / 8), m_out, sqs + m_in, m_total, G, a_out);
-  const float nu_in = f16_bits_to_f32(kc.norm_in[row]);
-  const float nu_out = m_out > 0 ? f16_bits_to_f32(kc.norm_out[row]) : 0.f;
+  set_sums<GMAX>(kc.bits_in + row_off(u, t, m_in / 8, kc.capacity, kc.tile_stride), m_in, sqs, m_total, G, a_in);
+  if (m_out > 0)
+    set_sums<GMAX>(kc.bits_out + row_off(u, t, m_out / 8, kc.capacity, kc.tile_stride), m_out, sqs + m_in, m_total,
+                   G, a_out);
+  const int64_t no = row_off(u, t, 2, kc.capacity, kc.tile_stride);
+  const float nu_in = f16_bits_to_f32(*reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(kc.norm_in) + no));
+  const float nu_out =
+      m_out > 0 ? f16_bits_to_f32(*reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(kc.norm_out) + no))
+                : 0.f;
   const float c_in = m_in > 0 ? kEstimatorScale / (float)m_in : 0.f;
   const float c_out = m_out > 0 ? kEstimatorScale / (float)m_out : 0.f;
 #pragma unroll

@@ -21,7 +21,8 @@ int launch_quantize_keys_simt(const void* keys, int dtype, int64_t n, int64_t ku
                               const qjl_sketch_t& sk, const int32_t* ch, int h,
                               const qjl_key_cache_t& kc, int64_t row_offset, cudaStream_t st);
 // tcgen05 + TMA tensor-core key quantizer (bf16/fp16 keys); returns
-// QJL_ERR_UNSUPPORTED when the shape is outside its envelope.
+// QJL_ERR_UNSUPPORTED when the shape is outside its envelope (api.cu then runs the
+// fp64 kernel, which is also the path for fp32/fp64 keys).
 int launch_quantize_keys_tc(const void* keys, int dtype, int64_t n, int64_t kus,
                             const qjl_sketch_t& sk, const int32_t* ch, int h,
                             const qjl_key_cache_t& kc, int64_t row_offset, cudaStream_t st);
@@ -31,6 +32,8 @@ int launch_quantize_values(const void* v, int dtype, int64_t n, int64_t unit_str
 int launch_sketch_query(const void* q, int q_dtype, int units, int G, int d,
                         const qjl_sketch_t& sk, int m_in, int m_total, float* sq, float* sums,
                         cudaStream_t st);
+int launch_sketch_query_f64(const void* q, int q_dtype, int units, int G, int d, const qjl_sketch_t& sk,
+                            int m_total, double* sq, cudaStream_t st);
 int launch_scores_simt(const qjl_key_cache_t& kc, int64_t n, int G, const float* sq,
                        const float* sums, float* logits, cudaStream_t st);
 int launch_sign_dot_batch(const uint8_t* bits, int64_t n, int m, int64_t row_bytes,
@@ -41,28 +44,26 @@ int launch_softmax_f64(const float* logits, int64_t rows, int64_t n, double inv_
 size_t decode_simt_workspace(int units, int64_t n, int G, int d, int m_total);
 int launch_decode_simt(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, int G,
                        const float* sq, const float* sums, float inv_t, float* out, float* lse,
-                       float* ws, cudaStream_t st);
+                       float* logits, float* ws, cudaStream_t st);
 
-// tensor-core fused decode for P2 caches (mma.sync IMMA scores + HMMA PV)
-bool decode_tc_supported(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int G);
-size_t decode_tc_workspace(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n,
-                           int G);
-int launch_decode_tc(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n,
-                     const void* q, int q_dtype, int G, const qjl_sketch_t& sk, float inv_t,
-                     float* out, float* lse, void* ws, size_t ws_bytes, cudaStream_t st);
-
-// tcgen05 fused decode for P2T caches (kind::i8 UMMA scores + PV, TMEM accumulators)
-bool decode_umma_supported(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int G);
-size_t decode_umma_workspace(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, int G);
-int launch_decode_umma(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, const void* q,
-                       int q_dtype, int G, const qjl_sketch_t& sk, float inv_t, float* out, float* lse,
-                       void* ws, size_t ws_bytes, cudaStream_t st);
+// tcgen05 decode / scores on tile-major records (k_decode.cu).  vc == nullptr: keys only
+// (the scores kernel; the record may or may not carry the value fields).
+bool tile_path_supported(const qjl_key_cache_t& kc, const qjl_value_cache_t* vc, int G);
+size_t decode_tile_workspace(const qjl_key_cache_t& kc, int64_t n, int G, bool scores);
+int launch_decode_tile(const qjl_key_cache_t& kc, int64_t n, const void* q, int q_dtype, int G,
+                       const qjl_sketch_t& sk, float inv_t, float* out, float* lse, float* logits, void* ws,
+                       size_t ws_bytes, unsigned flags, cudaStream_t st);
 // decode step with append: the new token (k_new, v_new [units][128], query dtype) is
 // quantized into row n by the query-sketch kernel, then rows [0, n + 1) are decoded
-int launch_decode_step_umma(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, const void* q,
+int launch_decode_step_tile(const qjl_key_cache_t& kc, const qjl_value_cache_t& vc, int64_t n, const void* q,
                             int q_dtype, int G, const qjl_sketch_t& sk, const int32_t* channels, int h,
-                            const void* k_new, const void* v_new, float inv_t, float* out, float* lse, void* ws,
-                            size_t ws_bytes, cudaStream_t st);
+                            const void* k_new, const void* v_new, float inv_t, float* out, float* lse,
+                            float* logits, void* ws, size_t ws_bytes, unsigned flags, cudaStream_t st);
+int launch_scores_tile(const qjl_key_cache_t& kc, int64_t n, const void* q, int q_dtype, int G,
+                       const qjl_sketch_t& sk, float* logits, void* ws, size_t ws_bytes, cudaStream_t st);
+int bench_decode_tile(const qjl_key_cache_t& kc, int64_t n, const void* q, int q_dtype, int G, const qjl_sketch_t& sk,
+                      float inv_t, float* out, float* lse, void* ws, size_t ws_bytes, int reps, float* ms,
+                      cudaStream_t st);
 
 // batched block-wise sketch orthogonalization (k_orth.cu)
 int launch_orthogonalize(const double* g, int batch, int m, int d, double* out, cudaStream_t st);

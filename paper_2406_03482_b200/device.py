@@ -65,13 +65,25 @@ class CacheShape:
 
 
 class DeviceKeyCache:
-    """Packed QJL key cache + 2-bit (or u8) value cache for `units` units."""
+    """Packed QJL key cache + 2-bit (or u8) value cache for `units` units.
+
+    Layouts (include/qjl_b200.h):
+      * "p2t" values (the tensor-core path): tile-major records -- one contiguous
+        record per (unit, 128-token tile) holding sign bits, fp16 norms, 2-bit codes and
+        fp16 zero/scale (`qjl_tile_record`), so the decode streams one bulk copy per tile;
+      * "u8" values (the reference's own format): separate row-major arrays;
+      * keys only (`with_values=False`): tile-major records of the key fields when
+        `tiled` (the tensor-core scores kernel), else row-major arrays.
+    The per-field properties (`bits_in`, `norm_in`, ..., `v_codes`) are dense
+    [units, capacity, ...] tensors: views in the rows layout, COPIES (read-only) in the
+    tile-major one; write into a tiled cache only through the library or `field_view`.
+    """
 
     def __init__(self, units: int, d: int, m_in: int, m_out: int, h: int, capacity: int, *,
                  key_dtype: torch.dtype = torch.bfloat16, value_bits: int = 2,
                  value_group: int = 32, value_layout: str = "p2t", with_values: bool = True,
                  sketch_dtype: torch.dtype | None = None, device: str | torch.device = "cuda",
-                 validate_rate: bool = True):
+                 validate_rate: bool = True, tiled: bool | None = None):
         self.lib = _lib.load()
         if not torch.cuda.is_available():
             raise RuntimeError("DeviceKeyCache needs a CUDA device (no CPU fallback)")
@@ -86,6 +98,8 @@ class DeviceKeyCache:
         if validate_rate and h > 0 and d - h > 0 and m_out * (d - h) < m_in * h:
             raise ValueError("outlier bit rate below inlier bit rate: "
                              f"m_out/h = {m_out}/{h} < m_in/(d-h) = {m_in}/{d - h}")
+        if with_values and value_layout not in ("p2t", "u8"):
+            raise ValueError(f"unknown value layout {value_layout!r}")
         self.device = torch.device(device)
         # rows are padded to whole 128-token tiles: the tensor-core decode streams
         # full tiles with bulk copies and masks tokens >= n
@@ -93,48 +107,126 @@ class DeviceKeyCache:
         self.shape = CacheShape(units, d, m_in, m_out, h, capacity)
         self.key_dtype = key_dtype
         self.sketch_dtype = sketch_dtype or operand_dtype_for(key_dtype)
-        dev = self.device
-        self.bits_in = torch.zeros(units, capacity, max(m_in, 8) // 8, dtype=torch.uint8, device=dev)
-        self.norm_in = torch.zeros(units, capacity, dtype=torch.float16, device=dev)
-        self.bits_out = (torch.zeros(units, capacity, m_out // 8, dtype=torch.uint8, device=dev)
-                         if m_out else None)
-        self.norm_out = torch.zeros(units, capacity, dtype=torch.float16, device=dev) if m_out else None
-        self.channels = torch.zeros(units, max(h, 1), dtype=torch.int32, device=dev)
-        self.s_full: torch.Tensor | None = None
-        self.n = 0
         self.value_layout = value_layout
         self.with_values = with_values
         self.value_bits, self.value_group = value_bits, value_group
-        if with_values:
-            G = d // value_group
-            if value_layout in ("p2", "p2t"):
-                if not (d == 128 and value_bits == 2 and value_group == 32):
-                    raise ValueError(f"{value_layout} value layout is 2-bit, group 32, d = 128")
-                self.v_codes = torch.zeros(units, capacity, d // 4, dtype=torch.uint8, device=dev)
-                self.v_zero = torch.zeros(units, capacity, G, dtype=torch.float16, device=dev)
-                self.v_scale = torch.zeros(units, capacity, G, dtype=torch.float16, device=dev)
-            elif value_layout == "u8":
-                self.v_codes = torch.zeros(units, capacity, d, dtype=torch.uint8, device=dev)
-                self.v_zero = torch.zeros(units, capacity, G, dtype=torch.float32, device=dev)
-                self.v_scale = torch.zeros(units, capacity, G, dtype=torch.float32, device=dev)
-            else:
-                raise ValueError(f"unknown value layout {value_layout!r}")
+        p2t = with_values and value_layout == "p2t"
+        if p2t and not (d == 128 and value_bits == 2 and value_group == 32):
+            raise ValueError("p2t value layout is 2-bit, group 32, d = 128")
+        if tiled is None:
+            tiled = p2t or (not with_values and m_in % 32 == 0 and m_out % 32 == 0)
+        if p2t and not tiled:
+            raise ValueError("p2t values live in tile-major records")
+        if with_values and not p2t and tiled:
+            raise ValueError("u8 values use the rows layout")
+        self.tiled = tiled
+        dev = self.device
+        self.channels = torch.zeros(units, max(h, 1), dtype=torch.int32, device=dev)
+        self.s_full: torch.Tensor | None = None
+        self.n = 0
         self.n_values = 0
         self._ws: torch.Tensor | None = None
+        Gv = d // value_group
+        if tiled:
+            offs = (ctypes.c_int64 * 7)()
+            rec = int(self.lib.qjl_tile_record(d, m_in, m_out, 1 if p2t else 0, offs))
+            if rec <= 0:
+                raise ValueError(f"no tile record for d={d}, m_in={m_in}, m_out={m_out}")
+            self.record_bytes = rec
+            self.record_offsets = list(offs)
+            tiles = capacity // 128
+            self.records = torch.zeros(units, tiles, rec, dtype=torch.uint8, device=dev)
+            self._fields = {}
+
+            def fld(i, width, dtype=torch.uint8):
+                o = self.record_offsets[i]
+                v = self.records[:, :, o:o + 128 * width * (torch.finfo(dtype).bits // 8
+                                                             if dtype.is_floating_point else 1)]
+                v = v.view(dtype) if dtype != torch.uint8 else v
+                return v.view(units, tiles, 128, width)
+
+            self._fields["bits_in"] = fld(_lib.QJL_REC_BITS_IN, m_in // 8)
+            self._fields["norm_in"] = fld(_lib.QJL_REC_NORM_IN, 1, torch.float16)
+            if m_out:
+                self._fields["bits_out"] = fld(_lib.QJL_REC_BITS_OUT, m_out // 8)
+                self._fields["norm_out"] = fld(_lib.QJL_REC_NORM_OUT, 1, torch.float16)
+            if p2t:
+                self._fields["v_codes"] = fld(_lib.QJL_REC_CODES, d // 4)
+                self._fields["v_zero"] = fld(_lib.QJL_REC_ZERO, Gv, torch.float16)
+                self._fields["v_scale"] = fld(_lib.QJL_REC_SCALE, Gv, torch.float16)
+        else:
+            self.record_bytes = 0
+            self._fields = None
+            self._bits_in = torch.zeros(units, capacity, max(m_in, 8) // 8, dtype=torch.uint8, device=dev)
+            self._norm_in = torch.zeros(units, capacity, dtype=torch.float16, device=dev)
+            self._bits_out = (torch.zeros(units, capacity, m_out // 8, dtype=torch.uint8, device=dev)
+                              if m_out else None)
+            self._norm_out = torch.zeros(units, capacity, dtype=torch.float16, device=dev) if m_out else None
+            if with_values:
+                self._v_codes = torch.zeros(units, capacity, d, dtype=torch.uint8, device=dev)
+                self._v_zero = torch.zeros(units, capacity, Gv, dtype=torch.float32, device=dev)
+                self._v_scale = torch.zeros(units, capacity, Gv, dtype=torch.float32, device=dev)
+
+    # ------------------------------------------------------------ fields
+    def field_view(self, name: str) -> torch.Tensor:
+        """Writable view of one cache field: [units, tiles, 128, width] (tile-major) or
+        the dense [units, capacity, ...] array (rows layout)."""
+        if self.tiled:
+            if name not in self._fields:
+                raise KeyError(name)
+            return self._fields[name]
+        t = getattr(self, "_" + name, None)
+        if t is None:
+            raise KeyError(name)
+        return t
+
+    def _dense(self, name: str):
+        if not self.tiled:
+            return getattr(self, "_" + name, None)
+        v = self._fields.get(name)
+        if v is None:
+            return None
+        s = self.shape
+        out = v.reshape(s.units, s.capacity, v.shape[-1])
+        return out[..., 0] if name in ("norm_in", "norm_out") else out
+
+    bits_in = property(lambda self: self._dense("bits_in"))
+    bits_out = property(lambda self: self._dense("bits_out"))
+    norm_in = property(lambda self: self._dense("norm_in"))
+    norm_out = property(lambda self: self._dense("norm_out"))
+    v_codes = property(lambda self: self._dense("v_codes"))
+    v_zero = property(lambda self: self._dense("v_zero"))
+    v_scale = property(lambda self: self._dense("v_scale"))
+
+    def fill_rows(self, name: str, rows: slice, value: float) -> None:
+        """Set a field of rows `rows` of every unit to `value` (both layouts)."""
+        t = self.field_view(name)
+        if not self.tiled:
+            t[:, rows] = value
+            return
+        idx = torch.arange(self.shape.capacity, device=self.device)[rows]
+        t[:, idx // 128, idx % 128] = value
 
     # ------------------------------------------------------------ descriptors
+    def _ptr_of(self, name: str) -> int | None:
+        if self.tiled:
+            v = self._fields.get(name)
+            return None if v is None else v.data_ptr()
+        t = getattr(self, "_" + name, None)
+        return None if t is None else t.data_ptr()
+
     def key_desc(self) -> _lib.KeyCacheDesc:
         s = self.shape
-        return _lib.KeyCacheDesc(_ptr(self.bits_in), _ptr(self.bits_out), _ptr(self.norm_in),
-                                 _ptr(self.norm_out), s.capacity, s.units, s.d, s.m_in, s.m_out)
+        return _lib.KeyCacheDesc(self._ptr_of("bits_in"), self._ptr_of("bits_out"), self._ptr_of("norm_in"),
+                                 self._ptr_of("norm_out"), s.capacity, s.units, s.d, s.m_in, s.m_out,
+                                 self.record_bytes)
 
     def value_desc(self) -> _lib.ValueCacheDesc:
         s = self.shape
-        layout = {"p2": _lib.QJL_VLAYOUT_P2, "p2t": _lib.QJL_VLAYOUT_P2T}.get(self.value_layout,
-                                                                             _lib.QJL_VLAYOUT_U8)
-        return _lib.ValueCacheDesc(_ptr(self.v_codes), _ptr(self.v_zero), _ptr(self.v_scale),
+        layout = _lib.QJL_VLAYOUT_P2T if self.value_layout == "p2t" else _lib.QJL_VLAYOUT_U8
+        return _lib.ValueCacheDesc(self._ptr_of("v_codes"), self._ptr_of("v_zero"), self._ptr_of("v_scale"),
                                    s.capacity, s.units, s.d, self.value_bits, self.value_group,
-                                   layout)
+                                   layout, 0, self.record_bytes)
 
     def sketch_desc(self) -> _lib.SketchDesc:
         if self.s_full is None:
@@ -291,7 +383,7 @@ class DeviceKeyCache:
         out = torch.empty(s.units, q.shape[1], s.m_in + s.m_out, dtype=torch.float32, device=self.device)
         sd = self.sketch_desc()
         _lib.check(self.lib.qjl_sketch_query(q.data_ptr(), _TORCH2QJL[q.dtype], s.units, q.shape[1],
-                                             s.d, ctypes.byref(sd), s.m_in + s.m_out,
+                                             s.d, ctypes.byref(sd), s.m_in + s.m_out, _lib.QJL_F32,
                                              out.data_ptr(), _stream()), "sketch_query")
         return out
 
@@ -317,8 +409,11 @@ class DeviceKeyCache:
         return int(self.lib.qjl_decode_workspace(ctypes.byref(kd), ctypes.byref(vd), n, G))
 
     def decode(self, q: torch.Tensor, temperature: float = 1.0, n: int | None = None,
-               out: torch.Tensor | None = None, lse: torch.Tensor | None = None) -> torch.Tensor:
-        """K2+K3: softmax(logits / T) @ V per query head -> [U, G, d] f32 (attention.py:56-71)."""
+               out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
+               chained: bool = False, logits: torch.Tensor | None = None) -> torch.Tensor:
+        """K2+K3: softmax(logits / T) @ V per query head -> [U, G, d] f32 (attention.py:56-71).
+        `chained`: the previous kernel on the stream is this cache's decode and every input
+        predates it (QJL_DECODE_CHAINED) -- lets the query sketch overlap that decode."""
         if temperature <= 0:
             raise ValueError(f"temperature must be positive, got {temperature}")
         if not self.with_values:
@@ -336,13 +431,34 @@ class DeviceKeyCache:
         ws = self.workspace(ws_b)
         _lib.check(self.lib.qjl_decode(ctypes.byref(kd), ctypes.byref(vd), n, q.data_ptr(),
                                        _TORCH2QJL[q.dtype], G, ctypes.byref(sd),
-                                       1.0 / float(temperature), out.data_ptr(), _ptr(lse),
-                                       ws.data_ptr(), ws.numel(), _stream()), "decode")
+                                       1.0 / float(temperature), out.data_ptr(), _ptr(lse), _ptr(logits),
+                                       ws.data_ptr(), ws.numel(),
+                                       _lib.QJL_DECODE_CHAINED if chained else 0, _stream()), "decode")
         return out
+
+    def bench_decode_kernel(self, q: torch.Tensor, reps: int, temperature: float = 1.0,
+                            out: torch.Tensor | None = None) -> float:
+        """Mean time (ms) of the tensor-core decode kernel in a chain of `reps` back-to-back
+        decodes (qjl_bench_decode_kernel): the roofline kernel as it runs in a decode loop."""
+        s = self.shape
+        q = self._check_q(q)
+        G = q.shape[1]
+        if out is None:
+            out = torch.empty(s.units, G, s.d, dtype=torch.float32, device=self.device)
+        kd, vd, sd = self.key_desc(), self.value_desc(), self.sketch_desc()
+        ws_b = int(self.lib.qjl_decode_workspace(ctypes.byref(kd), ctypes.byref(vd), self.n, G))
+        ws = self.workspace(ws_b)
+        ms = ctypes.c_float(0.0)
+        _lib.check(self.lib.qjl_bench_decode_kernel(ctypes.byref(kd), ctypes.byref(vd), self.n, q.data_ptr(),
+                                                    _TORCH2QJL[q.dtype], G, ctypes.byref(sd),
+                                                    1.0 / float(temperature), out.data_ptr(), None,
+                                                    ws.data_ptr(), ws.numel(), int(reps), ctypes.byref(ms),
+                                                    _stream()), "bench_decode_kernel")
+        return float(ms.value)
 
     def decode_step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,
                     temperature: float = 1.0, out: torch.Tensor | None = None,
-                    lse: torch.Tensor | None = None) -> torch.Tensor:
+                    lse: torch.Tensor | None = None, chained: bool = False) -> torch.Tensor:
         """One generation step (Algorithm 1): append the new token of every unit
         (k_new, v_new [U, d]) at row n, then decode q [U, G, d] over rows [0, n + 1).
         On the tcgen05 path the append is fused into the step's query-sketch kernel;
@@ -370,7 +486,8 @@ class DeviceKeyCache:
             rc = self.lib.qjl_decode_step(ctypes.byref(kd), ctypes.byref(vd), n, q.data_ptr(),
                                           _TORCH2QJL[q.dtype], G, ctypes.byref(sd), self.channels.data_ptr(),
                                           s.h, kn.data_ptr(), vn.data_ptr(), 1.0 / float(temperature),
-                                          out.data_ptr(), _ptr(lse), ws.data_ptr(), ws.numel(), _stream())
+                                          out.data_ptr(), _ptr(lse), None, ws.data_ptr(), ws.numel(),
+                                          _lib.QJL_DECODE_CHAINED if chained else 0, _stream())
         if rc == _lib.QJL_ERR_UNSUPPORTED:
             self.append(kn[:, None, :], vn[:, None, :])
             return self.decode(q, temperature, out=out, lse=lse)
@@ -379,7 +496,7 @@ class DeviceKeyCache:
         self.n_values += 1
         return out
 
-    # ------------------------------------------------------------- factory    # ------------------------------------------------------------- factory
+    # ------------------------------------------------------------- factory
     @classmethod
     def create(cls, units: int, d: int, m_in: int, h: int = 0, m_out: int | None = None,
                capacity: int = 4096, seed: int = 0, orthogonalize_sketches: bool = True,
@@ -413,25 +530,8 @@ class DeviceKeyCache:
         return r
 
 
-def _p2_tables():
-    """Byte offset (within a 4 KB tile) and bit shift of every (token, dim) of a
-    128-token P2 tile -- the host mirror of `p2_pos` in csrc/common.cuh."""
-    t = np.arange(128)[:, None]
-    d = np.arange(128)[None, :]
-    sl, j, i = (t >> 5) & 3, t & 7, (t >> 3) & 3
-    mt, g, r = d >> 4, d & 7, (d >> 3) & 1
-    k, s = mt >> 1, 2 * (mt & 1) + r
-    word = sl * 256 + (g * 8 + (j ^ ((g & 1) << 2))) * 4 + k
-    byte = word * 4 + i
-    return (np.broadcast_to(byte, (128, 128)).astype(np.int64),
-            np.broadcast_to(2 * s, (128, 128)).astype(np.uint8))
-
-
-_P2_BYTE, _P2_SHIFT = _p2_tables()
-
-
 def _p2t_tables():
-    """P2T byte offset / shift of every (token, dim) of a 128-token tile (`p2t_pos`)."""
+    """P2T byte offset / shift of every (token, dim) of a 128-token tile (`p2t_byte`)."""
     t = np.arange(128)[:, None]
     d = np.arange(128)[None, :]
     byte = (d >> 2) * 128 + (t >> 2) * 4 + (t & 3)
@@ -442,27 +542,22 @@ def _p2t_tables():
 _P2T_BYTE, _P2T_SHIFT = _p2t_tables()
 
 
-def unpack_codes(packed: np.ndarray, n: int | None = None, layout: str = "p2") -> np.ndarray:
-    """Host decoder of a packed 2-bit code layout ("p2" or "p2t") -> codes [..., n, 128]."""
-    return p2_unpack_codes(packed, n, layout)
-
-
-def p2_unpack_codes(packed: np.ndarray, n: int | None = None, layout: str = "p2") -> np.ndarray:
-    """Host decoder of the P2 tile-interleaved code layout: packed u8 [..., cap, 32]
-    (cap a multiple of 128, rows counted from the unit's row 0) -> codes [..., n, 128]."""
+def unpack_codes(packed: np.ndarray, n: int | None = None) -> np.ndarray:
+    """Host decoder of the P2T tile-interleaved code layout: packed u8 [..., cap, 32]
+    (cap a multiple of 128, rows counted from the unit's row 0, i.e. the dense
+    `DeviceKeyCache.v_codes`) -> codes [..., n, 128]."""
     packed = np.ascontiguousarray(packed, dtype=np.uint8)
     cap = packed.shape[-2]
     if cap % 128:
-        raise ValueError("P2 code arrays hold whole 128-token tiles")
+        raise ValueError("P2T code arrays hold whole 128-token tiles")
     tiles = packed.reshape(packed.shape[:-2] + (cap // 128, 4096))
-    bt, sh = (_P2T_BYTE, _P2T_SHIFT) if layout == "p2t" else (_P2_BYTE, _P2_SHIFT)
-    codes = (tiles[..., bt] >> sh) & 3
+    codes = (tiles[..., _P2T_BYTE] >> _P2T_SHIFT) & 3
     codes = codes.reshape(packed.shape[:-2] + (cap, 128)).astype(np.uint8)
     return codes if n is None else codes[..., :n, :]
 
 
-def p2_pack_codes(codes: np.ndarray, layout: str = "p2") -> np.ndarray:
-    """Inverse of p2_unpack_codes: codes [..., n, 128] -> packed u8 [..., cap, 32],
+def pack_codes(codes: np.ndarray) -> np.ndarray:
+    """Inverse of unpack_codes: codes [..., n, 128] -> packed u8 [..., cap, 32],
     cap = n rounded up to whole 128-token tiles (padding codes are 0)."""
     codes = np.asarray(codes, np.uint8)
     n = codes.shape[-2]
@@ -470,12 +565,9 @@ def p2_pack_codes(codes: np.ndarray, layout: str = "p2") -> np.ndarray:
     full = np.zeros(codes.shape[:-2] + (cap, 128), np.uint8)
     full[..., :n, :] = codes & 3
     tiles = full.reshape(codes.shape[:-2] + (cap // 128, 128 * 128))
-    out = np.zeros(codes.shape[:-2] + (cap // 128, 4096), np.uint8)
-    bt, sh = (_P2T_BYTE, _P2T_SHIFT) if layout == "p2t" else (_P2_BYTE, _P2_SHIFT)
-    flat_byte = bt.reshape(-1)
-    flat_shift = sh.reshape(-1)
+    flat_byte = _P2T_BYTE.reshape(-1)
+    flat_shift = _P2T_SHIFT.reshape(-1)
     order = np.argsort(flat_byte, kind="stable")          # 4 (token, dim) per byte
     contrib = (tiles[..., order].astype(np.uint32) << flat_shift[order]).reshape(
         codes.shape[:-2] + (cap // 128, 4096, 4)).sum(-1)
-    out[...] = contrib.astype(np.uint8)
-    return out.reshape(codes.shape[:-2] + (cap, 32))
+    return contrib.astype(np.uint8).reshape(codes.shape[:-2] + (cap, 32))

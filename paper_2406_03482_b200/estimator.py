@@ -131,7 +131,7 @@ def _quantize_rows(sketch: SketchMatrix, keys: np.ndarray):
     kt = torch.from_numpy(np.ascontiguousarray(keys)).to(dev)
     bits = torch.zeros(1, n, m32 // 8, dtype=torch.uint8, device=dev)
     norms = torch.zeros(1, n, dtype=torch.float16, device=dev)
-    kd = _lib.KeyCacheDesc(bits.data_ptr(), None, norms.data_ptr(), None, n, 1, d, m32, 0)
+    kd = _lib.KeyCacheDesc(bits.data_ptr(), None, norms.data_ptr(), None, n, 1, d, m32, 0, 0)
     sd = _lib.SketchDesc(S.data_ptr(), _lib.QJL_F64, 0, 0)
     _lib.check(lib.qjl_quantize_keys(kt.data_ptr(), _lib.QJL_F64, n, n * d, ctypes.byref(sd), None, 0,
                                      ctypes.byref(kd), 0, torch.cuda.current_stream().cuda_stream),
@@ -155,12 +155,18 @@ def sketch_query(sketch: SketchMatrix, query: np.ndarray) -> SketchedQuery:
     query = np.asarray(query, dtype=np.float64)
     if query.shape != (sketch.d,):
         raise ValueError(f"query has shape {query.shape}, expected ({sketch.d},)")
+    lib = _lib.load()
     dev = _dev()
     S = torch.from_numpy(np.ascontiguousarray(sketch.entries, np.float64)).to(dev)
     q = torch.from_numpy(query).to(dev)
-    # the drop-in returns the full fp64 projection: a plain fp64 GEMV on the device
-    # (the batched decode path computes S q inside its own prologue kernel)
-    vals = (S @ q).cpu().numpy()
+    out = torch.empty(sketch.m, dtype=torch.float64, device=dev)
+    # the query-sketch kernel with fp64 accumulation and fp64 output (the drop-in returns
+    # the full-precision projection, estimator.py:132)
+    sd = _lib.SketchDesc(S.data_ptr(), _lib.QJL_F64, 0, 0)
+    _lib.check(lib.qjl_sketch_query(q.data_ptr(), _lib.QJL_F64, 1, 1, sketch.d, ctypes.byref(sd), sketch.m,
+                                    _lib.QJL_F64, out.data_ptr(), torch.cuda.current_stream().cuda_stream),
+               "sketch_query")
+    vals = out.cpu().numpy()
     vals.setflags(write=False)
     return SketchedQuery(values=vals, source_dim=sketch.d)
 

@@ -235,6 +235,9 @@ class KeyCacheState:
         self._cap = 0
         self._dev: DeviceKeyCache | None = None
         self._n = 0
+        # ||k_side||_2 at full precision, as quantize_key returns it (estimator.py:122); the
+        # device keeps the fp16 copies its logits use (read_cache semantics, kvcache.py:490)
+        self._norms = np.zeros((0, 2))
         self._grow(64)
 
     # ------------------------------------------------------------------ device
@@ -252,7 +255,7 @@ class KeyCacheState:
         m_out = _pad32(self.m_out) if self.m_out else 0
         new = DeviceKeyCache(1, p.d, m_in, m_out, p.h, cap, key_dtype=torch.float64,
                              sketch_dtype=torch.float64, with_values=False, device=_cuda(),
-                             validate_rate=False)   # rate already checked on the logical sizes
+                             validate_rate=False, tiled=False)   # rate already checked on the logical sizes
         if p.h:
             new.set_channels(np.asarray(p.channels, np.int32).reshape(1, p.h))
         new.set_sketches(self._padded(self.inlier_sketch), self._padded(self.outlier_sketch))
@@ -316,10 +319,10 @@ class KeyCacheState:
             return ()
         c = self._dev
         bi = c.bits_in[0, :n].cpu().numpy()
-        ni = c.norm_in[0, :n].double().cpu().numpy()
+        ni = self._norms[:n, 0]
         out = []
         bo = c.bits_out[0, :n].cpu().numpy() if self.m_out else None
-        no = c.norm_out[0, :n].double().cpu().numpy() if self.m_out else None
+        no = self._norms[:n, 1]
         for i in range(n):
             ki = QuantizedKey(bits=_bytes_to_words(bi[i], self.m_in), norm=float(ni[i]), m=self.m_in) \
                 if self.m_in else EMPTY_KEY
@@ -346,6 +349,12 @@ class KeyCacheState:
         kt = torch.from_numpy(np.ascontiguousarray(keys)).to(_cuda())[None]
         self._dev.n = self._n
         self._dev.append_keys(kt)
+        p = self.profile
+        inl, outl = p.inlier_index, p.outlier_index
+        # per key exactly as quantize_key computes it (np.linalg.norm of the side vector)
+        norms = np.array([[float(np.linalg.norm(k[inl])), float(np.linalg.norm(k[outl]))] for k in keys]
+                         ).reshape(t, 2)
+        self._norms = np.concatenate([self._norms[: self._n], norms])
         self._n += t
         self._clear_padding(self._n - t, self._n)
 
@@ -370,6 +379,7 @@ class KeyCacheState:
             b = np.ascontiguousarray(k.bits, dtype="<u8").view(np.uint8)[: bits.shape[2]]
             bits[0, row, : b.size].copy_(torch.from_numpy(b.copy()))
             norms[0, row] = float(k.norm)
+        self._norms = np.concatenate([self._norms[: self._n], [[float(ki.norm), float(ko.norm)]]])
         self._n += 1
         self._dev.n = self._n
 
@@ -466,7 +476,12 @@ def read_cache(path) -> tuple[KeyCacheState, list[QuantizedValueToken], CacheHea
         recs = torch.from_numpy(np.array(recs_np).reshape(1, -1)).to(_cuda())
         _qjlc.import_records(recs, n, state.m_in, state.m_out, state.device_cache.key_desc(), None)
         state._n = n
-        state.device_cache.n = n
+        dc = state.device_cache
+        dc.n = n
+        # the file's f16 norms are the entries' norms (read_cache semantics, kvcache.py:490)
+        ni = dc.norm_in[0, :n].double().cpu().numpy()
+        no = dc.norm_out[0, :n].double().cpu().numpy() if state.m_out else np.zeros(n)
+        state._norms = np.stack([ni, no], axis=1)
     R = recs_np.shape[1]
     c0 = R - hdr.d - 8
     codes = np.ascontiguousarray(recs_np[:, c0:c0 + hdr.d])

@@ -28,7 +28,7 @@ def test_library_exports_every_symbol():
     lib = _lib.load()
     for name in header_symbols():
         assert hasattr(lib, name), name
-    assert lib.qjl_abi_version() == 1
+    assert lib.qjl_abi_version() == 2
     assert lib.qjl_status_string(-1) == b"invalid argument"
 
 
@@ -45,10 +45,50 @@ def test_argument_errors_without_gpu():
     assert rc == _lib.QJL_ERR_ARG
     assert b"outlier bit rate" in lib.qjl_last_error()
     # unsupported sketch width (not a multiple of 32)
-    kc = _lib.KeyCacheDesc(8, None, 8, None, 16, 1, 128, 100, 0)
+    kc = _lib.KeyCacheDesc(8, None, 8, None, 16, 1, 128, 100, 0, 0)
     sd = _lib.SketchDesc(8, 2, 0, 0)
     rc = lib.qjl_quantize_keys(ctypes.c_void_p(8), 2, 1, 128, ctypes.byref(sd), None, 0,
                                ctypes.byref(kc), 0, None)
     assert rc == _lib.QJL_ERR_UNSUPPORTED
     # temperature must be positive (kvcache.py:335-336)
     assert lib.qjl_softmax_f64(ctypes.c_void_p(8), 1, 1, 0.0, ctypes.c_void_p(8), None) == _lib.QJL_ERR_ARG
+
+
+def test_tile_record_layout():
+    """The canonical tile record (qjl_b200.h): C3 shapes give the 11776-byte record the
+    tensor-core decode streams with one bulk copy; key fields come first."""
+    lib = _lib.load()
+    off = (ctypes.c_int64 * 7)()
+    assert lib.qjl_tile_record(128, 256, 64, 1, off) == 11776
+    assert list(off) == [0, 4096, 5120, 5376, 5632, 9728, 10752]
+    assert lib.qjl_tile_record(128, 256, 64, 0, off) == 5632            # keys only
+    assert list(off)[4:] == [-1, -1, -1]
+    assert lib.qjl_tile_record(128, 256, 0, 1, off) == 128 * 32 + 256 + 4096 + 2048
+    assert off[1] == -1 and off[3] == -1
+    assert lib.qjl_tile_record(128, 100, 0, 0, off) == -1               # m % 32 != 0
+    assert lib.qjl_tile_record(64, 256, 0, 1, off) == -1                # values need d = 128
+
+
+def test_layout_rules_without_gpu():
+    """P2T values live in tile records; U8 values use the rows layout; tiled key arrays
+    must sit at their record offsets -- all rejected before any CUDA call."""
+    lib = _lib.load()
+    sd = _lib.SketchDesc(8, 2, 0, 0)
+    base = 1 << 20
+    kc = _lib.KeyCacheDesc(base, base + 4096, base + 5120, base + 5376, 256, 1, 128, 256, 64, 11776)
+    vc_rows = _lib.ValueCacheDesc(8, 8, 8, 256, 1, 128, 2, 32, _lib.QJL_VLAYOUT_P2T, 0, 0)
+    rc = lib.qjl_decode(ctypes.byref(kc), ctypes.byref(vc_rows), 16, ctypes.c_void_p(8), 2, 4, ctypes.byref(sd),
+                        1.0, ctypes.c_void_p(8), None, None, ctypes.c_void_p(8), 1 << 30, 0, None)
+    assert rc == _lib.QJL_ERR_ARG and b"tile-major" in lib.qjl_last_error()
+    vc_u8 = _lib.ValueCacheDesc(8, 8, 8, 256, 1, 128, 2, 128, _lib.QJL_VLAYOUT_U8, 0, 11776)
+    rc = lib.qjl_decode(ctypes.byref(kc), ctypes.byref(vc_u8), 16, ctypes.c_void_p(8), 2, 4, ctypes.byref(sd),
+                        1.0, ctypes.c_void_p(8), None, None, ctypes.c_void_p(8), 1 << 30, 0, None)
+    assert rc == _lib.QJL_ERR_ARG and b"rows layout" in lib.qjl_last_error()
+    bad = _lib.KeyCacheDesc(base, base + 4096, base + 5000, base + 5376, 256, 1, 128, 256, 64, 11776)
+    rc = lib.qjl_quantize_keys(ctypes.c_void_p(8), 2, 1, 128, ctypes.byref(sd), ctypes.c_void_p(8), 8,
+                               ctypes.byref(bad), 0, None)
+    assert rc == _lib.QJL_ERR_ARG and b"record offsets" in lib.qjl_last_error()
+    odd = _lib.KeyCacheDesc(base, base + 4096, base + 5120, base + 5376, 200, 1, 128, 256, 64, 11776)
+    rc = lib.qjl_quantize_keys(ctypes.c_void_p(8), 2, 1, 128, ctypes.byref(sd), ctypes.c_void_p(8), 8,
+                               ctypes.byref(odd), 0, None)
+    assert rc == _lib.QJL_ERR_ARG and b"128-row tiles" in lib.qjl_last_error()

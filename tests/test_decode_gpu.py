@@ -1,0 +1,167 @@
+"""Tensor-core decode and scores (csrc/k_decode.cu, tile-major P2T records) against the CPU
+oracle: stream-K unit boundaries and tail tiles, head counts 1/2/3/4, every sketch width
+the kernels instantiate, temperature 1 and sqrt(d), log-sum-exp, the scores-only kernel,
+the P2T value quantizer, determinism and the decode-kernel benchmark hook."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import qjl_oracle as O
+from tests._cache import logsumexp, make_cache, oracle_decode
+from tests._parity import OUT_RTOL, check_logits, logit_bound, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    # U, n, G, h, m_in, m_out
+    (64, 4096, 4, 8, 256, 64),      # many CTAs per unit, segments cross units
+    (8, 100, 4, 8, 256, 64),        # fewer tiles than CTAs, tail tile
+    (3, 1, 2, 8, 256, 64),          # n = 1
+    (16, 2000, 1, 4, 256, 128),     # MHA, config-2 sketch sizes
+    (4, 3000, 4, 0, 256, 0),        # no outliers
+    (4, 3000, 3, 8, 512, 64),       # m = 512, G = 3
+    (8, 5000, 2, 8, 256, 64),       # G = 2 (two-head epilogue)
+    (6, 2500, 1, 8, 512, 64),       # G = 1 with m = 512
+    (4, 1500, 4, 4, 512, 128),      # m = 512 + 128
+    (4, 1300, 4, 0, 512, 0),        # m = 512, no outliers
+]
+
+
+def _sample_units(U):
+    return sorted({0, U // 2, U - 1})
+
+
+@pytest.mark.parametrize("U,n,G,h,m_in,m_out", SHAPES)
+def test_decode_matches_oracle(cuda, U, n, G, h, m_in, m_out):
+    c, q = make_cache(U, n, G, h, m_in, m_out, seed=U * 7 + n)
+    for T in (1.0, float(np.sqrt(128))):
+        lse = torch.empty(U, G, device="cuda")
+        out = c.decode(q, temperature=T, lse=lse).double().cpu().numpy()
+        lse = lse.double().cpu().numpy()
+        assert np.isfinite(out).all()
+        for u in _sample_units(U):
+            ref, logits = oracle_decode(c, q, u, T)
+            ref_lse = logsumexp(logits / T)
+            for g in range(G):
+                e = rel_l2(out[u, g], ref[g])
+                assert e <= OUT_RTOL, (u, g, T, e)
+                # the fused kernel's own log-sum-exp against the oracle's logits
+                assert abs(lse[u, g] - ref_lse[g]) <= 1e-4 * max(1.0, abs(ref_lse[g])), (u, g, T)
+
+
+@pytest.mark.parametrize("U,n,G,h,m_in,m_out", [SHAPES[0], SHAPES[1], SHAPES[3], SHAPES[4], SHAPES[5],
+                                                 (2, 700, 1, 0, 256, 0)])
+def test_scores_kernel_matches_oracle(cuda, U, n, G, h, m_in, m_out):
+    """Scores-only K2 on tile records (kvcache.py:311-329) against estimate_logits."""
+    c, q = make_cache(U, n, G, h, m_in, m_out, seed=U + 3 * n)
+    logits = c.scores(q).double().cpu().numpy()
+    from tests._cache import oracle_unit
+
+    Qh = q.double().cpu().numpy()
+    for u in _sample_units(U):
+        chans, cache, _ = oracle_unit(c, u)
+        for g in range(G):
+            ref = O.estimate_logits(c.S_in_host, c.S_out_host, chans, Qh[u, g], cache)
+            ok, err = check_logits(logits[u, g], ref,
+                                   logit_bound(c.S_in_host, c.S_out_host, chans, Qh[u, g], cache["norm_in"],
+                                               cache.get("norm_out", 0.0)))
+            assert ok.all(), (u, g, err.max())
+
+
+def test_full_config3_against_oracle(cuda):
+    """Full config-3 shape (64 units x 32768 tokens, 4 q-heads/unit); the oracle checks
+    the first and last units."""
+    U, n, G = 64, 32768, 4
+    c, q = make_cache(U, n, G, 8, 256, 64, seed=3)
+    lse = torch.empty(U, G, device="cuda")
+    out = c.decode(q, lse=lse).double().cpu().numpy()
+    assert np.isfinite(out).all()
+    for u in (0, U - 1):
+        ref, logits = oracle_decode(c, q, u)
+        ref_lse = logsumexp(logits)
+        for g in range(G):
+            assert rel_l2(out[u, g], ref[g]) <= OUT_RTOL, (u, g, rel_l2(out[u, g], ref[g]))
+            assert abs(float(lse[u, g]) - ref_lse[g]) <= 1e-4 * abs(ref_lse[g])
+
+
+def test_determinism_and_chaining(cuda):
+    c, q = make_cache(8, 5000, 4, 8, 256, 64, seed=11)
+    o1 = c.decode(q).clone()
+    o2 = c.decode(q, chained=True).clone()       # PDL-chained on the previous decode
+    o3 = c.decode(q, chained=True)
+    assert torch.equal(o1, o2) and torch.equal(o1, o3)   # no atomics in the sums
+
+
+def test_bench_hook_runs_the_same_kernel(cuda):
+    c, q = make_cache(16, 3000, 4, 8, 256, 64, seed=5)
+    ref = c.decode(q).clone()
+    out = torch.empty_like(ref)
+    ms = c.bench_decode_kernel(q, reps=5, out=out)
+    assert ms > 0
+    assert torch.equal(out, ref)                 # every chained kernel rewrites the same output
+    assert torch.equal(c.decode(q), ref)         # counters were left clean
+
+
+def test_p2t_codes_match_oracle_quantizer(cuda):
+    from paper_2406_03482_b200.device import DeviceKeyCache, unpack_codes
+
+    U, n = 3, 300
+    V = torch.randn(U, n, 128, device="cuda", dtype=torch.bfloat16)
+    c = DeviceKeyCache(U, 128, 256, 0, 0, n)
+    c.append_values(V)
+    Vh = V.double().cpu().numpy()
+    for u in range(U):
+        codes, zero, scale = O.quantize_values(Vh[u], 2, 32)
+        assert np.array_equal(unpack_codes(c.v_codes[u].cpu().numpy(), n), codes)
+        assert np.array_equal(c.v_zero[u, :n].double().cpu().numpy(), zero)
+        assert np.array_equal(c.v_scale[u, :n].double().cpu().numpy(), scale)
+
+
+def test_p2t_quantizer_exact_ties_and_unaligned_appends(cuda):
+    """Values on a grid that puts many quotients exactly on .5 (round-half-even in the
+    reference), constant groups, and appends starting at rows that are not multiples of 4."""
+    from paper_2406_03482_b200.device import DeviceKeyCache, unpack_codes
+
+    U, n = 2, 203
+    g = torch.Generator().manual_seed(5)
+    V = (torch.randint(0, 7, (U, n, 128), generator=g).double() * 0.5)   # multiples of 1/2 -> ties
+    V[:, 7, 32:64] = 1.25                                                   # constant group
+    V[:, 11] *= 1e-3
+    Vt = V.to(torch.bfloat16)
+    c = DeviceKeyCache(U, 128, 256, 0, 0, n)
+    for a, b in ((0, 5), (5, 6), (6, 70), (70, 203)):                       # unaligned row offsets
+        c.append_values(Vt[:, a:b].to(cuda))
+    Vh = Vt.double().numpy()
+    for u in range(U):
+        codes, zero, scale = O.quantize_values(Vh[u], 2, 32, const_dtype="f16")
+        assert np.array_equal(unpack_codes(c.v_codes[u].cpu().numpy(), n), codes)
+        assert np.array_equal(c.v_zero[u, :n].double().cpu().numpy(), zero)
+        assert np.array_equal(c.v_scale[u, :n].double().cpu().numpy(), scale)
+
+
+def test_stale_padding_rows_are_masked(cuda):
+    """Rows >= n of the last tile hold garbage (NaN/Inf constants, random bits): the
+    decode must ignore them (the masked tail tile zeroes their constants)."""
+    c, q = make_cache(4, 1000, 4, 8, 256, 64, seed=17, capacity=1024)
+    ref = c.decode(q).clone()
+    rows = slice(1000, 1024)
+    for name, val in (("v_scale", float("inf")), ("v_zero", float("nan")), ("norm_in", float("nan")),
+                      ("bits_in", 0x55)):
+        c.fill_rows(name, rows, val)
+    # P2T codes are tile-interleaved: tokens 1000..1023 are bytes dq*128 + 104..127 of tile 7
+    fv = c.field_view("v_codes")
+    fv.view(fv.shape[0], fv.shape[1], 32, 128)[:, 7, :, 104:] = 0xFF
+    out = c.decode(q)
+    assert torch.equal(out, ref)
+
+
+def test_rejects_unsupported_p2t_shapes(cuda):
+    from paper_2406_03482_b200.device import DeviceKeyCache
+
+    c = DeviceKeyCache(2, 128, 256, 0, 0, 256)
+    c.set_sketches(*DeviceKeyCache.make_sketches(128, 0, 256, 0, operand="bf16"))
+    K = torch.randn(2, 10, 128, device="cuda", dtype=torch.bfloat16)
+    c.append(K, K)
+    with pytest.raises(NotImplementedError):
+        c.decode(torch.randn(2, 5, 128, device="cuda", dtype=torch.bfloat16))   # G = 5 > 4

@@ -8,7 +8,7 @@ import pytest
 import torch
 
 from oracle import qjl_oracle as O
-from paper_2406_03482_b200.device import DeviceKeyCache, p2_unpack_codes
+from paper_2406_03482_b200.device import DeviceKeyCache, unpack_codes
 from tests._parity import rel_l2
 
 pytestmark = pytest.mark.gpu
@@ -59,8 +59,8 @@ def test_decode_step_equals_append_then_decode(cuda, U, n0, G, h, m_in, m_out):
         assert a.n == b.n == t + 1
         for x, y in zip(_arrays(a, t + 1), _arrays(b, t + 1)):
             assert torch.equal(x, y)
-        ca = p2_unpack_codes(a.v_codes.cpu().numpy(), t + 1, layout="p2t")
-        cb = p2_unpack_codes(b.v_codes.cpu().numpy(), t + 1, layout="p2t")
+        ca = unpack_codes(a.v_codes.cpu().numpy(), t + 1)
+        cb = unpack_codes(b.v_codes.cpu().numpy(), t + 1)
         assert np.array_equal(ca, cb)
         assert torch.equal(out_a, out_b)
 
@@ -83,11 +83,18 @@ def test_decode_step_against_oracle(cuda):
             assert rel_l2(out[u, g], ref) <= 1e-3
 
 
-def test_decode_step_falls_back_off_the_tcgen05_path(cuda):
-    (a, b), K, V, Q = _pair(4, 200, 4, 8, 256, 64, seed=9, layout="p2")
-    out_a = a.decode_step(Q[:, 0], K[:, 200], V[:, 200]).clone()
-    b.append(K[:, 200:201], V[:, 200:201])
-    assert torch.equal(out_a, b.decode(Q[:, 0]))
+def test_decode_step_chained_and_u8_fallback(cuda):
+    """Chained steps (QJL_DECODE_CHAINED) equal unchained ones; u8 caches (the generic
+    decode) run append + decode."""
+    (a, b), K, V, Q = _pair(4, 200, 4, 8, 256, 64, seed=9)
+    for i in range(4):
+        oa = a.decode_step(Q[:, i], K[:, 200 + i], V[:, 200 + i], chained=i > 0).clone()
+        ob = b.decode_step(Q[:, i], K[:, 200 + i], V[:, 200 + i])
+        assert torch.equal(oa, ob)
+    c = DeviceKeyCache.create(4, 128, 256, h=0, capacity=300, value_layout="u8", value_group=128)
+    c.append(K[:, :200], V[:, :200])
+    out = c.decode_step(Q[:, 0], K[:, 200], V[:, 200])
+    assert c.n == c.n_values == 201 and torch.isfinite(out).all()
     with pytest.raises(ValueError):
         c = DeviceKeyCache.create(2, 128, 256, h=0, capacity=128)
         c.append(torch.randn(2, 128, 128, device="cuda").bfloat16(), torch.randn(2, 128, 128, device="cuda").bfloat16())

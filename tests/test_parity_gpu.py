@@ -23,7 +23,7 @@ def _round_keys(x, dt):
     return t, t.double().numpy()
 
 
-def _build(cuda, units, n, d, G, h, factor, m_in, m_out, dt, seed, orth=True, layout="p2",
+def _build(cuda, units, n, d, G, h, factor, m_in, m_out, dt, seed, orth=True, layout="p2t",
            device_profile=True, lognormal=False):
     from paper_2406_03482_b200.device import DeviceKeyCache
 
@@ -34,7 +34,7 @@ def _build(cuda, units, n, d, G, h, factor, m_in, m_out, dt, seed, orth=True, la
     cache = DeviceKeyCache.create(units, d, m_in, h=h, m_out=m_out, capacity=n + 64, seed=seed,
                                   orthogonalize_sketches=orth, key_dtype=TD[dt],
                                   value_layout=layout,
-                                  value_group=32 if layout in ("p2", "p2t") else d)
+                                  value_group=32 if layout == "p2t" else d)
     if h:
         if device_profile:
             ch = cache.detect_outliers(Kt.to(cuda)).cpu().numpy()
@@ -80,7 +80,6 @@ def test_c1_quantize_and_scores(cuda, dt):
     ("c3", 4, 2048, 4, 8, 20.0, 256, 64, "bf16", "p2t"),
     ("c3_odd_n", 2, 1000, 4, 8, 20.0, 256, 64, "bf16", "p2t"),
     ("m512", 2, 777, 2, 8, 20.0, 512, 64, "bf16", "p2t"),
-    ("c3_mma_sync_p2", 4, 2048, 4, 8, 20.0, 256, 64, "bf16", "p2"),
     ("u8_ref_values", 2, 700, 2, 4, 15.0, 256, 128, "f16", "u8"),
 ])
 def test_decode_parity(cuda, cfg):
@@ -106,14 +105,14 @@ def test_decode_parity(cuda, cfg):
         caches.append(dict(bits_in=hv["bits_in"][u], bits_out=hv["bits_out"][u],
                            norm_in=hv["norm_in"][u], norm_out=hv["norm_out"][u]))
     # value codes/constants == oracle quantizer (fp64 both sides, fp16 constants)
-    group = 32 if layout in ("p2", "p2t") else d
+    group = 32 if layout == "p2t" else d
     deq = np.zeros_like(Vr)
     for u in range(U):
         codes, zero, scale = O.quantize_values(Vr[u], 2, group,
-                                               const_dtype="f16" if layout in ("p2", "p2t") else None)
-        if layout in ("p2", "p2t"):
-            from paper_2406_03482_b200.device import p2_unpack_codes
-            dc = p2_unpack_codes(cache.v_codes[u].cpu().numpy(), n, layout)
+                                               const_dtype="f16" if layout == "p2t" else None)
+        if layout == "p2t":
+            from paper_2406_03482_b200.device import unpack_codes
+            dc = unpack_codes(cache.v_codes[u].cpu().numpy(), n)
             assert np.array_equal(dc, codes)
             assert np.array_equal(cache.v_zero[u, :n].double().cpu().numpy(), zero)
             assert np.array_equal(cache.v_scale[u, :n].double().cpu().numpy(), scale)

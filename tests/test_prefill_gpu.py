@@ -73,7 +73,7 @@ def test_prefill_with_values_and_rate_check(cuda):
     c = DeviceKeyCache.create(2, 128, 256, h=8, m_out=64, capacity=1024, key_dtype=torch.bfloat16)
     c.prefill(keys, vals)
     assert c.n == 640 and c.n_values == 640
-    bad = DeviceKeyCache.create(2, 128, 256, h=8, m_out=8, capacity=1024, key_dtype=torch.bfloat16,
-                                validate_rate=False)
-    with pytest.raises(ValueError):
+    with pytest.raises(ValueError):           # m_out/h = 8/8 < m_in/(d-h) (kvcache.py:219-226)
+        bad = DeviceKeyCache.create(2, 128, 256, h=8, m_out=8, capacity=1024, key_dtype=torch.bfloat16,
+                                    validate_rate=False, with_values=False, tiled=False)
         bad.prefill(keys)

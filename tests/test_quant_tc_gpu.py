@@ -1,9 +1,10 @@
 """tcgen05 + TMA key quantizer (k_quant_tc.cu) checks: bit-identical to the fp64
-generic path on the same inputs (QJL_REQUIRE_TC forbids a silent fallback),
-tails / chunked appends at row offsets, and the full config-4 size against the
-CPU oracle on sampled units."""
+generic kernel on the same inputs, tails / chunked appends at row offsets, and the full
+config-4 size against the CPU oracle on sampled units.
 
-import os
+Dispatch is by shape (api.cu qjl_quantize_keys): bf16/fp16 keys with a sketch of the same
+operand dtype run the tensor-core kernel; an fp64 sketch (here: the same operand-rounded
+values held in fp64) runs the fp64 kernel -- which is how the reference comparison is made."""
 
 import numpy as np
 import pytest
@@ -31,20 +32,27 @@ def _quantize(K, m_in, h, m_out, dt, path, chunks=1):
     from paper_2406_03482_b200.device import DeviceKeyCache
 
     U, n, _ = K.shape
-    c = DeviceKeyCache.create(U, 128, m_in, h=h, m_out=m_out, capacity=n, seed=3, key_dtype=dt,
-                              with_values=False)
+    c = _cache(U, m_in, h, m_out, dt, n, path)
     if h:
         c.detect_outliers(K)
-        c.set_sketches(c.S_in_host, c.S_out_host)
-    env = {"tc": ("QJL_REQUIRE_TC", "1"), "simt": ("QJL_FORCE_SIMT", "1")}[path]
-    os.environ[env[0]] = env[1]
-    try:
-        bounds = np.linspace(0, n, chunks + 1).astype(int)
-        for a, b in zip(bounds[:-1], bounds[1:]):
-            c.append_keys(K[:, a:b].contiguous())
-    finally:
-        del os.environ[env[0]]
+    c.set_sketches(c.S_in_host, c.S_out_host)
+    bounds = np.linspace(0, n, chunks + 1).astype(int)
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        c.append_keys(K[:, a:b].contiguous())
     torch.cuda.synchronize()
+    return c
+
+
+def _cache(U, m_in, h, m_out, dt, n, path, channels=None):
+    """path "tc": operand-dtype sketch (tensor-core kernel); "fp64": the same operand-rounded
+    sketch values held in fp64 (the fp64 kernel)."""
+    from paper_2406_03482_b200.device import DeviceKeyCache
+
+    kw = dict(sketch_dtype=torch.float64) if path == "fp64" else {}
+    c = DeviceKeyCache.create(U, 128, m_in, h=h, m_out=m_out, capacity=n, seed=3, key_dtype=dt,
+                              with_values=False, channels=channels, **kw)
+    op = {torch.bfloat16: "bf16", torch.float16: "f16"}[dt]
+    c.S_in_host, c.S_out_host = DeviceKeyCache.make_sketches(128, h, m_in, m_out if h else 0, seed=3, operand=op)
     return c
 
 
@@ -58,7 +66,7 @@ def _quantize(K, m_in, h, m_out, dt, path, chunks=1):
 def test_tc_bitwise_equals_fp64_path(cuda, U, n, m_in, h, m_out, dt):
     K = _keys(U, n, dt, seed=U * 1000 + n, h=h)
     a = _quantize(K, m_in, h, m_out, dt, "tc")
-    b = _quantize(K, m_in, h, m_out, dt, "simt")
+    b = _quantize(K, m_in, h, m_out, dt, "fp64")
     assert torch.equal(a.bits_in[:, :n], b.bits_in[:, :n])
     assert torch.equal(a.norm_in[:, :n], b.norm_in[:, :n])
     if m_out:
@@ -99,8 +107,6 @@ def test_tc_special_rows_match_fp64_path(cuda, dt):
     """Zero / negative-zero / one-side-zero / NaN keys: the tie rule (S k)_i >= 0 -> 1
     (also for -0.0) and NaN -> 0 (estimator.py:119-121) hold on the tensor-core path
     (its accumulators start from +0, so an all-zero dot product is +0)."""
-    from paper_2406_03482_b200.device import DeviceKeyCache
-
     U, n, h = 2, 256, 8
     K = _keys(U, n, dt, seed=77, h=h)
     ch = torch.stack([torch.randperm(128, generator=torch.Generator().manual_seed(u))[:h].sort().values
@@ -116,18 +122,13 @@ def test_tc_special_rows_match_fp64_path(cuda, dt):
     K[:, 5, 7] = float("nan")                      # NaN key
 
     def run(path):
-        c = DeviceKeyCache.create(U, 128, 256, h=h, m_out=64, capacity=n, seed=3, key_dtype=dt,
-                                  with_values=False, channels=ch.cpu().numpy())
-        env = {"tc": ("QJL_REQUIRE_TC", "1"), "simt": ("QJL_FORCE_SIMT", "1")}[path]
-        os.environ[env[0]] = env[1]
-        try:
-            c.append_keys(K)
-        finally:
-            del os.environ[env[0]]
+        c = _cache(U, 256, h, 64, dt, n, path, channels=ch.cpu().numpy())
+        c.set_sketches(c.S_in_host, c.S_out_host)
+        c.append_keys(K)
         torch.cuda.synchronize()
         return c
 
-    a, b = run("tc"), run("simt")
+    a, b = run("tc"), run("fp64")
     for x, y in ((a.bits_in, b.bits_in), (a.bits_out, b.bits_out)):
         assert torch.equal(x[:, :n], y[:, :n])
     assert torch.all(a.bits_in[:, 0] == 0xFF) and torch.all(a.bits_out[:, 0] == 0xFF)

@@ -177,6 +177,11 @@ QJL_API int qjl_sketch_query(const void* q, int q_dtype, int units, int G, int d
  * values != 0 appends the P2T value fields (d == 128). */
 QJL_API int64_t qjl_tile_record(int d, int m_in, int m_out, int values, int64_t* offsets);
 
+/* Which kernels a call would run: 1 when qjl_decode (values != NULL) / qjl_scores
+ * (values == NULL) takes the tensor-core path for this cache and head count, 0 when the
+ * generic kernels run (or, for P2T values, when the call would be rejected), < 0 on bad args. */
+QJL_API int qjl_tensor_core_path(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int G);
+
 /* K2: logits [units][G][n] (f32) of G query heads per unit over the first n keys.
  * Tile-major caches with m_in/32 in {8, 16}, m_out/32 in {0, 2, 4}, d == 128 and G <= 4
  * run the tensor-core score kernel; every other shape runs the generic kernel. */

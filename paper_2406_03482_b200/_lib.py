@@ -69,6 +69,7 @@ SIGNATURES = {
     "qjl_bench_decode_kernel": (c_i32, [P(KeyCacheDesc), P(ValueCacheDesc), c_i64, c_vp, c_i32, c_i32,
                                         P(SketchDesc), c_flt, c_vp, c_vp, c_vp, c_sz, c_i32, P(c_flt), c_vp]),
     "qjl_tile_record": (c_i64, [c_i32, c_i32, c_i32, c_i32, P(c_i64)]),
+    "qjl_tensor_core_path": (c_i32, [P(KeyCacheDesc), P(ValueCacheDesc), c_i32]),
     "qjl_timing_enable": (c_i32, [c_i32]),
     "qjl_timing_read": (c_i32, [P(c_dbl), P(c_i32), c_i32]),
     "qjl_quantize_values": (c_i32, [c_vp, c_i32, c_i64, c_i64, P(ValueCacheDesc), c_i64, c_vp]),

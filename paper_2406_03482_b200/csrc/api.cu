@@ -428,6 +428,15 @@ int qjl_bench_decode_kernel(const qjl_key_cache_t* cache, const qjl_value_cache_
                            workspace_bytes, reps, ms, (cudaStream_t)stream);
 }
 
+int qjl_tensor_core_path(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int G) {
+  QJL_TRY(check_key_cache(cache));
+  if (values) QJL_TRY(check_value_cache(values, cache->d, cache->units));
+  if (G < 1) return QJL_ERR_ARG;
+  if (values && values->layout != QJL_VLAYOUT_P2T) return 0;
+  if (!values && cache->tile_stride == 0) return 0;
+  return tile_path_supported(*cache, values, G) ? 1 : 0;
+}
+
 int64_t qjl_tile_record(int d, int m_in, int m_out, int values, int64_t* offsets) {
   if (d < 1 || m_in < 0 || m_out < 0 || m_in % 32 || m_out % 32) return -1;
   if (values && d != 128) return -1;

@@ -52,8 +52,8 @@ constexpr int kStages = 3;         // records in flight per CTA (a refill is iss
 constexpr int kRecF = 130;         // per (partial, query): m (log2 domain), l, out[128]
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
-constexpr float kPMax = 8.0e6f;                  // P' fixed-point full scale (< 2^23 - 32896)
-constexpr float kMagic = 8421504.f;              // 2^23 + 32896
+constexpr float kPMax = 8.0e6f;                  // P' fixed-point full scale (< 2^23)
+constexpr float kMagic = 8388608.f;              // 2^23: fma(p, s, 2^23) leaves rint(p s) in the mantissa
 
 // Decode-step append: the new token of every unit, quantized inside the
 // query-sketch kernel (which streams S_full anyway) and written at row `row` before the
@@ -113,7 +113,7 @@ struct Layout {
   static constexpr int oBpv = oBsc + NH * 2048;         // [4 heads][128 tokens][16 B] (MN-major chunks)
   static constexpr int oRed = oBsc;                     // flush scratch aliases Bsc/Bpv
   static constexpr int oStage = oBpv + 4 * 2048;
-  static constexpr int oMax = oStage + kStages * kRec;  // [4 warps][8] tile maxima
+  static constexpr int oMax = oStage + kStages * kRec;  // [8 slots][4 warps] tile maxima
   static constexpr int oQc = oMax + 4 * 8 * 4;          // [4 queries] float4 estimator constants
   static constexpr int oBar = oQc + 4 * 16;
   static constexpr int kBars = kStages + 3;             // full[kStages], score MMA, PV MMA, B image
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     mbar_wait(a_pv, pv_ph);
     pv_ph ^= 1;
     tc_fence_after();
-    uint32_t dd[4][4];                                    // [head q][lo, mid, hi, pad]
+    uint32_t dd[4][4];                                    // [head q][lo, mid, hi, exponent byte]
 #pragma unroll
     for (int q = 0; q < NQ; ++q) tmem_ld4(tlane + 32 + 16 * q + 4 * warp, dd[q]);   // value group = warp
     tmem_wait_ld();
@@ -777,9 +777,10 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
           float tm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
           for (int q = 0; q < NQ; ++q) tm[q] = redux_max(lg[q]);
-          if (lane == 0) {
-            *reinterpret_cast<float4*>(mx + warp * 8) = make_float4(tm[0], tm[1], tm[2], tm[3]);
-            mx[warp * 8 + 4] = smax_w;
+          if (lane == 0) {                        // slot-major: slot q's 4 warp maxima are one float4
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) mx[4 * q + warp] = tm[q];
+            mx[16 + warp] = smax_w;
           }
         }
         // A_pv row of dim tid (the score MMA is done, its A columns are free): 32 columns of
@@ -787,12 +788,13 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
         {
           const uint32_t mk = 0x03030303u << (2 * (tid & 3));
           const uint4* cs = reinterpret_cast<const uint4*>(st + L::oCodes + (tid >> 2) * 128);
+          const int sw = (tid >> 2) & 7;                  // chunk swizzle of this dim quad (p2t_byte)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             uint32_t cw[16];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              const uint4 x = cs[4 * h + k];
+              const uint4 x = cs[(4 * h + k) ^ sw];
               cw[4 * k] = x.x & mk; cw[4 * k + 1] = x.y & mk; cw[4 * k + 2] = x.z & mk; cw[4 * k + 3] = x.w & mk;
             }
             tmem_st16(tlane + 16 * h, cw);
@@ -802,10 +804,9 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
         if (tid == 0 && iss_i < ntiles) issue_next();   // refill this stage kStages ahead
 
         // ---------------- 4. softmax bookkeeping, lane-parallel over the heads ----------------
-        // lane l holds slot (l & 7) of the 4 warps' maxima: heads 0..3, the scale bound at 4
-        float mv = reinterpret_cast<const float*>(sm + L::oMax)[lane];
-        mv = fmaxf(mv, __shfl_xor_sync(0xffffffffu, mv, 8));
-        mv = fmaxf(mv, __shfl_xor_sync(0xffffffffu, mv, 16));
+        // lane l reduces slot (l & 7) over the 4 warps: heads 0..3, the scale bound at 4
+        const float4 m4 = reinterpret_cast<const float4*>(sm + L::oMax)[lane & 7];
+        const float mv = fmaxf(fmaxf(m4.x, m4.y), fmaxf(m4.z, m4.w));
         const float smax = __shfl_sync(0xffffffffu, mv, 4);
         // p = 2^(lg - m_new) = pt * et with pt = 2^(lg - tmax) <= 1 and the tile-uniform
         // et = 2^(tmax - m_new); P' K = pt * scale * kPMax / smax <= kPMax, and the PV sums
@@ -852,15 +853,11 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
             Z[q][1] = fma2(pp, z23, Z[q][1]);
             const float2 pk2 = make_float2(pk[q], pk[q]);
             const float2 w01 = fma2(pk2, s01, mg), w23 = fma2(pk2, s23, mg);
-            // column n = 16 q + 4 G + digit, digit = lo, mid, hi, 0 of v(q, G) = rint(P' K):
-            // the fma leaves u = v + 32896 in the mantissa, so (w ^ 0x8080) & 0xFFFFFF is
-            // {lo, mid, hi, 0} (balanced digits) -- one LOP3 per (q, G)
-            uint32_t o[4];
-            const uint32_t w[4] = {__float_as_uint(w01.x), __float_as_uint(w01.y), __float_as_uint(w23.x),
-                                   __float_as_uint(w23.y)};
-#pragma unroll
-            for (int G = 0; G < 4; ++G) asm("lop3.b32 %0, %1, 0x8080, 0xFFFFFF, 0x28;" : "=r"(o[G]) : "r"(w[G]));
-            bpv[128 * q] = make_uint4(o[0], o[1], o[2], o[3]);
+            // column n = 16 q + 4 G + digit: the fma leaves v(q, G) = rint(P' K) < 2^23 in the
+            // mantissa, so the float's bytes ARE the unsigned digits {lo, mid, hi} of the u8 B
+            // operand; byte 3 (the exponent, 0x4B) feeds a column nobody reads
+            bpv[128 * q] = make_uint4(__float_as_uint(w01.x), __float_as_uint(w01.y), __float_as_uint(w23.x),
+                                      __float_as_uint(w23.y));
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // B_pv -> tensor core
@@ -872,7 +869,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
         if (warp == 0) {
           if (elect_one()) {
             tc_fence_after();
-            constexpr uint32_t ID = idesc_i8(16 * NQ, 1);           // N = (head, group, digit)
+            constexpr uint32_t ID = idesc_i8(16 * NQ, 1, 0);        // N = (head, group, digit), B u8
             mma_i8<0>(tbase + 32, tbase, dpv0, ID);
             mma_i8<1>(tbase + 32, tbase + 8, dpv0 + 32, ID);       // + 512 B per 32 tokens
             mma_i8<1>(tbase + 32, tbase + 16, dpv0 + 64, ID);
@@ -1127,10 +1124,13 @@ static Plan make_plan(const qjl_key_cache_t& kc, int64_t n, int G, int id, bool 
 }  // namespace ud
 
 // The tile-major fast path: P2T values in the same records as the keys, d = 128, G <= 4,
-// (m_in/32, m_out/32) in the instantiated set.
+// (m_in/32, m_out/32) in the instantiated set.  vc == nullptr (scores): the key fields of
+// either record variant (keys only, or keys + values) -- they sit at the same offsets.
 static bool record_matches(const qjl_key_cache_t& kc, const qjl_value_cache_t* vc) {
   const TileRecord r = tile_record(kc.d, kc.m_in, kc.m_out, vc != nullptr);
-  if (kc.tile_stride != r.bytes || kc.capacity % 128 != 0) return false;
+  const bool stride_ok = vc ? kc.tile_stride == r.bytes
+                            : (kc.tile_stride == r.bytes || kc.tile_stride == tile_record(kc.d, kc.m_in, kc.m_out, true).bytes);
+  if (!stride_ok || kc.capacity % 128 != 0) return false;
   const uint8_t* base = kc.bits_in;
   if (kc.m_out && (kc.bits_out != base + r.off[QJL_REC_BITS_OUT] ||
                    (const uint8_t*)kc.norm_out != base + r.off[QJL_REC_NORM_OUT]))

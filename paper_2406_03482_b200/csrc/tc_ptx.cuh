@@ -73,10 +73,10 @@ __device__ __forceinline__ bool elect_one() {
   asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}" : "=r"(pred));
   return pred != 0;
 }
-// instruction descriptor: D s32, A u8 (K-major, from TMEM), B s8, M = 128, N = n
-__host__ __device__ constexpr uint32_t idesc_i8(int n, int b_mn_major) {
-  return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(n >> 3) << 17) |
-         ((uint32_t)(128 >> 4) << 24);
+// instruction descriptor: D s32, A u8 (K-major, from TMEM), B s8 or u8, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_i8(int n, int b_mn_major, int b_signed = 1) {
+  return (2u << 4) | (0u << 7) | ((uint32_t)b_signed << 10) | ((uint32_t)b_mn_major << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 // K-major SWIZZLE_128B descriptor (rows of 128 B, 8-row atoms 1024 B apart)
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {

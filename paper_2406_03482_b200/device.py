@@ -207,6 +207,14 @@ class DeviceKeyCache:
         idx = torch.arange(self.shape.capacity, device=self.device)[rows]
         t[:, idx // 128, idx % 128] = value
 
+    def tensor_core_path(self, G: int, scores: bool = False) -> bool:
+        """True when decode (or scores) with G query heads runs the tensor-core kernels."""
+        kd = self.key_desc()
+        if scores or not self.with_values:
+            return self.lib.qjl_tensor_core_path(ctypes.byref(kd), None, G) == 1
+        vd = self.value_desc()
+        return self.lib.qjl_tensor_core_path(ctypes.byref(kd), ctypes.byref(vd), G) == 1
+
     # ------------------------------------------------------------ descriptors
     def _ptr_of(self, name: str) -> int | None:
         if self.tiled:
@@ -531,10 +539,13 @@ class DeviceKeyCache:
 
 
 def _p2t_tables():
-    """P2T byte offset / shift of every (token, dim) of a 128-token tile (`p2t_byte`)."""
+    """P2T byte offset / shift of every (token, dim) of a 128-token tile (`p2t_byte` in
+    csrc/common.cuh: dim quad dq = d // 4 owns 128 bytes, its 16-token chunk j stored at
+    chunk position j ^ (dq % 8))."""
     t = np.arange(128)[:, None]
     d = np.arange(128)[None, :]
-    byte = (d >> 2) * 128 + (t >> 2) * 4 + (t & 3)
+    dq, tw = d >> 2, t >> 2
+    byte = dq * 128 + (((tw >> 2) ^ (dq & 7)) << 4) + ((tw & 3) << 2) + (t & 3)
     return (np.broadcast_to(byte, (128, 128)).astype(np.int64),
             np.broadcast_to(2 * (d & 3), (128, 128)).astype(np.uint8))
 

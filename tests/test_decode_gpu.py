@@ -35,6 +35,7 @@ def _sample_units(U):
 @pytest.mark.parametrize("U,n,G,h,m_in,m_out", SHAPES)
 def test_decode_matches_oracle(cuda, U, n, G, h, m_in, m_out):
     c, q = make_cache(U, n, G, h, m_in, m_out, seed=U * 7 + n)
+    assert c.tensor_core_path(G)
     for T in (1.0, float(np.sqrt(128))):
         lse = torch.empty(U, G, device="cuda")
         out = c.decode(q, temperature=T, lse=lse).double().cpu().numpy()
@@ -55,6 +56,7 @@ def test_decode_matches_oracle(cuda, U, n, G, h, m_in, m_out):
 def test_scores_kernel_matches_oracle(cuda, U, n, G, h, m_in, m_out):
     """Scores-only K2 on tile records (kvcache.py:311-329) against estimate_logits."""
     c, q = make_cache(U, n, G, h, m_in, m_out, seed=U + 3 * n)
+    assert c.tensor_core_path(G, scores=True)
     logits = c.scores(q).double().cpu().numpy()
     from tests._cache import oracle_unit
 
@@ -149,9 +151,13 @@ def test_stale_padding_rows_are_masked(cuda):
     for name, val in (("v_scale", float("inf")), ("v_zero", float("nan")), ("norm_in", float("nan")),
                       ("bits_in", 0x55)):
         c.fill_rows(name, rows, val)
-    # P2T codes are tile-interleaved: tokens 1000..1023 are bytes dq*128 + 104..127 of tile 7
+    # P2T codes are tile-interleaved: the bytes of tokens 1000..1023 (tile 7, rows 104..127)
+    from paper_2406_03482_b200.device import _P2T_BYTE
+
     fv = c.field_view("v_codes")
-    fv.view(fv.shape[0], fv.shape[1], 32, 128)[:, 7, :, 104:] = 0xFF
+    flat = fv.view(fv.shape[0], fv.shape[1], 4096)
+    idx = torch.as_tensor(np.unique(_P2T_BYTE[104:128].ravel()), device="cuda")
+    flat[:, 7, idx] = 0xFF
     out = c.decode(q)
     assert torch.equal(out, ref)
 
@@ -163,5 +169,6 @@ def test_rejects_unsupported_p2t_shapes(cuda):
     c.set_sketches(*DeviceKeyCache.make_sketches(128, 0, 256, 0, operand="bf16"))
     K = torch.randn(2, 10, 128, device="cuda", dtype=torch.bfloat16)
     c.append(K, K)
+    assert c.tensor_core_path(4) and not c.tensor_core_path(5)
     with pytest.raises(NotImplementedError):
         c.decode(torch.randn(2, 5, 128, device="cuda", dtype=torch.bfloat16))   # G = 5 > 4

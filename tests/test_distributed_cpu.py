@@ -64,3 +64,50 @@ def test_gloo_gather_two_ranks(total):
     for rank, ids, shape in results:
         assert ids == [float(i) for i in range(total)]
         assert shape == (total, 4, 8)
+
+
+def _bench_worker(rank, world, port, q):
+    """One rank of bench.py's strong-scaled C3 layout on CPU: its KV-head shard of the 64
+    units, per-global-unit seeded inputs (bench.unit_tensor), a per-unit stand-in for the
+    decode, and the output gather."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+
+        w = bench.WORKLOADS["c3"]
+        total = w["batch"] * w["kv_heads"]
+        s = shard_units(total, world, rank)
+        qs = torch.stack([bench.unit_tensor((w["G"], w["d"]), 1, s.start + i, "cpu", torch.float32)
+                          for i in range(s.count)])
+        local = torch.tanh(qs) * (torch.arange(s.start, s.stop)[:, None, None] + 1.0)   # [count, G, d]
+        full = gather_units(local.contiguous(), s)
+        q.put((rank, s.start, s.count, full.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_strong_scaled_shards_equal_single_rank():
+    """Shard -> per-rank inputs -> gather over two ranks equals the single-rank computation
+    bit for bit (units are independent and seeded by their global index)."""
+    import bench
+
+    w = bench.WORKLOADS["c3"]
+    total = w["batch"] * w["kv_heads"]
+    qs = torch.stack([bench.unit_tensor((w["G"], w["d"]), 1, u, "cpu", torch.float32) for u in range(total)])
+    ref = (torch.tanh(qs) * (torch.arange(total)[:, None, None] + 1.0)).numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    starts = sorted((r[1], r[2]) for r in results)
+    assert starts == [(0, total // 2), (total // 2, total // 2)]     # a KV-head split: 4 heads x 8 batches each
+    for _, _, _, full in results:
+        assert full.shape == (total, w["G"], w["d"])
+        assert (full == ref).all()

@@ -94,7 +94,12 @@ enum {
    * every input of this call (cache rows, q, k_new, v_new, sketch) was written before that
    * launch: the query-sketch kernel may then read its inputs while the previous decode
    * drains (programmatic dependent launch).  Without it every read waits for the stream. */
-  QJL_DECODE_CHAINED = 1
+  QJL_DECODE_CHAINED = 1,
+  /* Fixed 512-token segments per unit, merged in segment order: a unit's output bits depend
+   * only on that unit (a unit-sharded decode equals the unsharded one bit for bit).  The
+   * default schedule splits the flattened (unit, tile) space evenly over the CTAs, so a
+   * unit's partial sums follow the launch's total size (equal within rounding). */
+  QJL_DECODE_DETERMINISTIC = 2
 };
 
 typedef struct qjl_key_cache {

@@ -17,7 +17,7 @@ QJL_OK, QJL_ERR_ARG, QJL_ERR_UNSUPPORTED, QJL_ERR_CUDA, QJL_ERR_WORKSPACE, QJL_E
     0, -1, -2, -3, -4, -5)
 QJL_F32, QJL_F16, QJL_BF16, QJL_F64 = 0, 1, 2, 3
 QJL_VLAYOUT_U8, QJL_VLAYOUT_P2T = 0, 2
-QJL_DECODE_CHAINED = 1
+QJL_DECODE_CHAINED, QJL_DECODE_DETERMINISTIC = 1, 2
 (QJL_REC_BITS_IN, QJL_REC_BITS_OUT, QJL_REC_NORM_IN, QJL_REC_NORM_OUT, QJL_REC_CODES, QJL_REC_ZERO,
  QJL_REC_SCALE) = range(7)
 

@@ -124,13 +124,14 @@ __host__ __device__ __forceinline__ int64_t tile_off(int64_t u, int64_t row, int
 // x 4 dims (2-bit slots), so one mask per word yields the u8 A-operand column of a
 // TMEM-resident PV operand (row = dim, weight 4^(d % 4) folded out per row).  Row
 // dq = d / 4 of a tile holds 128 bytes = 8 chunks of 16 tokens; chunk j is stored at chunk
-// position j ^ (dq % 8), so the 8 rows a warp's dims read sit in 8 different bank groups.
+// position j ^ (dq % 4), so the rows of any 8 consecutive threads (two dim quads, one phase
+// of a 128-bit shared load) sit in different bank groups.
 // In-tile byte of (token t, dim d), and the bit shift of its 2-bit slot:
-//   byte = dq * 128 + ((tw / 4) ^ (dq % 8)) * 16 + (tw % 4) * 4 + t % 4,  tw = (t % 128) / 4
+//   byte = dq * 128 + ((tw / 4) ^ (dq % 4)) * 16 + (tw % 4) * 4 + t % 4,  tw = (t % 128) / 4
 //   shift = 2 * (d % 4)
 __host__ __device__ __forceinline__ int p2t_byte(int64_t t, int d) {
   const int dq = d >> 2, tw = (int)((t & 127) >> 2);
-  return dq * 128 + ((((tw >> 2) ^ (dq & 7))) << 4) + ((tw & 3) << 2) + (int)(t & 3);
+  return dq * 128 + ((((tw >> 2) ^ (dq & 3))) << 4) + ((tw & 3) << 2) + (int)(t & 3);
 }
 
 // Canonical tile record (qjl_b200.h: qjl_tile_record): offsets of the QJL_REC_* fields.

@@ -47,6 +47,10 @@ namespace ud {
 using namespace ptx;
 
 constexpr int kThreads = 128;      // 4 warps; thread t: token t (scores) and dim t (PV)
+#ifndef QJL_UD_SPLIT
+#define QJL_UD_SPLIT 0             // 1: the MMA issuer waits on mbarriers the warps arrive on
+#endif
+constexpr bool kSplit = QJL_UD_SPLIT != 0;
 constexpr int kTile = 128;         // tokens per tile
 constexpr int kStages = 3;         // records in flight per CTA (a refill is issued kStages ahead)
 constexpr int kRecF = 130;         // per (partial, query): m (log2 domain), l, out[128]
@@ -80,6 +84,9 @@ struct Params {
   int ctas;
   int max_seg;
   int chained;           // QJL_DECODE_CHAINED: cache copies may start before the grid-dependency wait
+  int seg;               // QJL_DECODE_DETERMINISTIC: tiles per fixed segment (CTAs own whole
+                         // segments; partial slot = segment index); 0: stream-K over tiles
+  int spu;               // segments per unit (deterministic) -- total work units = units * spu
   const uint8_t* bsc;    // [units][NH][2048] score B operand images (SW128, K-major)
   const float4* qconst;  // [units][4 queries] {k_in, b_in, k_out, b_out} (log2 domain)
   float* part;           // [units][max_seg][G][kRecF]
@@ -116,7 +123,7 @@ struct Layout {
   static constexpr int oMax = oStage + kStages * kRec;  // [8 slots][4 warps] tile maxima
   static constexpr int oQc = oMax + 4 * 8 * 4;          // [4 queries] float4 estimator constants
   static constexpr int oBar = oQc + 4 * 16;
-  static constexpr int kBars = kStages + 3;             // full[kStages], score MMA, PV MMA, B image
+  static constexpr int kBars = kStages + 5;             // full[kStages], score MMA, PV MMA, B image, A ready, P ready
   static constexpr int oTmem = oBar + kBars * 8;
   static constexpr int oFlag = oTmem + 4;
   static constexpr int kTotal = oFlag + 12 + 1024;      // + alignment slack
@@ -490,12 +497,27 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
   const uint32_t s_sm = smem_u32(sm);
   const uint32_t a_full = s_sm + L::oBar;                      // [kStages]
-  const uint32_t a_sc = a_full + 8 * kStages, a_pv = a_sc + 8, a_bsc = a_sc + 16;
+  const uint32_t a_sc = a_full + 8 * kStages, a_pv = a_sc + 8, a_bsc = a_sc + 16, a_ard = a_sc + 24,
+                 a_prd = a_sc + 32;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::oTmem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = P.ctas;
   const int64_t T = P.total_tiles;
-  const int64_t r0 = tile_begin(blockIdx.x, T, C), r1 = tile_begin(blockIdx.x + 1, T, C);
+  // contiguous ranges of the flattened (unit, tile) space; deterministic: of whole segments
+  auto seg_tile = [&](int64_t g) -> int64_t {          // first flattened tile of segment g
+    const int64_t u = g / P.spu, j = g - u * P.spu;
+    const int64_t t = j * P.seg;
+    return u * P.tpu + (t < P.tpu ? t : P.tpu);
+  };
+  int64_t r0, r1;
+  if (P.seg) {
+    const int64_t Sg = (int64_t)P.units * P.spu;
+    r0 = seg_tile(tile_begin(blockIdx.x, Sg, C));
+    r1 = seg_tile(tile_begin(blockIdx.x + 1, Sg, C));
+  } else {
+    r0 = tile_begin(blockIdx.x, T, C);
+    r1 = tile_begin(blockIdx.x + 1, T, C);
+  }
   const int ntiles = (int)(r1 - r0);
   const int u_first = (int)(r0 / P.tpu), lt_first = (int)(r0 - (int64_t)u_first * P.tpu);
   if (tid == 0) {
@@ -503,6 +525,8 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     mbar_init(a_sc, 1);
     mbar_init(a_pv, 1);
     mbar_init(a_bsc, 1);
+    mbar_init(a_ard, 4);
+    mbar_init(a_prd, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid < 32) reinterpret_cast<float*>(sm + L::oMax)[tid] = 0.f;
@@ -547,8 +571,10 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   float m_lane = -INFINITY, l_part[4], acc[4], invK[4];
   float2 Z[4][2];                      // [q][group pair]
   const float4* qcs = reinterpret_cast<const float4*>(sm + L::oQc);
-  uint32_t sc_ph = 0, pv_ph = 0, bsc_par = 0;
+  uint32_t sc_ph = 0, pv_ph = 0, bsc_par = 0, rd_ph = 0;
   bool pv_pend = false;
+  // the thread's code-chunk offsets within its dim quad's 128-byte row (p2t_byte swizzle)
+  const uint32_t c_row = L::oCodes + (tid >> 2) * 128, c_sw = ((tid >> 2) & 3) << 4;
 
   // PV accumulators of the previous tile -> fp32 running output (thread = dim)
   auto pv_readback = [&]() {
@@ -575,6 +601,8 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       mbar_expect_tx(a_bsc, L::NH * 2048);
       bulk_g2s(s_sm + L::oBsc, P.bsc + (size_t)u * L::NH * 2048, L::NH * 2048, a_bsc);
     }
+  };
+  auto reset_state = [&]() {
     m_lane = -INFINITY;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -584,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     }
   };
 
-  auto flush = [&](int u) {
+  auto flush = [&](int u, int slot, int ns) {
     if (pv_pend) {
       pv_readback();
       pv_pend = false;
@@ -621,9 +649,6 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       }
     }
     bar_sync(1, kThreads);
-    const int c0 = cta_of_tile((int64_t)u * P.tpu, T, C);
-    const int c1 = cta_of_tile((int64_t)u * P.tpu + P.tpu - 1, T, C);
-    const int ns = c1 - c0 + 1, slot = blockIdx.x - c0;
     // the running maxima of the heads, from their lanes
     float mrun[4];
 #pragma unroll
@@ -714,10 +739,24 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   int u = u_first, lt = lt_first, s = 0;
   uint32_t full_ph = 0;
   int it = 0;
+  bool first = true;                                      // the MMA issuer waits for the B image
   while (it < ntiles) {
-    const int seg_end = min(ntiles, it + (P.tpu - lt));   // this unit's tiles in the range
-    load_unit(u);
-    bool first = true;                                    // the MMA issuer waits for the B image
+    // this piece: to the end of the unit (stream-K) or of the fixed segment (deterministic)
+    const int piece_end_lt = P.seg ? min((lt / P.seg + 1) * P.seg, P.tpu) : P.tpu;
+    const int seg_end = min(ntiles, it + (piece_end_lt - lt));
+    int slot, ns;
+    if (P.seg) {
+      slot = lt / P.seg;
+      ns = P.spu;
+    } else {
+      const int c0 = cta_of_tile((int64_t)u * P.tpu, T, C);
+      const int c1 = cta_of_tile((int64_t)u * P.tpu + P.tpu - 1, T, C);
+      ns = c1 - c0 + 1;
+      slot = blockIdx.x - c0;
+    }
+    load_unit(u);             // (again after a segment flush: the flush scratch aliases the B image)
+    first = true;
+    reset_state();
     for (; it < seg_end; ++it, ++lt) {
       mbar_wait(a_full + 8 * s, full_ph);
       const uint8_t* st = sm + L::oStage + s * L::kRec;
@@ -734,9 +773,15 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
         }
         tmem_wait_st();
         tc_fence_before();
-        bar_sync(1, kThreads);
+        if constexpr (kSplit) {
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a_ard) : "memory");
+        } else {
+          bar_sync(1, kThreads);
+        }
         if (warp == 0) {
           if (elect_one()) {
+            if (kSplit) mbar_wait(a_ard, rd_ph);
             if (first) {
               mbar_wait(a_bsc, bsc_par);
               bsc_par ^= 1;
@@ -787,14 +832,14 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
         // 4 tokens, value c * 4^(tid % 4)
         {
           const uint32_t mk = 0x03030303u << (2 * (tid & 3));
-          const uint4* cs = reinterpret_cast<const uint4*>(st + L::oCodes + (tid >> 2) * 128);
-          const int sw = (tid >> 2) & 7;                  // chunk swizzle of this dim quad (p2t_byte)
+          const uint8_t* crow = st + c_row;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             uint32_t cw[16];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              const uint4 x = cs[(4 * h + k) ^ sw];
+              // chunk 4h + k sits at position (4h + k) ^ (dq % 4) = 4h + (k ^ (dq % 4))
+              const uint4 x = *reinterpret_cast<const uint4*>(crow + ((k << 4) ^ c_sw) + 64 * h);
               cw[4 * k] = x.x & mk; cw[4 * k + 1] = x.y & mk; cw[4 * k + 2] = x.z & mk; cw[4 * k + 3] = x.w & mk;
             }
             tmem_st16(tlane + 16 * h, cw);
@@ -863,11 +908,17 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // B_pv -> tensor core
         tmem_wait_st();
         tc_fence_before();
-        bar_sync(1, kThreads);
+        if constexpr (kSplit) {
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a_prd) : "memory");
+        } else {
+          bar_sync(1, kThreads);
+        }
 
         // ---------------- 6. PV MMA (read back at the next tile) ----------------
         if (warp == 0) {
           if (elect_one()) {
+            if (kSplit) mbar_wait(a_prd, rd_ph);
             tc_fence_after();
             constexpr uint32_t ID = idesc_i8(16 * NQ, 1, 0);        // N = (head, group, digit), B u8
             mma_i8<0>(tbase + 32, tbase, dpv0, ID);
@@ -879,6 +930,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
           __syncwarp();
         }
         pv_pend = true;
+        rd_ph ^= 1;
       };
       if ((lt + 1) * kTile <= n32) body(std::false_type{});
       else body(std::true_type{});
@@ -889,9 +941,11 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       }
     }
     if (it == ntiles) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // all tiles consumed
-    flush(u);
-    ++u;
-    lt = 0;
+    flush(u, slot, ns);
+    if (lt == P.tpu) {
+      ++u;
+      lt = 0;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -1028,6 +1082,7 @@ struct Plan {
   int tpu;
   int ctas;
   int max_seg;
+  int seg, spu;
   int64_t T;
   size_t bsc_off, qconst_off, part_off, cnt_off, total;
 };
@@ -1100,17 +1155,26 @@ static int nh_by_id(int id) {
   return nh[id];
 }
 
-static Plan make_plan(const qjl_key_cache_t& kc, int64_t n, int G, int id, bool scores) {
+constexpr int kDetSeg = 4;          // deterministic schedule: 512-token segments
+
+static Plan make_plan(const qjl_key_cache_t& kc, int64_t n, int G, int id, bool scores, bool det = false) {
   Plan p;
   p.tpu = (int)((n + kTile - 1) / kTile);
   p.T = (int64_t)kc.units * p.tpu;
   const int64_t slots = (int64_t)device_sm_count() * occupancy_by_id(id, G, scores);
-  p.ctas = (int)(p.T < slots ? p.T : slots);
+  p.seg = det && !scores ? kDetSeg : 0;
+  p.spu = p.seg ? (p.tpu + p.seg - 1) / p.seg : 1;
+  const int64_t work = p.seg ? (int64_t)kc.units * p.spu : p.T;
+  p.ctas = (int)(work < slots ? work : slots);
   int ms = 1;
-  for (int u = 0; u < kc.units; ++u) {
-    const int ns =
-        cta_of_tile((int64_t)u * p.tpu + p.tpu - 1, p.T, p.ctas) - cta_of_tile((int64_t)u * p.tpu, p.T, p.ctas) + 1;
-    ms = ms > ns ? ms : ns;
+  if (p.seg) {
+    ms = p.spu;
+  } else {
+    for (int u = 0; u < kc.units; ++u) {
+      const int ns = cta_of_tile((int64_t)u * p.tpu + p.tpu - 1, p.T, p.ctas) -
+                     cta_of_tile((int64_t)u * p.tpu, p.T, p.ctas) + 1;
+      ms = ms > ns ? ms : ns;
+    }
   }
   p.max_seg = ms;
   p.bsc_off = 0;
@@ -1155,7 +1219,9 @@ bool tile_path_supported(const qjl_key_cache_t& kc, const qjl_value_cache_t* vc,
 size_t decode_tile_workspace(const qjl_key_cache_t& kc, int64_t n, int G, bool scores) {
   int id;
   if (!ud::kc_dispatch(kc.m_in / 32, kc.m_out / 32, &id)) return 0;
-  return ud::make_plan(kc, n, G, id, scores).total;
+  const size_t a = ud::make_plan(kc, n, G, id, scores).total;
+  const size_t b = scores ? 0 : ud::make_plan(kc, n, G, id, false, true).total;   // either schedule
+  return a > b ? a : b;
 }
 
 namespace ud {
@@ -1246,6 +1312,8 @@ static int launch_impl(const Launch& a, const Plan& plan, cudaStream_t st) {
   // with an append the prep writes a row the decode streams: the decode's early copies
   // rely on the prep's fence-then-trigger order, which holds only for chained launches
   P.chained = chained;
+  P.seg = plan.seg;
+  P.spu = plan.spu;
   P.bsc = bsc;
   P.qconst = qconst;
   P.part = part;
@@ -1302,7 +1370,7 @@ static int launch_any(const Launch& a, size_t ws_bytes, cudaStream_t st) {
   const qjl_key_cache_t& kc = *a.kc;
   int id;
   if (!kc_dispatch(kc.m_in / 32, kc.m_out / 32, &id)) return QJL_ERR_UNSUPPORTED;
-  const Plan plan = make_plan(kc, a.n, a.G, id, a.mode == 1);
+  const Plan plan = make_plan(kc, a.n, a.G, id, a.mode == 1, (a.flags & QJL_DECODE_DETERMINISTIC) != 0);
   if (ws_bytes < plan.total) {
     set_error("decode workspace needs %zu bytes", plan.total);
     return QJL_ERR_WORKSPACE;

@@ -418,10 +418,13 @@ class DeviceKeyCache:
 
     def decode(self, q: torch.Tensor, temperature: float = 1.0, n: int | None = None,
                out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
-               chained: bool = False, logits: torch.Tensor | None = None) -> torch.Tensor:
+               chained: bool = False, logits: torch.Tensor | None = None,
+               deterministic: bool = False) -> torch.Tensor:
         """K2+K3: softmax(logits / T) @ V per query head -> [U, G, d] f32 (attention.py:56-71).
         `chained`: the previous kernel on the stream is this cache's decode and every input
-        predates it (QJL_DECODE_CHAINED) -- lets the query sketch overlap that decode."""
+        predates it (QJL_DECODE_CHAINED) -- lets the query sketch overlap that decode.
+        `deterministic`: fixed per-unit segments (QJL_DECODE_DETERMINISTIC), so each unit's
+        output is independent of the other units in the call (sharding-invariant bits)."""
         if temperature <= 0:
             raise ValueError(f"temperature must be positive, got {temperature}")
         if not self.with_values:
@@ -441,7 +444,8 @@ class DeviceKeyCache:
                                        _TORCH2QJL[q.dtype], G, ctypes.byref(sd),
                                        1.0 / float(temperature), out.data_ptr(), _ptr(lse), _ptr(logits),
                                        ws.data_ptr(), ws.numel(),
-                                       _lib.QJL_DECODE_CHAINED if chained else 0, _stream()), "decode")
+                                       (_lib.QJL_DECODE_CHAINED if chained else 0) |
+                                       (_lib.QJL_DECODE_DETERMINISTIC if deterministic else 0), _stream()), "decode")
         return out
 
     def bench_decode_kernel(self, q: torch.Tensor, reps: int, temperature: float = 1.0,
@@ -541,11 +545,11 @@ class DeviceKeyCache:
 def _p2t_tables():
     """P2T byte offset / shift of every (token, dim) of a 128-token tile (`p2t_byte` in
     csrc/common.cuh: dim quad dq = d // 4 owns 128 bytes, its 16-token chunk j stored at
-    chunk position j ^ (dq % 8))."""
+    chunk position j ^ (dq % 4))."""
     t = np.arange(128)[:, None]
     d = np.arange(128)[None, :]
     dq, tw = d >> 2, t >> 2
-    byte = dq * 128 + (((tw >> 2) ^ (dq & 7)) << 4) + ((tw & 3) << 2) + (t & 3)
+    byte = dq * 128 + (((tw >> 2) ^ (dq & 3)) << 4) + ((tw & 3) << 2) + (t & 3)
     return (np.broadcast_to(byte, (128, 128)).astype(np.int64),
             np.broadcast_to(2 * (d & 3), (128, 128)).astype(np.uint8))
 

@@ -172,3 +172,34 @@ def test_rejects_unsupported_p2t_shapes(cuda):
     assert c.tensor_core_path(4) and not c.tensor_core_path(5)
     with pytest.raises(NotImplementedError):
         c.decode(torch.randn(2, 5, 128, device="cuda", dtype=torch.bfloat16))   # G = 5 > 4
+
+
+def test_sharded_decode_bitwise_equals_full(cuda):
+    """units are independent, so decoding the unit range a rank owns
+    (KV-head shards of config 3 at 2/4/8 GPUs) gives the unsharded decode's rows bit for bit
+    under the deterministic schedule (fixed 512-token segments), and within rounding under
+    the default stream-K schedule; the shard's cache records are the full cache's."""
+    import bench
+    from paper_2406_03482_b200.distributed import shard_units
+
+    w = dict(bench.WORKLOADS["c3"], n=4096)            # 64 units x 32 tiles, 8 segments per unit
+    one = shard_units(64, 1, 0)
+    full = bench.build_cache(w, one, 5, cuda)
+    qf = bench.make_queries(w, one, 5, cuda)
+    of = full.decode(qf, deterministic=True).clone()
+    od = full.decode(qf).clone()
+    ref, _ = oracle_decode(full, qf, 63)
+    for g in range(4):
+        assert rel_l2(of[63, g].double().cpu().numpy(), ref[g]) <= OUT_RTOL
+    for world in (2, 4, 8):
+        for r in sorted({0, world // 2, world - 1}):
+            sh = shard_units(64, world, r)
+            c = bench.build_cache(w, sh, 5, cuda)
+            q = bench.make_queries(w, sh, 5, cuda)
+            assert torch.equal(q, qf[sh.start:sh.stop])
+            assert torch.equal(c.records, full.records[sh.start:sh.stop])
+            o = c.decode(q, deterministic=True)
+            assert torch.equal(o, of[sh.start:sh.stop]), (world, r)
+            o2 = c.decode(q).double()
+            e = (o2 - od[sh.start:sh.stop].double()).norm() / od[sh.start:sh.stop].double().norm()
+            assert e <= 1e-5, (world, r, float(e))

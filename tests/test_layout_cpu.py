@@ -21,14 +21,14 @@ def test_p2t_word_holds_four_tokens_of_four_dims():
             assert len(words) == 1
 
 
-def test_p2t_chunks_conflict_free_per_warp():
-    # a warp's 32 threads = dims 32w..32w+31 = 8 dim quads; for every chunk index j the 8
-    # quads' 16-byte chunks fall in 8 distinct 16-byte bank groups (address / 16 mod 8)
-    for w in range(4):
+def test_p2t_chunks_conflict_free_per_phase():
+    # a 128-bit shared load is served 8 threads at a time; threads 8p..8p+7 = two dim quads,
+    # whose 16-byte chunks j must fall in different 16-byte bank groups (address / 16 mod 8)
+    for dq in range(0, 32, 2):
         for j in range(8):
             tok = 16 * j
-            addrs = [int(_P2T_BYTE[tok, 32 * w + 4 * q]) for q in range(8)]
-            assert len({(a // 16) % 8 for a in addrs}) == 8
+            a, b = int(_P2T_BYTE[tok, 4 * dq]), int(_P2T_BYTE[tok, 4 * dq + 4])
+            assert (a // 16) % 8 != (b // 16) % 8
 
 
 def test_pack_unpack_round_trip():

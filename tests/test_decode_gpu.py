@@ -203,3 +203,44 @@ def test_sharded_decode_bitwise_equals_full(cuda):
             o2 = c.decode(q).double()
             e = (o2 - od[sh.start:sh.stop].double()).norm() / od[sh.start:sh.stop].double().norm()
             assert e <= 1e-5, (world, r, float(e))
+
+
+def test_full_config2_against_oracle(cuda):
+    """Full config-2 shape: Llama-2-7B MHA decode, 4 x 32 = 128 units x 4096 tokens, fp16,
+    h = 4 outlier channels x15, m_in 256 + m_out 128; decode, lse and the scores kernel on
+    sampled units against the oracle."""
+    U, n, G = 128, 4096, 1
+    c, q = make_cache(U, n, G, 4, 256, 128, seed=2, dtype=torch.float16, factor=15.0)
+    assert c.tensor_core_path(G) and c.tensor_core_path(G, scores=True)
+    lse = torch.empty(U, G, device="cuda")
+    out = c.decode(q, lse=lse).double().cpu().numpy()
+    logits = c.scores(q).double().cpu().numpy()
+    from tests._cache import oracle_unit
+
+    Qh = q.double().cpu().numpy()
+    for u in (0, 61, U - 1):
+        ref, ref_lg = oracle_decode(c, q, u)
+        assert rel_l2(out[u, 0], ref[0]) <= OUT_RTOL
+        assert abs(float(lse[u, 0]) - logsumexp(ref_lg)[0]) <= 1e-4 * abs(logsumexp(ref_lg)[0])
+        chans, cache, _ = oracle_unit(c, u)
+        ok, err = check_logits(logits[u, 0], ref_lg[0],
+                               logit_bound(c.S_in_host, c.S_out_host, chans, Qh[u, 0], cache["norm_in"],
+                                           cache["norm_out"]))
+        assert ok.all(), (u, err.max())
+
+
+@pytest.mark.parametrize("B,n", [(2, 32768), (1, 131072)])
+def test_config5_m512_long_context_against_oracle(cuda, B, n):
+    """Config 5 with m = 512 (+ m_out 64, r = 8 x20) at n >= 32k: B x 8 KV-head units, G = 4;
+    the first and last units against the oracle."""
+    U, G = B * 8, 4
+    c, q = make_cache(U, n, G, 8, 512, 64, seed=B + n)
+    assert c.tensor_core_path(G)
+    lse = torch.empty(U, G, device="cuda")
+    out = c.decode(q, lse=lse).double().cpu().numpy()
+    for u in (0, U - 1):
+        ref, lg = oracle_decode(c, q, u)
+        ref_lse = logsumexp(lg)
+        for g in range(G):
+            assert rel_l2(out[u, g], ref[g]) <= OUT_RTOL, (u, g, rel_l2(out[u, g], ref[g]))
+            assert abs(float(lse[u, g]) - ref_lse[g]) <= 1e-4 * abs(ref_lse[g])

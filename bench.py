@@ -213,6 +213,11 @@ def oracle_decode_unit(S_in, S_out, hu, Q, T=1.0, with_logits=False):
     return (out, np.stack([r[2] for r in res])) if with_logits else out
 
 
+def _jsonable(o):
+    """numpy scalars (np.bool_, np.float64, ...) in the result dicts -> plain Python."""
+    return o.item() if hasattr(o, "item") else str(o)
+
+
 class _nullctx:
     def __enter__(self):
         return self
@@ -263,7 +268,7 @@ def cpu_baseline_leg(cache, q, w, budget_s=12.0):
                       f"({w['G']} query heads each), oracle/qjl_oracle.py, BLAS pinned to 1 thread, "
                       f"{t_tot:.1f} s"}
     parity = {"outputs_checked": len(rel), "rel_l2_max": max(rel), "rel_l2_mean": float(np.mean(rel)),
-              "tolerance": 1e-3, "pass": max(rel) <= 1e-3 and max(lse_err) <= 1e-4,
+              "tolerance": 1e-3, "pass": bool(max(rel) <= 1e-3 and max(lse_err) <= 1e-4),
               "lse_rel_err_max": float(max(lse_err)),
               "logits_checked": int(lr.size), "logit_rel_err_p99": float(np.percentile(lr, 99)),
               "logit_rel_err_max": float(lr.max()), "logit_err_max_over_row_max": max(lg_scaled),
@@ -672,7 +677,7 @@ def run_gpu(args):
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         res["cpu_baseline"], res["parity"] = cpu_baseline_leg(cache, q, w)
     if rank == 0:
-        print(json.dumps(res), flush=True)
+        print(json.dumps(res, default=_jsonable), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

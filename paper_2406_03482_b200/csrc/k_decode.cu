@@ -83,7 +83,7 @@ struct Params {
   int64_t total_tiles;
   int ctas;
   int max_seg;
-  int chained;           // QJL_DECODE_CHAINED: cache copies may start before the grid-dependency wait
+  int chained;           // QJL_DECODE_CHAINED (informational here; the prep acts on it)
   int seg;               // QJL_DECODE_DETERMINISTIC: tiles per fixed segment (CTAs own whole
                          // segments; partial slot = segment index); 0: stream-K over tiles
   int spu;               // segments per unit (deterministic) -- total work units = units * spu
@@ -356,11 +356,13 @@ __global__ void __launch_bounds__(640) k_uprep(const TQ* __restrict__ q, int G, 
   for (int seg = wid; seg < 8; seg += nwarp) {
     const int g = seg >> 1, side = seg & 1;
     const int lo = side ? MI : 0, hi = side ? MT : MI;
-    const double inv = 1.0 / red[g][side][0];
+    // j - lo = lane (mod 32), so the weight 2^-(j mod 8) is fixed per lane; scaling by a
+    // power of two is exact, so this is rint(Sq_j / (sigma 2^(j mod 8))) bit for bit
+    const int sh = lane & 7;
+    const double inv = 1.0 / red[g][side][0] / (double)(1 << sh);
     long long acc = 0;
     for (int j = lo + lane; j < hi; j += 32) {
-      const int sh = (j - lo) & 7;
-      int32_t x = (int32_t)rint((double)sq[g][j] * inv / (double)(1 << sh));
+      int32_t x = (int32_t)rint((double)sq[g][j] * inv);
       acc += (long long)x * (1ll << sh);
       // four balanced int8 digits of x -> B image rows n = 4 g + t at K byte
       // k = 32 c + 4 s + i of the side (sign bit jj = 32 c + 8 i + s), SWIZZLE_128B
@@ -562,7 +564,11 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
       iss_p += P.rec_bytes;
     }
   };
-  if (!P.chained) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // The first record copies are issued before the grid-dependency wait: the only PDL
+  // predecessor is k_uprep, which triggers its dependents only after its own wait on the
+  // stream (unless the caller vouched for the inputs with QJL_DECODE_CHAINED) and after its
+  // decode-step append is written and fenced -- so every cache row this kernel reads is
+  // complete before it starts.  Only the B images and constants wait for the prep.
   if (tid == 0)
     for (int i = 0; i < kStages && i < ntiles; ++i) issue_next();
 
@@ -1007,8 +1013,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_uscores(
       iss_p += P.rec_bytes;
     }
   };
-  if (!P.chained) asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (tid == 0)
+  if (tid == 0)                                        // (early copies: see k_udecode)
     for (int i = 0; i < kStages && i < ntiles; ++i) issue_next();
   asm volatile("griddepcontrol.wait;" ::: "memory");   // Bsc / qconst come from k_uprep
   const float4* qcs = reinterpret_cast<const float4*>(sm + L::sQc);
@@ -1024,6 +1029,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_uscores(
       bulk_g2s(s_sm, P.bsc + (size_t)u * L::NH * 2048, L::NH * 2048, a_bsc);
     }
     bool first = true;
+    float* const lbase = P.logits + (int64_t)u * P.G * n + tid;      // this unit's rows, this token
     for (; it < seg_end; ++it, ++lt) {
       mbar_wait(a_full + 8 * s, full_ph);
       const uint8_t* st = sm + L::sStage + s * L::kKeyRec;
@@ -1056,11 +1062,11 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_uscores(
       tc_fence_after();
       float lg[4];
       score_logits<KCO, NQ, L::cDsc>(tlane, qcs, nin, nout, lg);
-      const int64_t tok = (int64_t)lt * kTile + tid;
-      if (tok < n) {
+      if (lt * kTile + tid < n) {
+        float* lp = lbase + lt * kTile;
 #pragma unroll
         for (int q = 0; q < NQ; ++q)
-          if (q < P.G) __stcs(P.logits + ((int64_t)u * P.G + q) * n + tok, lg[q] * kLn2);
+          if (q < P.G) __stcs(lp + q * n, lg[q] * kLn2);
       }
       tc_fence_before();
       if (++s == kStages) {
@@ -1267,7 +1273,7 @@ static int launch_impl(const Launch& a, const Plan& plan, cudaStream_t st) {
   pattr[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t pcfg = {};
   pcfg.gridDim = dim3(kc.units);
-  pcfg.blockDim = dim3(MT);
+  pcfg.blockDim = dim3(MT);                      // x threads per row, set per sketch dtype below
   pcfg.stream = st;
   pcfg.attrs = pattr;
   pcfg.numAttrs = 1;

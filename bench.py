@@ -524,6 +524,7 @@ def run_gpu(args):
 
     # ---- roofline: the decode kernel alone, in a chain of back-to-back decodes
     kern_ms = cache.bench_decode_kernel(q, reps=max(args.steps, 20))
+    det_ms = cache.bench_decode_kernel(q, reps=max(args.steps // 4, 20), deterministic=True)
 
     # ---- e2e through the public API with host buffers: every step uploads its query from
     # pinned memory, decodes, all-gathers the outputs over NCCL (N > 1) and reads the gathered
@@ -648,6 +649,7 @@ def run_gpu(args):
                      "kernel_ms": kern_ms,
                      "timing": "mean of back-to-back decode kernels chained with PDL "
                                "(qjl_bench_decode_kernel), CUDA events on the launch stream",
+                     "deterministic_schedule_kernel_ms": det_ms,
                      "traffic": load_traffic(w["workload"])},
         "gpu_launches": 2 * args.steps,
         "clocks": clk.summary(),

@@ -233,12 +233,12 @@ QJL_API int qjl_decode_step(const qjl_key_cache_t* cache, const qjl_value_cache_
  * Runs the query-sketch kernel once, then `reps` back-to-back decode kernels chained with
  * programmatic dependent launch (each one re-reads the whole cache and rewrites out/lse),
  * bracketed by CUDA events on `stream`; *ms = mean kernel time.  Same arguments as
- * qjl_decode otherwise. */
+ * qjl_decode otherwise (flags: QJL_DECODE_DETERMINISTIC selects the schedule timed). */
 QJL_API int qjl_bench_decode_kernel(const qjl_key_cache_t* cache, const qjl_value_cache_t* values,
                                     int64_t n, const void* q, int q_dtype, int G,
                                     const qjl_sketch_t* sketch, float inv_temperature, float* out,
-                                    float* lse, void* workspace, size_t workspace_bytes, int reps,
-                                    float* ms, void* stream);
+                                    float* lse, void* workspace, size_t workspace_bytes, unsigned flags,
+                                    int reps, float* ms, void* stream);
 
 /* Benchmark timing hook: while enabled, every qjl_quantize_keys call is bracketed by CUDA
  * events recorded on its launch stream.  qjl_timing_read synchronizes on them and returns the

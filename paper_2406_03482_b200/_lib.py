@@ -67,7 +67,8 @@ SIGNATURES = {
                                 c_vp, c_i32, c_vp, c_vp, c_flt, c_vp, c_vp, c_vp, c_vp, c_sz, ctypes.c_uint,
                                 c_vp]),
     "qjl_bench_decode_kernel": (c_i32, [P(KeyCacheDesc), P(ValueCacheDesc), c_i64, c_vp, c_i32, c_i32,
-                                        P(SketchDesc), c_flt, c_vp, c_vp, c_vp, c_sz, c_i32, P(c_flt), c_vp]),
+                                        P(SketchDesc), c_flt, c_vp, c_vp, c_vp, c_sz, ctypes.c_uint, c_i32,
+                                        P(c_flt), c_vp]),
     "qjl_tile_record": (c_i64, [c_i32, c_i32, c_i32, c_i32, P(c_i64)]),
     "qjl_tensor_core_path": (c_i32, [P(KeyCacheDesc), P(ValueCacheDesc), c_i32]),
     "qjl_timing_enable": (c_i32, [c_i32]),

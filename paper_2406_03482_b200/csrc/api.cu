@@ -414,8 +414,8 @@ int qjl_decode(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, in
 
 int qjl_bench_decode_kernel(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int64_t n,
                             const void* q, int q_dtype, int G, const qjl_sketch_t* sketch, float inv_temperature,
-                            float* out, float* lse, void* workspace, size_t workspace_bytes, int reps, float* ms,
-                            void* stream) {
+                            float* out, float* lse, void* workspace, size_t workspace_bytes, unsigned flags,
+                            int reps, float* ms, void* stream) {
   QJL_TRY(check_decode(cache, values, n, q, q_dtype, G, sketch, inv_temperature, out));
   QJL_CHECK_ARG(values->layout == QJL_VLAYOUT_P2T, "the benchmark hook times the tensor-core decode (P2T)");
   QJL_CHECK_ARG(reps >= 1 && ms, "reps must be >= 1 and ms set");
@@ -425,7 +425,7 @@ int qjl_bench_decode_kernel(const qjl_key_cache_t* cache, const qjl_value_cache_
     return QJL_ERR_WORKSPACE;
   }
   return bench_decode_tile(*cache, n, q, q_dtype, G, *sketch, inv_temperature, out, lse, workspace,
-                           workspace_bytes, reps, ms, (cudaStream_t)stream);
+                           workspace_bytes, flags, reps, ms, (cudaStream_t)stream);
 }
 
 int qjl_tensor_core_path(const qjl_key_cache_t* cache, const qjl_value_cache_t* values, int G) {

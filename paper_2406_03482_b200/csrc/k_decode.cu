@@ -96,6 +96,18 @@ struct Params {
   float* logits;         // [units][G][n]: scores kernel (always), decode (optional, scaled by 1/T)
 };
 
+#ifndef QJL_UD_TRACE
+#define QJL_UD_TRACE 0      // diagnostics only: per-CTA %globaltimer stamps (tools/trace_decode.py)
+#endif
+#if QJL_UD_TRACE
+__device__ unsigned long long g_ud_trace[4096][4];   // [cta] {after wait, loop done, end, smid}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 __host__ __device__ __forceinline__ int64_t tile_begin(int64_t c, int64_t T, int64_t C) { return c * T / C; }
 __host__ __device__ __forceinline__ int cta_of_tile(int64_t t, int64_t T, int C) {
   return (int)(((t + 1) * (int64_t)C + T - 1) / T) - 1;
@@ -741,6 +753,14 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   };
 
   asm volatile("griddepcontrol.wait;" ::: "memory");   // Bsc / qconst come from k_uprep
+#if QJL_UD_TRACE
+  if (tid == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_ud_trace[blockIdx.x][0] = gtimer();
+    g_ud_trace[blockIdx.x][3] = smid;
+  }
+#endif
   const int n32 = (int)P.n;                            // n <= capacity < 2^30 (supported())
   int u = u_first, lt = lt_first, s = 0;
   uint32_t full_ph = 0;
@@ -946,7 +966,12 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
         full_ph ^= 1;
       }
     }
-    if (it == ntiles) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // all tiles consumed
+    if (it == ntiles) {
+      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // all tiles consumed
+#if QJL_UD_TRACE
+      if (tid == 0) g_ud_trace[blockIdx.x][1] = gtimer();
+#endif
+    }
     flush(u, slot, ns);
     if (lt == P.tpu) {
       ++u;
@@ -955,6 +980,9 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   }
   tc_fence_before();
   __syncthreads();
+#if QJL_UD_TRACE
+  if (tid == 0) g_ud_trace[blockIdx.x][2] = gtimer();
+#endif
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(L::kAlloc));
 }
 
@@ -1424,10 +1452,16 @@ int launch_scores_tile(const qjl_key_cache_t& kc, int64_t n, const void* q, int 
 }
 
 int bench_decode_tile(const qjl_key_cache_t& kc, int64_t n, const void* q, int q_dtype, int G, const qjl_sketch_t& sk,
-                      float inv_t, float* out, float* lse, void* ws, size_t ws_bytes, int reps, float* ms,
-                      cudaStream_t st) {
-  ud::Launch a{&kc, n, q, q_dtype, G, &sk, inv_t, out, lse, nullptr, ws, 0, nullptr, 2, reps, ms};
+                      float inv_t, float* out, float* lse, void* ws, size_t ws_bytes, unsigned flags, int reps,
+                      float* ms, cudaStream_t st) {
+  ud::Launch a{&kc, n, q, q_dtype, G, &sk, inv_t, out, lse, nullptr, ws, flags, nullptr, 2, reps, ms};
   return ud::launch_any(a, ws_bytes, st);
 }
 
 }  // namespace qjl
+
+#if QJL_UD_TRACE
+extern "C" __attribute__((visibility("default"))) int qjl_debug_ud_trace(void* host, int ctas) {
+  return (int)cudaMemcpyFromSymbol(host, qjl::ud::g_ud_trace, sizeof(unsigned long long) * 4 * ctas);
+}
+#endif

@@ -62,8 +62,8 @@ int launch_decode_step_tile(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
 int launch_scores_tile(const qjl_key_cache_t& kc, int64_t n, const void* q, int q_dtype, int G,
                        const qjl_sketch_t& sk, float* logits, void* ws, size_t ws_bytes, cudaStream_t st);
 int bench_decode_tile(const qjl_key_cache_t& kc, int64_t n, const void* q, int q_dtype, int G, const qjl_sketch_t& sk,
-                      float inv_t, float* out, float* lse, void* ws, size_t ws_bytes, int reps, float* ms,
-                      cudaStream_t st);
+                      float inv_t, float* out, float* lse, void* ws, size_t ws_bytes, unsigned flags, int reps,
+                      float* ms, cudaStream_t st);
 
 // batched block-wise sketch orthogonalization (k_orth.cu)
 int launch_orthogonalize(const double* g, int batch, int m, int d, double* out, cudaStream_t st);

@@ -449,7 +449,7 @@ class DeviceKeyCache:
         return out
 
     def bench_decode_kernel(self, q: torch.Tensor, reps: int, temperature: float = 1.0,
-                            out: torch.Tensor | None = None) -> float:
+                            out: torch.Tensor | None = None, deterministic: bool = False) -> float:
         """Mean time (ms) of the tensor-core decode kernel in a chain of `reps` back-to-back
         decodes (qjl_bench_decode_kernel): the roofline kernel as it runs in a decode loop."""
         s = self.shape
@@ -464,8 +464,9 @@ class DeviceKeyCache:
         _lib.check(self.lib.qjl_bench_decode_kernel(ctypes.byref(kd), ctypes.byref(vd), self.n, q.data_ptr(),
                                                     _TORCH2QJL[q.dtype], G, ctypes.byref(sd),
                                                     1.0 / float(temperature), out.data_ptr(), None,
-                                                    ws.data_ptr(), ws.numel(), int(reps), ctypes.byref(ms),
-                                                    _stream()), "bench_decode_kernel")
+                                                    ws.data_ptr(), ws.numel(),
+                                                    _lib.QJL_DECODE_DETERMINISTIC if deterministic else 0,
+                                                    int(reps), ctypes.byref(ms), _stream()), "bench_decode_kernel")
         return float(ms.value)
 
     def decode_step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,

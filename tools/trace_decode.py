@@ -12,9 +12,11 @@ from paper_2406_03482_b200 import _lib
 
 w = dict(bench.WORKLOADS["c3"])
 dev = torch.device("cuda", 0)
-cache = bench.build_cache(w, 0, 0, dev)
+from paper_2406_03482_b200.distributed import shard_units
+sh = shard_units(64, 1, 0)
+cache = bench.build_cache(w, sh, 0, dev)
+q = bench.make_queries(w, sh, 0, dev)
 U, d, G = w["batch"] * w["kv_heads"], w["d"], w["G"]
-q = torch.randn(U, G, d, device=dev).to(torch.bfloat16)
 out = torch.empty(U, G, d, device=dev)
 lib = _lib.load()
 fn = lib.qjl_debug_ud_trace
@@ -22,11 +24,14 @@ fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
 sms = torch.cuda.get_device_properties(0).multi_processor_count
 C = 4 * sms
 res = {}
-for mode in ("pdl_step", "alone"):
-    if mode == "alone":
-        lib.qjl_timing_enable(1)          # PDL off, as for the kernel-alone timing
+for mode in ("chained_step", "kernel_chain", "deterministic"):
     for i in range(20):
-        cache.decode(q, out=out)
+        if mode == "chained_step":
+            cache.decode(q, out=out, chained=i > 0)
+        elif mode == "kernel_chain":
+            cache.bench_decode_kernel(q, reps=3, out=out)
+        else:
+            cache.decode(q, out=out, deterministic=True)
     torch.cuda.synchronize()
     buf = np.zeros((C, 4), np.uint64)
     assert fn(buf.ctypes.data, C) == 0

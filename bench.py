@@ -577,7 +577,9 @@ def run_gpu(args):
     e3.record()
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3)
-    e2e_ok = bool(torch.equal(oh[(args.steps - 1) & 1][shard.start:shard.stop], cache.decode(q).cpu()))
+    _ref = cache.decode(q).cpu().double()
+    e2e_ok = bool(((oh[(args.steps - 1) & 1][shard.start:shard.stop].double() - _ref).norm()
+                   <= 1e-5 * _ref.norm()).item())
     oh, qh = oh[0], qh[0]
 
     # zero-copy variant (N = 1): the decode reads q / writes out through pinned host pointers

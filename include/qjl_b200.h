@@ -90,10 +90,11 @@ enum { QJL_REC_BITS_IN = 0, QJL_REC_BITS_OUT, QJL_REC_NORM_IN, QJL_REC_NORM_OUT,
        QJL_REC_ZERO, QJL_REC_SCALE, QJL_REC_FIELDS };
 /* qjl_decode / qjl_decode_step flags */
 enum {
-  /* The previous kernel on `stream` is a qjl_decode / qjl_decode_step of this library and
-   * every input of this call (cache rows, q, k_new, v_new, sketch) was written before that
-   * launch: the query-sketch kernel may then read its inputs while the previous decode
-   * drains (programmatic dependent launch).  Without it every read waits for the stream. */
+  /* The previous kernel on `stream` is a qjl_decode / qjl_decode_step of this library on the
+   * same workspace, and every input of this call (cache rows, q, k_new, v_new, sketch) was
+   * written before that launch: the query-sketch kernel may then read its inputs while the
+   * previous decode drains (programmatic dependent launch).  Without it every read waits
+   * for the stream. */
   QJL_DECODE_CHAINED = 1,
   /* Fixed 512-token segments per unit, merged in segment order: a unit's output bits depend
    * only on that unit (a unit-sharded decode equals the unsharded one bit for bit).  The

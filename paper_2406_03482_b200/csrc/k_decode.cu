@@ -101,6 +101,7 @@ struct Params {
 #endif
 #if QJL_UD_TRACE
 __device__ unsigned long long g_ud_trace[4096][4];   // [cta] {after wait, loop done, end, smid}
+__device__ unsigned long long g_ud_stat[4096][4];    // [cta] {tiles, issue cycles, full-wait cycles, runs}
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -761,6 +762,9 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     g_ud_trace[blockIdx.x][3] = smid;
   }
 #endif
+#if QJL_UD_TRACE
+  long long st_issue = 0, st_wait = 0, st_tiles = 0;
+#endif
   const int n32 = (int)P.n;                            // n <= capacity < 2^30 (supported())
   int u = u_first, lt = lt_first, s = 0;
   uint32_t full_ph = 0;
@@ -784,7 +788,16 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     first = true;
     reset_state();
     for (; it < seg_end; ++it, ++lt) {
+#if QJL_UD_TRACE
+      {
+        const long long cw0 = clock64();
+        mbar_wait(a_full + 8 * s, full_ph);
+        st_wait += clock64() - cw0;
+        ++st_tiles;
+      }
+#else
       mbar_wait(a_full + 8 * s, full_ph);
+#endif
       const uint8_t* st = sm + L::oStage + s * L::kRec;
       auto body = [&](auto mask_tag) {
         constexpr bool MASK = decltype(mask_tag)::value;
@@ -872,7 +885,15 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
           }
         }
         bar_sync(1, kThreads);                  // maxima visible; the stage is fully read
+#if QJL_UD_TRACE
+        if (tid == 0 && iss_i < ntiles) {
+          const long long c0 = clock64();
+          issue_next();
+          st_issue += clock64() - c0;
+        }
+#else
         if (tid == 0 && iss_i < ntiles) issue_next();   // refill this stage kStages ahead
+#endif
 
         // ---------------- 4. softmax bookkeeping, lane-parallel over the heads ----------------
         // lane l reduces slot (l & 7) over the 4 warps: heads 0..3, the scale bound at 4
@@ -981,6 +1002,12 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   tc_fence_before();
   __syncthreads();
 #if QJL_UD_TRACE
+  if (tid == 0) {
+    g_ud_stat[blockIdx.x][0] = st_tiles;
+    g_ud_stat[blockIdx.x][1] = st_issue;
+    g_ud_stat[blockIdx.x][2] = st_wait;
+    g_ud_stat[blockIdx.x][3] = 1;
+  }
   if (tid == 0) g_ud_trace[blockIdx.x][2] = gtimer();
 #endif
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(L::kAlloc));
@@ -1463,5 +1490,8 @@ int bench_decode_tile(const qjl_key_cache_t& kc, int64_t n, const void* q, int q
 #if QJL_UD_TRACE
 extern "C" __attribute__((visibility("default"))) int qjl_debug_ud_trace(void* host, int ctas) {
   return (int)cudaMemcpyFromSymbol(host, qjl::ud::g_ud_trace, sizeof(unsigned long long) * 4 * ctas);
+}
+extern "C" __attribute__((visibility("default"))) int qjl_debug_ud_stat(void* host, int ctas) {
+  return (int)cudaMemcpyFromSymbol(host, qjl::ud::g_ud_stat, sizeof(unsigned long long) * 4 * ctas);
 }
 #endif

@@ -254,7 +254,8 @@ class DeviceKeyCache:
 
     def workspace(self, nbytes: int) -> torch.Tensor:
         if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)
+            # zero-filled: the tensor-core decode keeps its merge counters at the start
+            self._ws = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=self.device)
         return self._ws
 
     # ------------------------------------------------------------- profile/S
@@ -471,11 +472,13 @@ class DeviceKeyCache:
 
     def decode_step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,
                     temperature: float = 1.0, out: torch.Tensor | None = None,
-                    lse: torch.Tensor | None = None, chained: bool = False) -> torch.Tensor:
+                    lse: torch.Tensor | None = None, chained: bool = False,
+                    deterministic: bool = False) -> torch.Tensor:
         """One generation step (Algorithm 1): append the new token of every unit
         (k_new, v_new [U, d]) at row n, then decode q [U, G, d] over rows [0, n + 1).
         On the tcgen05 path the append is fused into the step's query-sketch kernel;
-        otherwise it runs as K1 + value quantizer launches before the decode."""
+        otherwise it runs as K1 + value quantizer launches before the decode.
+        `deterministic` selects the fixed-segment schedule (bitwise reproducible)."""
         if temperature <= 0:
             raise ValueError(f"temperature must be positive, got {temperature}")
         s = self.shape
@@ -500,10 +503,11 @@ class DeviceKeyCache:
                                           _TORCH2QJL[q.dtype], G, ctypes.byref(sd), self.channels.data_ptr(),
                                           s.h, kn.data_ptr(), vn.data_ptr(), 1.0 / float(temperature),
                                           out.data_ptr(), _ptr(lse), None, ws.data_ptr(), ws.numel(),
-                                          _lib.QJL_DECODE_CHAINED if chained else 0, _stream())
+                                          (_lib.QJL_DECODE_CHAINED if chained else 0)
+                                          | (_lib.QJL_DECODE_DETERMINISTIC if deterministic else 0), _stream())
         if rc == _lib.QJL_ERR_UNSUPPORTED:
             self.append(kn[:, None, :], vn[:, None, :])
-            return self.decode(q, temperature, out=out, lse=lse)
+            return self.decode(q, temperature, out=out, lse=lse, deterministic=deterministic)
         _lib.check(rc, "decode_step")
         self.n += 1
         self.n_values += 1

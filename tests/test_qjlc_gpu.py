@@ -141,7 +141,7 @@ def test_batched_save_matches_oracle_and_load_round_trips(cuda, tmp_path):
     assert torch.equal(c2.channels.cpu(), c.channels.cpu())
     assert torch.equal(c2.s_full.cpu(), c.s_full.cpu())
     q = torch.randn(U, 4, 128, device="cuda").to(torch.bfloat16)
-    assert torch.equal(c.decode(q), c2.decode(q))
+    assert torch.equal(c.decode(q, deterministic=True), c2.decode(q, deterministic=True))
     # idempotent: saving the loaded cache gives the same files
     paths2 = [tmp_path / f"v{u}.qjlc" for u in range(U)]
     Q.save(c2, paths2)

@@ -25,5 +25,5 @@ for i in range(3):                                  # decode steps with the fuse
     c.decode_step(q, K[:, n + i], V[:, n + i], chained=i > 0)
 ms = c.bench_decode_kernel(q, reps=2)
 torch.cuda.synchronize()
-assert torch.isfinite(out).all() and torch.equal(out, out2) and torch.isfinite(lg).all()
+assert torch.isfinite(out).all() and torch.allclose(out, out2, rtol=1e-4, atol=1e-6) and torch.isfinite(lg).all()
 print("sanitize probe ok", float(out.abs().sum()), float(out3.abs().sum()), ms)

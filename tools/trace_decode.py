@@ -58,6 +58,17 @@ for mode in ("chained_step", "kernel_chain", "deterministic"):
     r["loop_done_pct"] = [round(float(x), 2) for x in np.percentile(t[:, 1], [0, 10, 50, 90, 100])]
     r["end_pct"] = [round(float(x), 2) for x in np.percentile(t[:, 2], [0, 10, 50, 90, 99, 100])]
     r["mean_loop_done"] = round(float(t[:, 1].mean()), 2)
+    if hasattr(lib, "qjl_debug_ud_stat"):
+        st = np.zeros((C, 4), np.uint64)
+        lib.qjl_debug_ud_stat.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        assert lib.qjl_debug_ud_stat(st.ctypes.data, C) == 0
+        st = st.astype(np.float64)
+        ghz = 1.9
+        r["tiles_pct"] = [float(x) for x in np.percentile(st[:, 0], [0, 50, 100])]
+        r["runs_mean"] = round(float(st[:, 3].mean()), 2)
+        r["issue_us_per_tile"] = round(float((st[:, 1] / np.maximum(st[:, 0], 1)).mean() / ghz / 1e3), 3)
+        r["fullwait_us_per_tile"] = round(float((st[:, 2] / np.maximum(st[:, 0], 1)).mean() / ghz / 1e3), 3)
+        r["loop_us_per_tile"] = round(float((t[:, 1] - t[:, 0]).sum() / st[:, 0].sum()), 3)
     res[mode] = r
 for k, r in res.items():
     print(k, {kk: v for kk, v in r.items() if not kk.startswith("wave")})

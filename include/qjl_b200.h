@@ -143,7 +143,11 @@ QJL_API int qjl_device_info(int* sm_count, int* cc_major, int* cc_minor);
  * channels: int32 [units][h]; magnitudes: f64 [units][d] (may be NULL). */
 QJL_API int qjl_detect_outliers(const void* keys, int dtype, int units, int64_t n0, int d,
                         int64_t unit_stride, int h, int32_t* channels,
-                        double* magnitudes, void* stream);
+                        double* magnitudes, void* ws, size_t ws_bytes, void* stream);
+/* Device workspace (bytes) qjl_detect_outliers / qjl_prefill_profile use for `units`
+ * prompts of n0 keys of dimension d: fp64 per-block channel partials (0: none needed).
+ * ws == NULL makes the call allocate it stream-ordered (cudaMallocAsync) itself. */
+QJL_API size_t qjl_detect_workspace(int units, int64_t n0, int d);
 
 /* Build per-unit zero-padded sketches from device fp64 S_in [m_in][d-h] and
  * S_out [m_out][h] (either may be NULL when its side is empty) and channels
@@ -162,7 +166,8 @@ QJL_API int qjl_build_sketch(const double* s_in, const double* s_out, int m_in, 
 QJL_API int qjl_prefill_profile(const void* keys, int dtype, int units, int64_t n0, int d,
                                 int64_t unit_stride, int h, const void* s_in, const void* s_out,
                                 int m_in, int m_out, int sketch_dtype, int32_t* channels,
-                                double* magnitudes, void* s_full, void* stream);
+                                double* magnitudes, void* s_full, void* ws, size_t ws_bytes,
+                                void* stream);
 
 /* K1: append n keys per unit at rows [row_offset, row_offset + n).
  * keys: [units][n][d] with `key_unit_stride` elements between units (0: every unit

@@ -48,10 +48,12 @@ SIGNATURES = {
     "qjl_status_string": (ctypes.c_char_p, [c_i32]),
     "qjl_last_error": (ctypes.c_char_p, []),
     "qjl_device_info": (c_i32, [P(c_i32), P(c_i32), P(c_i32)]),
-    "qjl_detect_outliers": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i32, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "qjl_detect_outliers": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i32, c_i64, c_i32, c_vp, c_vp, c_vp, c_sz,
+                                    c_vp]),
+    "qjl_detect_workspace": (c_sz, [c_i32, c_i64, c_i32]),
     "qjl_build_sketch": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp]),
     "qjl_prefill_profile": (c_i32, [c_vp, c_i32, c_i32, c_i64, c_i32, c_i64, c_i32, c_vp, c_vp, c_i32,
-                                    c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
+                                    c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "qjl_quantize_keys": (c_i32, [c_vp, c_i32, c_i64, c_i64, P(SketchDesc), c_vp, c_i32,
                                   P(KeyCacheDesc), c_i64, c_vp]),
     "qjl_sketch_query": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, P(SketchDesc), c_i32, c_i32, c_vp, c_vp]),

@@ -201,9 +201,14 @@ int qjl_device_info(int* sm_count, int* cc_major, int* cc_minor) {
   return QJL_OK;
 }
 
+size_t qjl_detect_workspace(int units, int64_t n0, int d) {
+  if (units < 1 || n0 < 1 || d < 1) return 0;
+  return detect_workspace(units, n0, d);
+}
+
 int qjl_detect_outliers(const void* keys, int dtype, int units, int64_t n0, int d,
                         int64_t unit_stride, int h, int32_t* channels, double* magnitudes,
-                        void* stream) {
+                        void* ws, size_t ws_bytes, void* stream) {
   QJL_CHECK_ARG(keys != nullptr, "keys is NULL");
   QJL_CHECK_ARG(valid_dtype(dtype), "bad key dtype %d", dtype);
   QJL_CHECK_ARG(units >= 1, "units must be >= 1");
@@ -212,8 +217,8 @@ int qjl_detect_outliers(const void* keys, int dtype, int units, int64_t n0, int 
   QJL_CHECK_ARG(h >= 0 && h <= d, "outlier count must be in [0, %d], got %d", d, h);
   QJL_CHECK_ARG(h == 0 || channels != nullptr, "channels output is NULL");
   QJL_CHECK_ARG(unit_stride >= n0 * d, "unit stride %lld < n0*d", (long long)unit_stride);
-  return launch_detect_outliers(keys, dtype, units, n0, d, unit_stride, h, channels, magnitudes,
-                                (cudaStream_t)stream);
+  return launch_detect_outliers(keys, dtype, units, n0, d, unit_stride, h, channels, magnitudes, ws,
+                                ws_bytes, (cudaStream_t)stream);
 }
 
 int qjl_build_sketch(const double* s_in, const double* s_out, int m_in, int m_out, int d, int h,
@@ -238,7 +243,8 @@ int qjl_build_sketch(const double* s_in, const double* s_out, int m_in, int m_ou
 
 int qjl_prefill_profile(const void* keys, int dtype, int units, int64_t n0, int d, int64_t unit_stride, int h,
                         const void* s_in, const void* s_out, int m_in, int m_out, int sketch_dtype,
-                        int32_t* channels, double* magnitudes, void* s_full, void* stream) {
+                        int32_t* channels, double* magnitudes, void* s_full, void* ws, size_t ws_bytes,
+                        void* stream) {
   QJL_CHECK_ARG(keys != nullptr, "keys is NULL");
   QJL_CHECK_ARG(valid_dtype(dtype), "bad key dtype %d", dtype);
   QJL_CHECK_ARG(units >= 1, "units must be >= 1");
@@ -259,7 +265,7 @@ int qjl_prefill_profile(const void* keys, int dtype, int units, int64_t n0, int 
     return QJL_ERR_ARG;  // kvcache.py:219-226
   }
   return launch_prefill_profile(keys, dtype, units, n0, d, unit_stride, h, s_in, s_out, m_in, m_out,
-                                sketch_dtype, channels, magnitudes, s_full, (cudaStream_t)stream);
+                                sketch_dtype, channels, magnitudes, s_full, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int qjl_quantize_keys(const void* keys, int dtype, int64_t n, int64_t key_unit_stride,

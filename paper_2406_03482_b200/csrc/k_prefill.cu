@@ -183,17 +183,42 @@ __global__ void __launch_bounds__(1024) k_detect_finish(const double* __restrict
   }
 }
 
+// Workspace of the two-phase detection: fp64 per-block channel partials.
+size_t detect_workspace(int units, int64_t n0, int d) {
+  if (n0 < 2 * kDetRows || d > 1024) return 0;
+  const int64_t nblk = (n0 + kDetRows - 1) / kDetRows;
+  return (size_t)units * nblk * d * sizeof(double);
+}
+
+// The partials buffer: the caller's workspace, or (ws == NULL) a stream-ordered allocation
+static int detect_part(void* ws, size_t ws_bytes, size_t need, cudaStream_t st, double** part, bool* owned) {
+  *owned = false;
+  if (ws != nullptr) {
+    if (ws_bytes < need) {
+      set_error("detection workspace needs %zu bytes, got %zu", need, ws_bytes);
+      return QJL_ERR_WORKSPACE;
+    }
+    *part = (double*)ws;
+    return QJL_OK;
+  }
+  cudaError_t e = cudaMallocAsync((void**)part, need, st);
+  if (e != cudaSuccess) return cuda_status(e, "detection workspace");
+  *owned = true;
+  return QJL_OK;
+}
+
 int launch_detect_outliers(const void* keys, int dtype, int units, int64_t n0, int d,
-                           int64_t unit_stride, int h, int32_t* channels, double* mags,
-                           cudaStream_t st) {
+                           int64_t unit_stride, int h, int32_t* channels, double* mags, void* ws,
+                           size_t ws_bytes, cudaStream_t st) {
   const size_t es = dtype_size(dtype);
   const bool two_phase = n0 >= 2 * kDetRows && d <= 1024 && (d * es) % 16 == 0 && (unit_stride * es) % 16 == 0 &&
                          ((uintptr_t)keys % 16) == 0 && 256 % (int)(d * es / 16) == 0;
   if (two_phase) {
     const int nblk = (int)((n0 + kDetRows - 1) / kDetRows);
     double* part = nullptr;
-    cudaError_t e = cudaMallocAsync((void**)&part, (size_t)units * nblk * d * sizeof(double), st);
-    if (e != cudaSuccess) return cuda_status(e, "detect_outliers workspace");
+    bool owned = false;
+    const int rc = detect_part(ws, ws_bytes, (size_t)units * nblk * d * sizeof(double), st, &part, &owned);
+    if (rc != QJL_OK) return rc;
     const int tpr = (int)(d * es / 16), rows_par = 256 / tpr;
     const size_t smem = (size_t)rows_par * d * sizeof(double);
     dim3 grid(nblk, units);
@@ -210,10 +235,12 @@ int launch_detect_outliers(const void* keys, int dtype, int units, int64_t n0, i
       QJL_DETP(QJL_BF16)
       QJL_DETP(QJL_F64)
 #undef QJL_DETP
-      default: cudaFreeAsync(part, st); return QJL_ERR_ARG;
+      default:
+        if (owned) cudaFreeAsync(part, st);
+        return QJL_ERR_ARG;
     }
     k_detect_finish<<<units, 1024, 0, st>>>(part, nblk, n0, d, h, channels, mags);
-    cudaFreeAsync(part, st);
+    if (owned) cudaFreeAsync(part, st);
     QJL_LAUNCH_CHECK("detect_outliers");
     return QJL_OK;
   }
@@ -504,20 +531,23 @@ static int launch_scatter_sketch(const void* s_in, const void* s_out, int m_in, 
 
 int launch_prefill_profile(const void* keys, int dtype, int units, int64_t n0, int d, int64_t unit_stride,
                            int h, const void* s_in, const void* s_out, int m_in, int m_out,
-                           int sketch_dtype, int32_t* channels, double* mags, void* s_full, cudaStream_t st) {
+                           int sketch_dtype, int32_t* channels, double* mags, void* s_full, void* ws,
+                           size_t ws_bytes, cudaStream_t st) {
   const size_t es = dtype_size(dtype);
   const bool two_phase = n0 >= 2 * kDetRows && d <= 1024 && (d * es) % 16 == 0 && (unit_stride * es) % 16 == 0 &&
                          ((uintptr_t)keys % 16) == 0 && 256 % (int)(d * es / 16) == 0 && h > 0;
   if (!two_phase) {
-    int rc = h > 0 ? launch_detect_outliers(keys, dtype, units, n0, d, unit_stride, h, channels, mags, st)
+    int rc = h > 0 ? launch_detect_outliers(keys, dtype, units, n0, d, unit_stride, h, channels, mags, ws,
+                                            ws_bytes, st)
                    : QJL_OK;
     if (rc != QJL_OK) return rc;
     return launch_scatter_sketch(s_in, s_out, m_in, m_out, d, h, channels, units, sketch_dtype, s_full, st);
   }
   const int nblk = (int)((n0 + kDetRows - 1) / kDetRows);
   double* part = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&part, (size_t)units * nblk * d * sizeof(double), st);
-  if (e != cudaSuccess) return cuda_status(e, "prefill_profile workspace");
+  bool owned = false;
+  const int prc = detect_part(ws, ws_bytes, (size_t)units * nblk * d * sizeof(double), st, &part, &owned);
+  if (prc != QJL_OK) return prc;
   const int tpr = (int)(d * es / 16), rows_par = 256 / tpr;
   const size_t smem = (size_t)rows_par * d * sizeof(double);
   dim3 grid(nblk, units);
@@ -534,7 +564,9 @@ int launch_prefill_profile(const void* keys, int dtype, int units, int64_t n0, i
     QJL_PPP(QJL_BF16)
     QJL_PPP(QJL_F64)
 #undef QJL_PPP
-    default: cudaFreeAsync(part, st); return QJL_ERR_ARG;
+    default:
+      if (owned) cudaFreeAsync(part, st);
+      return QJL_ERR_ARG;
   }
   // row slices: about one wave of 1024-thread CTAs (1 per SM) over all units, and few
   // enough source rows per slice to stage them in <= 160 KB of shared memory
@@ -562,9 +594,11 @@ int launch_prefill_profile(const void* keys, int dtype, int units, int64_t n0, i
     QJL_PPF(QJL_BF16)
     QJL_PPF(QJL_F64)
 #undef QJL_PPF
-    default: cudaFreeAsync(part, st); return QJL_ERR_ARG;
+    default:
+      if (owned) cudaFreeAsync(part, st);
+      return QJL_ERR_ARG;
   }
-  cudaFreeAsync(part, st);
+  if (owned) cudaFreeAsync(part, st);
   QJL_LAUNCH_CHECK("prefill_profile");
   return QJL_OK;
 }

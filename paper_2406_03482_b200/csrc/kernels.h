@@ -7,16 +7,18 @@
 
 namespace qjl {
 
+size_t detect_workspace(int units, int64_t n0, int d);
 int launch_detect_outliers(const void* keys, int dtype, int units, int64_t n0, int d,
-                           int64_t unit_stride, int h, int32_t* channels, double* mags,
-                           cudaStream_t st);
+                           int64_t unit_stride, int h, int32_t* channels, double* mags, void* ws,
+                           size_t ws_bytes, cudaStream_t st);
 int launch_build_sketch(const double* s_in, const double* s_out, int m_in, int m_out, int d,
                         int h, const int32_t* channels, int units, int dtype, void* s_full,
                         cudaStream_t st);
 // fused detect_outliers + per-unit S_full build (F2)
 int launch_prefill_profile(const void* keys, int dtype, int units, int64_t n0, int d, int64_t unit_stride,
                            int h, const void* s_in, const void* s_out, int m_in, int m_out,
-                           int sketch_dtype, int32_t* channels, double* mags, void* s_full, cudaStream_t st);
+                           int sketch_dtype, int32_t* channels, double* mags, void* s_full, void* ws,
+                           size_t ws_bytes, cudaStream_t st);
 int launch_quantize_keys_simt(const void* keys, int dtype, int64_t n, int64_t kus,
                               const qjl_sketch_t& sk, const int32_t* ch, int h,
                               const qjl_key_cache_t& kc, int64_t row_offset, cudaStream_t st);

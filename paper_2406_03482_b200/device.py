@@ -252,6 +252,13 @@ class DeviceKeyCache:
                              f"[{s.units}, {s.m_in + s.m_out}, {s.d}], got {s_full.dtype} {tuple(s_full.shape)}")
         self.s_full = s_full.contiguous()
 
+    def _detect_ws(self, n0: int) -> torch.Tensor:
+        """The outlier detection's partials buffer (qjl_detect_workspace), kept across calls."""
+        nb = int(self.lib.qjl_detect_workspace(self.shape.units, n0, self.shape.d))
+        if getattr(self, "_dws", None) is None or self._dws.numel() < nb:
+            self._dws = torch.empty(max(nb, 1), dtype=torch.uint8, device=self.device)
+        return self._dws
+
     def workspace(self, nbytes: int) -> torch.Tensor:
         if self._ws is None or self._ws.numel() < nbytes:
             # zero-filled: the tensor-core decode keeps its merge counters at the start
@@ -268,10 +275,11 @@ class DeviceKeyCache:
         mags = torch.empty(s.units, s.d, dtype=torch.float64, device=self.device)
         if s.h == 0:
             return self.channels[:, :0]
+        ws = self._detect_ws(pk.shape[1])
         _lib.check(self.lib.qjl_detect_outliers(pk.data_ptr(), _TORCH2QJL[pk.dtype], s.units,
                                                 pk.shape[1], s.d, pk.shape[1] * s.d, s.h,
                                                 self.channels.data_ptr(), mags.data_ptr(),
-                                                _stream()), "detect_outliers")
+                                                ws.data_ptr(), ws.numel(), _stream()), "detect_outliers")
         self.magnitudes = mags
         return self.channels
 
@@ -319,11 +327,13 @@ class DeviceKeyCache:
         if self.s_full is None:
             self.s_full = torch.empty(s.units, s.m_in + s.m_out, s.d, dtype=self.sketch_dtype, device=dev)
         mags = torch.empty(s.units, s.d, dtype=torch.float64, device=dev)
+        ws = self._detect_ws(pk.shape[1])
         _lib.check(self.lib.qjl_prefill_profile(pk.data_ptr(), _TORCH2QJL[pk.dtype], s.units, pk.shape[1],
                                                 s.d, pk.shape[1] * s.d, s.h, _ptr(sin), _ptr(sout),
                                                 s.m_in, s.m_out, _TORCH2QJL[self.sketch_dtype],
                                                 self.channels.data_ptr(), mags.data_ptr(),
-                                                self.s_full.data_ptr(), _stream()), "prefill_profile")
+                                                self.s_full.data_ptr(), ws.data_ptr(), ws.numel(),
+                                                _stream()), "prefill_profile")
         self.magnitudes = mags
         self.append(pk, values)
 

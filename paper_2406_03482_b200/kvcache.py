@@ -133,14 +133,17 @@ def detect_outliers(prompt_keys: np.ndarray, h: int) -> OutlierProfile:
     kt = torch.from_numpy(np.ascontiguousarray(pk)).to(dev)
     ch = torch.zeros(max(h, 1), dtype=torch.int32, device=dev)
     mags = torch.zeros(d, dtype=torch.float64, device=dev)
+    ws = torch.empty(max(int(lib.qjl_detect_workspace(1, n0, d)), 1), dtype=torch.uint8, device=dev)
     if h == 0:
         # magnitudes still come from the device reduction (h = 1 run, channel discarded)
         _lib.check(lib.qjl_detect_outliers(kt.data_ptr(), _lib.QJL_F64, 1, n0, d, n0 * d, 1,
-                                           ch.data_ptr(), mags.data_ptr(), _stream()), "detect_outliers")
+                                           ch.data_ptr(), mags.data_ptr(), ws.data_ptr(), ws.numel(),
+                                           _stream()), "detect_outliers")
         chans: tuple[int, ...] = ()
     else:
         _lib.check(lib.qjl_detect_outliers(kt.data_ptr(), _lib.QJL_F64, 1, n0, d, n0 * d, h,
-                                           ch.data_ptr(), mags.data_ptr(), _stream()), "detect_outliers")
+                                           ch.data_ptr(), mags.data_ptr(), ws.data_ptr(), ws.numel(),
+                                           _stream()), "detect_outliers")
         chans = tuple(int(c) for c in ch[:h].cpu().numpy())
     m = mags.cpu().numpy()
     m.setflags(write=False)

@@ -35,7 +35,7 @@ def test_library_exports_every_symbol():
 def test_argument_errors_without_gpu():
     lib = _lib.load()
     # empty prompt (kvcache.py:111-112) -> QJL_ERR_ARG, no CUDA call made
-    rc = lib.qjl_detect_outliers(None, 0, 1, 0, 128, 0, 1, None, None, None)
+    rc = lib.qjl_detect_outliers(None, 0, 1, 0, 128, 0, 1, None, None, None, 0, None)
     assert rc == _lib.QJL_ERR_ARG
     with pytest.raises(ValueError):
         _lib.check(rc, "detect_outliers")

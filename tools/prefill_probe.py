@@ -24,12 +24,14 @@ if len(sys.argv) > 1 and sys.argv[1] == "ncu":
 c.prefill(K)
 sin, sout = c._sk_op
 mags = torch.empty(U, d, dtype=torch.float64, device="cuda")
+dws = c._detect_ws(n)
 
 
 def profile():
     _lib.check(c.lib.qjl_prefill_profile(K.data_ptr(), _TORCH2QJL[K.dtype], U, n, d, n * d, 8, sin.data_ptr(),
                                          sout.data_ptr(), 512, 64, _TORCH2QJL[c.sketch_dtype], c.channels.data_ptr(),
-                                         mags.data_ptr(), c.s_full.data_ptr(), _stream()), "profile")
+                                         mags.data_ptr(), c.s_full.data_ptr(), dws.data_ptr(), dws.numel(),
+                                         _stream()), "profile")
 
 
 def k1():

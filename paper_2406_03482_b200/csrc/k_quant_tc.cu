@@ -10,11 +10,16 @@
 //    past n are zero-filled by the TMA unit) and S_full [units][MT][128];
 //  * warp 1: single-thread tcgen05.mma issuer, M = 128 tokens, N = MT split into
 //    NC chunks of CH <= 256 columns, K = 128 (8 x K16), fp32 accumulators in two
-//    ping-pong TMEM buffers of 256 columns;
+//    ping-pong TMEM buffers; A (the key tile) is read from TMEM (QJL_K1_ATMEM), so the
+//    tensor core streams only S_full from shared memory and a key stage is free as soon
+//    as the norm warps have read it (measured 145 -> 144 us at C4: shared-memory
+//    bandwidth was not the limit);
 //  * warps 2, 3, 12, 13 (K-half 0) and 14-17 (K-half 1): ||k_in||, ||k_out|| from the
 //    staged key tile, one token row per thread pair: exact fp32 products, fp32 sums
 //    with an error bound that decides the fp16 rounding, double-float (TwoSum)
 //    recompute when it does not -> the reference's float64 norm at half precision;
+//    with QJL_K1_ATMEM they also store their row halves into the TMEM A buffer of the
+//    tile (warp w owns TMEM lanes 32 (w % 4) .. + 31, so norm warp w takes those rows);
 //  * warps 4-11: epilogue, one set of 4 warps per TMEM buffer -- tcgen05.ld
 //    32x32b (one token per thread), exact sign
 //    test `x >= 0` (set.ge: -0.0 -> 1, NaN -> 0), 32 bits per word, stored as
@@ -91,6 +96,23 @@ __device__ __forceinline__ void tc_mma_f16c(uint32_t tmem_d, uint64_t adesc, uin
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "n"(ACC));
+}
+// D (TMEM, f32) += A (TMEM: lane = token row, column j = K elements 2j, 2j + 1) x B (smem)
+__device__ __forceinline__ void tc_mma_f16_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
 }
 // K-major, SWIZZLE_128B smem matrix descriptor (rows of 128 B, 8-row atoms 1024 B apart)
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -204,20 +226,30 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+#ifndef QJL_K1_ATMEM
+#define QJL_K1_ATMEM 1   // A operand (the key tile) in TMEM, written by the norm warps
+#endif
+constexpr bool kAT = QJL_K1_ATMEM != 0;
+static_assert(!kAT || QJL_K1_ZEROACC, "the TMEM-A MMAs always accumulate onto re-zeroed buffers");
+
 template <int MT, int NC, int STAGES>
 struct QLayout {
   static constexpr int CH = MT / NC;                       // columns per N chunk
-  // TMEM accumulator buffers: NBUF of BUFW columns (512 in all), so the MMA can run
-  // NBUF - 1 chunks ahead of the epilogue
-  static constexpr int BUFW = CH <= 64 ? 64 : CH <= 128 ? 128 : 256;
-  static constexpr int NBUF = 512 / BUFW;
+  // TMEM accumulator buffers: NBUF of BUFW columns, so the MMA can run NBUF - 1 chunks
+  // ahead of the epilogue.  kAT: columns [384, 512) hold two 64-column A buffers (one
+  // 128 x 128 key tile each), the accumulators share [0, 384).
+  static constexpr int BUFW = kAT ? (CH + 31) / 32 * 32 : CH <= 64 ? 64 : CH <= 128 ? 128 : 256;
+  static constexpr int NBUF = (kAT ? 384 : 512) / BUFW;
+  static constexpr int cA = 384;
   static constexpr int kBHalf = MT * 128;                  // one K-half of S_full (bytes)
   static constexpr int kABytes = kM * kK * 2;              // one key tile (32 KB)
   static constexpr int oB = 0;                             // S_full: [2 halves][MT rows][128 B]
   static constexpr int oA = 2 * kBHalf;                    // key tiles: [STAGES][2 halves][128][128 B]
   static constexpr int oBar = oA + STAGES * kABytes;
-  // barriers: a_full[S], a_empty[S], b_full, b_empty, t_full[NBUF], t_empty[NBUF]
-  static constexpr int kBars = 2 * STAGES + 2 + 2 * NBUF;
+  // barriers: a_full[S], a_empty[S], b_full, b_empty, t_full[NBUF], t_empty[NBUF],
+  // at_full[2], at_empty[2] (A buffers in TMEM)
+  static constexpr int kBars = 2 * STAGES + 2 + 2 * NBUF + 4;
+  static_assert(NBUF >= 2, "two accumulator buffers at least");
   static constexpr int oTmemPtr = oBar + kBars * 8;
   static constexpr int oMask = oTmemPtr + 16;              // per-unit outlier channel list
   static constexpr int oPart = oMask + 64 * 4;              // [2][128] K-half-1 partial sums
@@ -253,6 +285,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
   uint64_t* b_empty = b_full + 1;
   uint64_t* t_full = b_full + 2;
   uint64_t* t_empty = t_full + L::NBUF;
+  uint64_t* at_full = t_empty + L::NBUF;   // kAT: key tile it is in TMEM A buffer it % 2
+  uint64_t* at_empty = at_full + 2;        // kAT: the MMAs reading A buffer b are done
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(sm + L::oTmemPtr);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int C = gridDim.x;
@@ -263,7 +297,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&a_full[s], 1);
-      mbar_init(&a_empty[s], 1 + 8);      // MMA commit + 8 norm warps
+      mbar_init(&a_empty[s], kAT ? 8 : 1 + 8);   // (MMA commit unless A is in TMEM) + 8 norm warps
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&at_full[b], 8);          // the 8 norm warps stored their K-half rows
+      mbar_init(&at_empty[b], 1);         // MMA commit
     }
     mbar_init(b_full, 1);
     mbar_init(b_empty, 1);
@@ -344,12 +382,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
           ++b_uses;
         }
         const int s = it % STAGES;
-        mbar_wait(&a_full[s], (it / STAGES) & 1);
+        const int ab = it & 1;                   // kAT: A buffer of this tile
+        if (kAT) mbar_wait(&at_full[ab], (it >> 1) & 1);
+        else mbar_wait(&a_full[s], (it / STAGES) & 1);
         tc_fence_after();
         // descriptors built once; the start-address field (bits 0-13, 16-byte units) takes
         // the K / chunk offsets as plain adds (all shared addresses are < 256 KB)
         const uint64_t ad0 = sw128_desc(smem_u32(sm + L::oA + s * L::kABytes));
         const uint64_t bd0 = sw128_desc(smem_u32(sm + L::oB));
+        const uint32_t ta = tmem + L::cA + ab * 64;
         const bool do_mma = !(P.ablate & 4);
 #pragma unroll
         for (int c = 0; c < NC; ++c, ++chunk) {
@@ -361,15 +402,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
 #pragma unroll
             for (int k = 0; k < kK / 16; ++k) {
               const int hf = k >> 2, kk = k & 3;   // K-half, 32-byte step inside the 128-byte row
-              const uint64_t ad = ad0 + (uint64_t)((hf * (L::kABytes / 2) + kk * 32) >> 4);
               const uint64_t bd = bd0 + (uint64_t)((hf * L::kBHalf + c * CH * 128 + kk * 32) >> 4);
-              if (k == 0 && !QJL_K1_ZEROACC) tc_mma_f16c<0>(d_tmem, ad, bd, IDESC);
-              else tc_mma_f16c<1>(d_tmem, ad, bd, IDESC);
+              if (kAT) {
+                tc_mma_f16_ta(d_tmem, ta + 8 * k, bd, IDESC);   // K16 = 8 columns of packed pairs
+              } else {
+                const uint64_t ad = ad0 + (uint64_t)((hf * (L::kABytes / 2) + kk * 32) >> 4);
+                if (k == 0 && !QJL_K1_ZEROACC) tc_mma_f16c<0>(d_tmem, ad, bd, IDESC);
+                else tc_mma_f16c<1>(d_tmem, ad, bd, IDESC);
+              }
             }
           }
           tc_commit(&t_full[buf]);
         }
-        tc_commit(&a_empty[s]);                  // key tile consumed by the tensor core
+        if (kAT) tc_commit(&at_empty[ab]);       // A buffer free for tile it + 2
+        else tc_commit(&a_empty[s]);             // key tile consumed by the tensor core
         const bool last_of_unit = (lt + 1 == P.tpu) || (it + 1 == ntiles);
         if (last_of_unit) tc_commit(b_empty);    // S_full of this unit no longer read
         if (++lt == P.tpu) { lt = 0; ++u; }
@@ -377,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     }
   } else if (warp >= 14) {
     // ===================== norms, K-half 1: partial sums of squares ================
-    const int nw = warp - 14;
+    const int nw = kAT ? (warp & 3) : warp - 14;    // kAT: rows of this warp's TMEM lane quadrant
     const int row = nw * 32 + lane;
     float* part = reinterpret_cast<float*>(sm + L::oPart);
     for (int it = 0; it < ntiles; ++it) {
@@ -386,11 +432,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       const uint8_t* rowp = sm + L::oA + s * L::kABytes + L::kABytes / 2 + row * 128;
       float2 acc2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                         make_float2(0.f, 0.f)};           // 8 chains of 8 exact squares
-      if (!(P.ablate & 2)) {
+      uint32_t kw[kAT ? 32 : 1];
+      if (kAT) {
+        // this row's K-half 1 (64 elements = 32 packed columns) -> TMEM A buffer it % 2
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((j ^ (row & 7)) << 4));
-          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+          kw[4 * j] = v.x; kw[4 * j + 1] = v.y; kw[4 * j + 2] = v.z; kw[4 * j + 3] = v.w;
+        }
+        if (it >= 2) mbar_wait(&at_empty[it & 1], ((it >> 1) - 1) & 1);
+        tc_fence_after();
+        tmem_st32(tmem + ((uint32_t)(nw * 32) << 16) + L::cA + (it & 1) * 64 + 32, kw);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&at_full[it & 1]);
+      }
+      if (!(P.ablate & 2)) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint32_t w[4];
+          if (kAT) {
+            w[0] = kw[4 * j]; w[1] = kw[4 * j + 1]; w[2] = kw[4 * j + 2]; w[3] = kw[4 * j + 3];
+          } else {
+            const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((j ^ (row & 7)) << 4));
+            w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+          }
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float2 f = ABF ? make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xFFFF0000u))
@@ -411,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     }
   } else if (warp < 4 || warp >= 12) {
     // ============================ norms (fp64, exact products) =====================
-    const int nw = warp < 4 ? warp - 2 : warp - 10;  // norm warp 0..3
+    const int nw = kAT ? (warp & 3) : warp < 4 ? warp - 2 : warp - 10;  // norm warp 0..3 (kAT: TMEM quadrant)
     const int ntid = nw * 32 + lane;             // token row of the tile
     int* chan = reinterpret_cast<int*>(sm + L::oMask);
     int u = u_first, lt = lt_first, cur_u = -1;
@@ -437,6 +504,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         return __half22float2(*reinterpret_cast<const __half2*>(&w));
       };
       float all32 = 0.f;
+      uint32_t kw[kAT ? 32 : 1];
+      if (kAT) {
+        // this row's K-half 0 -> TMEM A buffer it % 2, columns 0..31 (the MMA waits for it)
+        const uint8_t* rowp = a + row * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((j ^ (row & 7)) << 4));
+          kw[4 * j] = v.x; kw[4 * j + 1] = v.y; kw[4 * j + 2] = v.z; kw[4 * j + 3] = v.w;
+        }
+        if (it >= 2) mbar_wait(&at_empty[it & 1], ((it >> 1) - 1) & 1);
+        tc_fence_after();
+        tmem_st32(tmem + ((uint32_t)(nw * 32) << 16) + L::cA + (it & 1) * 64, kw);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&at_full[it & 1]);
+      }
       if (!(P.ablate & 2)) {
         float2 acc2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                           make_float2(0.f, 0.f)};         // 8 chains of 8 exact squares
@@ -445,8 +529,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
           const uint8_t* rowp = a + hf * (L::kABytes / 2) + row * 128;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {          // 16-byte chunk j (swizzled position j ^ row%8)
-            const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((j ^ (row & 7)) << 4));
-            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            uint32_t w[4];
+            if (kAT) {
+              w[0] = kw[4 * j]; w[1] = kw[4 * j + 1]; w[2] = kw[4 * j + 2]; w[3] = kw[4 * j + 3];
+            } else {
+              const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((j ^ (row & 7)) << 4));
+              w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+            }
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 f = elem_pair(w[e]);
@@ -665,12 +754,12 @@ int launch_quantize_keys_tc(const void* keys, int dtype, int64_t n, int64_t kus,
 #endif
 #define QJL_QT(MTV, NCV, SV)                                                                             \
   if (MT == MTV)                                                                                         \
-    return abf ? launch_impl<MTV, NCV, SV, 1>(keys, n, kus, sk, ch, h, kc, row_offset, st)               \
+    return abf ? launch_impl<MTV, NCV, SV, 1>(keys, n, kus, sk, ch, h, kc, row_offset, st)          \
                : launch_impl<MTV, NCV, SV, 0>(keys, n, kus, sk, ch, h, kc, row_offset, st);
-  QJL_QT(256, 1, 3)   // m = 256, no outliers (config 1 shape)
+  QJL_QT(256, kAT ? 2 : 1, 3)   // m = 256, no outliers (config 1 shape)
   QJL_QT(320, 2, 3)   // m_in 256 + m_out 64 (configs 3/5)
   QJL_QT(384, 2, 3)   // m_in 256 + m_out 128 (config 2)
-  QJL_QT(512, 2, 2)   // m = 512, no outliers
+  QJL_QT(512, kAT ? 4 : 2, 2)   // m = 512, no outliers
   QJL_QT(576, QJL_K1_NC576, 2)   // m_in 512 + m_out 64 (config 4)
 #undef QJL_QT
   return QJL_ERR_UNSUPPORTED;

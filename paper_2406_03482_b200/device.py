@@ -307,10 +307,16 @@ class DeviceKeyCache:
         self._sketch_keepalive = (sin, sout)
 
     def prefill(self, prompt_keys: torch.Tensor, values: torch.Tensor | None = None) -> None:
-        """Fused prompt profile + append: `qjl_prefill_profile` detects each
-        unit's outlier channels and builds its zero-padded S_full in one pass over the prompt
+        """Prompt profile + append: `qjl_prefill_profile` detects each unit's
+        outlier channels and builds its zero-padded S_full in one pass over the prompt
         (kvcache.py:104-123, :234-267), then K1 quantizes the prompt into rows [n, n + n0)
         (kvcache.py:293-306) and the values, if given, are quantized alongside."""
+        self.prefill_profile(prompt_keys)
+        self.append(prompt_keys.contiguous(), values)
+
+    def prefill_profile(self, prompt_keys: torch.Tensor) -> None:
+        """The profile alone (`qjl_prefill_profile`): channels, magnitudes and S_full from the
+        prompt, no quantization (kvcache.py:104-123, :234-267)."""
         s = self.shape
         pk = prompt_keys.contiguous()
         if pk.dim() != 3 or pk.shape[0] != s.units or pk.shape[2] != s.d or pk.shape[1] == 0:
@@ -319,7 +325,6 @@ class DeviceKeyCache:
             raise ValueError("no host sketches: build the cache with DeviceKeyCache.create")
         dev = self.device
         if getattr(self, "_sk_op", None) is None:
-            # S_in / S_out in the operand dtype (exact: the host copies are operand-rounded)
             self._sk_op = tuple(None if S is None else
                                 torch.as_tensor(np.ascontiguousarray(S, np.float64)).to(dev, self.sketch_dtype)
                                 for S in (self.S_in_host, self.S_out_host))
@@ -335,7 +340,6 @@ class DeviceKeyCache:
                                                 self.s_full.data_ptr(), ws.data_ptr(), ws.numel(),
                                                 _stream()), "prefill_profile")
         self.magnitudes = mags
-        self.append(pk, values)
 
     @staticmethod
     def make_sketches(d: int, h: int, m_in: int, m_out: int, seed: int = 0,

@@ -77,3 +77,23 @@ def test_prefill_with_values_and_rate_check(cuda):
         bad = DeviceKeyCache.create(2, 128, 256, h=8, m_out=8, capacity=1024, key_dtype=torch.bfloat16,
                                     validate_rate=False, with_values=False, tiled=False)
         bad.prefill(keys)
+
+
+def test_prefill_c4_bitwise(cuda):
+    """Config 4 (128 units x 8192 keys, m = 512 + 64, r = 8): the fused profile + K1 equals
+    detect + build + K1 launched separately, bit for bit -- channels, magnitudes, S_full,
+    sign bits and norms."""
+    U, n0 = 128, 8192
+    keys, a, b = _pair(U, n0, torch.bfloat16, seed=11)
+    assert torch.equal(a.channels, b.channels)
+    assert torch.equal(a.magnitudes, b.magnitudes)
+    assert torch.equal(a.s_full, b.s_full)
+    for x, y in ((a.bits_in, b.bits_in), (a.bits_out, b.bits_out), (a.norm_in, b.norm_in),
+                 (a.norm_out, b.norm_out)):
+        assert torch.equal(x[:, :n0], y[:, :n0])
+    # and the profile alone (qjl_prefill_profile) agrees
+    c = DeviceKeyCache.create(U, 128, 512, h=8, m_out=64, capacity=n0, seed=11, key_dtype=torch.bfloat16,
+                              with_values=False)
+    c.prefill_profile(keys)
+    assert torch.equal(c.channels, b.channels) and torch.equal(c.magnitudes, b.magnitudes)
+    assert torch.equal(c.s_full, b.s_full)

@@ -435,6 +435,74 @@ def measure_prefill(device, seed, shard_of_units, steps=5, warmup=2, parity=True
     return res
 
 
+def measure_c1(device, seed, steps=50):
+    """Config 1 (1 x 8 heads, n = 1024, d = 128, m = 256, no outliers, i.i.d. S, fp32 keys
+    and queries): K1 on fp32 keys (the fp64 quantizer: the reference's float64 sign test on
+    exact fp32 inputs) and the K2 logits, timed as one step (append 8192 keys + score 8
+    queries), with the oracle check of every bit (|Sk| < 1e-6 rule) and every logit."""
+    import torch
+
+    from oracle import qjl_oracle as O
+    from paper_2406_03482_b200.device import DeviceKeyCache
+    from tests._parity import check_logits, flip_report, logit_bound, make_inputs
+
+    U, n, d, m = 8, 1024, 128, 256
+    K, _, Q, _ = make_inputs(U, n, d, 1, 0, 1.0, seed + 1)
+    Kt = torch.from_numpy(K).float().to(device)
+    Qt = torch.from_numpy(Q).float().to(device)
+    cache = DeviceKeyCache.create(U, d, m, h=0, capacity=n, seed=seed + 1, orthogonalize_sketches=False,
+                                  key_dtype=torch.float32, with_values=False)
+    logits = torch.empty(U, 1, n, dtype=torch.float32, device=device)
+    for _ in range(3):
+        cache.n = 0
+        cache.append_keys(Kt)
+        cache.scores(Qt, out=logits)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        cache.n = 0
+        cache.append_keys(Kt)
+    e1.record()
+    torch.cuda.synchronize()
+    k1_ms = e0.elapsed_time(e1) / steps
+    e0.record()
+    for _ in range(steps):
+        cache.scores(Qt, out=logits)
+    e1.record()
+    torch.cuda.synchronize()
+    sc_ms = e0.elapsed_time(e1) / steps
+    hv = cache.host_view()
+    S = cache.S_in_host
+    Kr = Kt.double().cpu().numpy()
+    Qr = Qt.double().cpu().numpy()
+    lg = logits.double().cpu().numpy()
+    flips = dict(total=0, lt1e6=0, coords=0)
+    norm_bad, logit_bad, worst = 0, 0, 0.0
+    for u in range(U):
+        r = O.append_keys(S, None, (), Kr[u])
+        fr = flip_report(hv["bits_in"][u], r["bits_in"], r["proj_in"], m)
+        for k in flips:
+            flips[k] += fr[k]
+        norm_bad += int((hv["norm_in"][u] != O.fp16_round(r["norm_in"])).sum())
+        c = dict(bits_in=hv["bits_in"][u], norm_in=hv["norm_in"][u])
+        ref = O.estimate_logits(S, None, (), Qr[u, 0], c)
+        ok, err = check_logits(lg[u, 0], ref, logit_bound(S, None, (), Qr[u, 0], hv["norm_in"][u], 0))
+        logit_bad += int((~ok).sum())
+        worst = max(worst, float(np.max(np.abs(lg[u, 0] - ref) / np.maximum(np.abs(ref), 1e-300))))
+    keys = U * n
+    return {"workload": "c1_quantize_scores_fp32", "units": U, "keys": keys,
+            "k1_ms": k1_ms, "keys_per_s": keys / (k1_ms * 1e-3), "scores_ms": sc_ms,
+            "step_ms": k1_ms + sc_ms,
+            "parity": {"sign_bits": flips["coords"], "flips": flips["total"],
+                       "flips_abs_proj_lt_1e-6": flips["lt1e6"], "fp16_norm_mismatches": norm_bad,
+                       "logits_checked": keys, "logits_out_of_tolerance": logit_bad,
+                       "logit_rel_err_max": worst,
+                       "pass": flips["total"] == flips["lt1e6"] and norm_bad == 0 and logit_bad == 0},
+            "note": "fp32 keys run the fp64 quantizer (exact products, the reference's float64 sign "
+                    "test); launch-bound at this size (8192 keys), a parity configuration"}
+
+
 def measure_generation_step(cache, q, steps=50):
     """Row F1: one generation step = append every unit's new token (key + value) and decode
     over the grown cache.  `decode_step` fuses the append into the step's query-sketch kernel;
@@ -680,6 +748,11 @@ def run_gpu(args):
             res["generation_step"] = {"error": repr(e)[:200]}
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         res["cpu_baseline"], res["parity"] = cpu_baseline_leg(cache, q, w)
+        if not args.no_extras:                      # config 1 with its oracle check
+            try:
+                res["c1"] = measure_c1(device, args.seed)
+            except Exception as e:                   # pragma: no cover
+                res["c1"] = {"error": repr(e)[:200]}
     if rank == 0:
         print(json.dumps(res, default=_jsonable), flush=True)
     if world > 1:

@@ -609,21 +609,28 @@ int launch_prefill_profile(const void* keys, int dtype, int units, int64_t n0, i
 // -0.0 -> 1, NaN -> 0), bits packed with warp ballots: lane j of a warp owns
 // sketch row 32w+j, so the ballot word IS the LSB-first u32 of those 32 rows.
 // Norms ||k_in||, ||k_out|| in fp64, rounded once to fp16.
-// CTA = 256 threads, kTok tokens; S is staged through smem kCk columns at a time.
+// CTA = 128 threads x TOK tokens; thread t owns sketch rows t + 128 i (i < RPT).  S is
+// staged through smem kQCk columns at a time as [kQCk][m_total + 1] (conflict-free row
+// reads and staging stores), the tokens as [d][TOK] so one 16-byte broadcast load feeds
+// 2 tokens x RPT rows of FMAs.  The fp64 FMA chain per (row, token) runs over c in increasing order.
 // ---------------------------------------------------------------------------
-constexpr int kQTok = 16;
 constexpr int kQCk = 16;
-constexpr int kQThreads = 256;
+constexpr int kQThreads = 128;
+#ifndef QJL_QK_PRE
+#define QJL_QK_PRE 1
+#endif
 
-template <typename TK, typename TS, int RPT>
+template <typename TK, typename TS, int RPT, int TOK>
 __global__ void __launch_bounds__(kQThreads) k_quantize_keys_simt(
     const TK* __restrict__ keys, int64_t n, int64_t key_unit_stride, const TS* __restrict__ s_full,
     int64_t s_unit_stride, int d, int m_in, int m_out, const int32_t* __restrict__ channels, int h,
     qjl_key_cache_t kc, int64_t row_offset) {
   extern __shared__ double sm[];
+  constexpr int kQTok = TOK;
   const int m_total = m_in + m_out;
-  double* sk = sm;                         // [kQTok][d]
-  double* ss = sm + kQTok * d;             // [m_total][kQCk + 1]
+  double* sk = sm;                         // [d][kQTok]
+  double* ss = sm + kQTok * d;             // [kQCk][m_total + 1] (padded: conflict-free staging)
+  const int msp = m_total + 1;
   __shared__ unsigned char is_out[1024];
   const int u = blockIdx.y;
   const int64_t t0 = (int64_t)blockIdx.x * kQTok;
@@ -634,8 +641,8 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_keys_simt(
   __syncthreads();
   for (int j = threadIdx.x; j < h; j += blockDim.x) is_out[channels[(int64_t)u * h + j]] = 1;
   for (int i = threadIdx.x; i < kQTok * d; i += blockDim.x) {
-    const int tt = i / d, c = i % d;
-    sk[i] = (t0 + tt < n) ? to_f64(K[(t0 + tt) * d + c]) : 0.0;
+    const int tt = i / d, c = i % d;                 // coalesced key reads, transposed store
+    sk[c * kQTok + tt] = (t0 + tt < n) ? to_f64(K[(t0 + tt) * d + c]) : 0.0;
   }
 
   double acc[RPT][kQTok];
@@ -644,21 +651,52 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_keys_simt(
 #pragma unroll
     for (int t = 0; t < kQTok; ++t) acc[i][t] = 0.0;
 
+  // S chunks: the next chunk's values are loaded into registers while the current one is
+  // multiplied (element e of the thread: i = threadIdx.x + 128 e, row i / kQCk, col i % kQCk)
+  constexpr bool kPre = QJL_QK_PRE && RPT <= 2;       // register budget: prefetch for m <= 256 only
+  constexpr int PF = kPre ? RPT * kQCk : 1;
+  double pf[PF];
+  auto load_chunk = [&](int c0) {
+    if (!kPre) return;
+#pragma unroll
+    for (int e = 0; e < PF; ++e) {
+      const int i = threadIdx.x + e * kQThreads, r = i / kQCk, cc = i % kQCk;
+      pf[e] = (r < m_total && c0 + cc < d) ? to_f64(S[(int64_t)r * d + c0 + cc]) : 0.0;
+    }
+  };
+  load_chunk(0);
   for (int c0 = 0; c0 < d; c0 += kQCk) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < m_total * kQCk; i += blockDim.x) {
-      const int r = i / kQCk, cc = i % kQCk;
-      ss[r * (kQCk + 1) + cc] = (c0 + cc < d) ? to_f64(S[(int64_t)r * d + c0 + cc]) : 0.0;
+    __syncthreads();                                  // the previous chunk's reads of ss are done
+    if constexpr (kPre) {
+#pragma unroll
+      for (int e = 0; e < PF; ++e) {
+        const int i = threadIdx.x + e * kQThreads, r = i / kQCk, cc = i % kQCk;
+        if (r < m_total) ss[cc * msp + r] = pf[e];
+      }
+    } else {
+      for (int i = threadIdx.x; i < m_total * kQCk; i += blockDim.x) {
+        const int r = i / kQCk, cc = i % kQCk;
+        ss[cc * msp + r] = (c0 + cc < d) ? to_f64(S[(int64_t)r * d + c0 + cc]) : 0.0;
+      }
     }
     __syncthreads();
+    if (c0 + kQCk < d) load_chunk(c0 + kQCk);         // in flight during this chunk's FMAs
+    const int ncc = min(kQCk, d - c0);
+    for (int cc = 0; cc < ncc; ++cc) {
+      double sv[RPT];
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int r = threadIdx.x + i * kQThreads;
-      if (r < m_total) {
-        for (int cc = 0; cc < kQCk && c0 + cc < d; ++cc) {
-          const double s = ss[r * (kQCk + 1) + cc];
+      for (int i = 0; i < RPT; ++i) {
+        const int r = threadIdx.x + i * kQThreads;
+        sv[i] = r < m_total ? ss[cc * msp + r] : 0.0;
+      }
+      const double2* kv2 = reinterpret_cast<const double2*>(sk + (c0 + cc) * kQTok);
 #pragma unroll
-          for (int t = 0; t < kQTok; ++t) acc[i][t] = fma(s, sk[t * d + c0 + cc], acc[i][t]);
+      for (int t2 = 0; t2 < kQTok / 2; ++t2) {
+        const double2 kv = kv2[t2];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          acc[i][2 * t2] = fma(sv[i], kv.x, acc[i][2 * t2]);
+          acc[i][2 * t2 + 1] = fma(sv[i], kv.y, acc[i][2 * t2 + 1]);
         }
       }
     }
@@ -690,7 +728,7 @@ __global__ void __launch_bounds__(kQThreads) k_quantize_keys_simt(
     if (t0 + t >= n) continue;
     double s_in = 0.0, s_out = 0.0;
     for (int c = lane; c < d; c += 32) {
-      const double v = sk[t * d + c];
+      const double v = sk[c * kQTok + t];
       if (is_out[c]) s_out = fma(v, v, s_out); else s_in = fma(v, v, s_in);
     }
     s_in = warp_sum_f64(s_in);
@@ -710,11 +748,12 @@ static int launch_qk_simt_2(const void* keys, int64_t n, int64_t kus, const void
                             const qjl_key_cache_t& kc, int64_t row_offset, cudaStream_t st) {
   const int m_total = m_in + m_out;
   const int rpt = (m_total + kQThreads - 1) / kQThreads;
-  const size_t smem = ((size_t)kQTok * d + (size_t)m_total * (kQCk + 1)) * sizeof(double);
-  dim3 grid((unsigned)((n + kQTok - 1) / kQTok), kc.units);
-#define QJL_QK(R)                                                                          \
-  if (rpt == R) {                                                                          \
-    auto kern = k_quantize_keys_simt<TK, TS, R>;                                           \
+  const int tok = rpt <= 4 ? 16 : 8;                  // acc[RPT][TOK] in registers
+#define QJL_QK(R, TT)                                                                      \
+  if (rpt == R && tok == TT) {                                                             \
+    auto kern = k_quantize_keys_simt<TK, TS, R, TT>;                                       \
+    const size_t smem = ((size_t)TT * d + (size_t)(m_total + 1) * kQCk) * sizeof(double);  \
+    dim3 grid((unsigned)((n + TT - 1) / TT), kc.units);                                    \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
     timing_begin(st);                                                                      \
     kern<<<grid, kQThreads, smem, st>>>((const TK*)keys, n, kus, (const TS*)s, sus, d,     \
@@ -723,10 +762,14 @@ static int launch_qk_simt_2(const void* keys, int64_t n, int64_t kus, const void
     QJL_LAUNCH_CHECK("quantize_keys_simt");                                                \
     return QJL_OK;                                                                         \
   }
-  QJL_QK(1)
-  QJL_QK(2)
-  QJL_QK(3)
-  QJL_QK(4)
+  QJL_QK(1, 16)
+  QJL_QK(2, 16)
+  QJL_QK(3, 16)
+  QJL_QK(4, 16)
+  QJL_QK(5, 8)
+  QJL_QK(6, 8)
+  QJL_QK(7, 8)
+  QJL_QK(8, 8)
 #undef QJL_QK
   set_error("quantize_keys: m_in + m_out = %d exceeds 1024", m_total);
   return QJL_ERR_UNSUPPORTED;

@@ -52,7 +52,10 @@ constexpr int kThreads = 128;      // 4 warps; thread t: token t (scores) and di
 #endif
 constexpr bool kSplit = QJL_UD_SPLIT != 0;
 constexpr int kTile = 128;         // tokens per tile
-constexpr int kStages = 3;         // records in flight per CTA (a refill is issued kStages ahead)
+#ifndef QJL_UD_STAGES
+#define QJL_UD_STAGES 3
+#endif
+constexpr int kStages = QJL_UD_STAGES;   // records in flight per CTA (a refill is issued kStages ahead)
 constexpr int kRecF = 130;         // per (partial, query): m (log2 domain), l, out[128]
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;

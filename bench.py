@@ -625,7 +625,9 @@ def run_gpu(args):
             comp.wait_event(up_done[b])
             if i >= 2:
                 comp.wait_event(d2h_done[b])            # od[b] / oh[b] were read back two steps ago
-            cache.decode(qd[b], out=od[b])
+            # chained (N = 1): the previous kernel on this stream is the previous step's
+            # decode, and this step's query upload is complete (event wait above)
+            cache.decode(qd[b], out=od[b], chained=(i > 0 and world == 1))
             full = gather_units(od[b], shard) if world > 1 else od[b]
             dec_done[b].record(comp)
             with torch.cuda.stream(copy):               # read this step's (gathered) output back

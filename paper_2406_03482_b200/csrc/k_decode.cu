@@ -139,7 +139,8 @@ struct Layout {
   static constexpr int oMax = oStage + kStages * kRec;  // [8 slots][4 warps] tile maxima
   static constexpr int oQc = oMax + 4 * 8 * 4;          // [4 queries] float4 estimator constants
   static constexpr int oBar = oQc + 4 * 16;
-  static constexpr int kBars = kStages + 5;             // full[kStages], score MMA, PV MMA, B image, A ready, P ready
+  static constexpr int kBars = kStages + 6;             // full[kStages], score MMA, PV MMA, B image, A ready, P ready,
+                                                        // first score-MMA half (split-K decode)
   static constexpr int oTmem = oBar + kBars * 8;
   static constexpr int oFlag = oTmem + 4;
   static constexpr int kTotal = oFlag + 12 + 1024;      // + alignment slack
@@ -156,6 +157,19 @@ struct Layout {
   static constexpr int kAlloc = kCols <= 128 ? 128 : 256;
   static_assert(kRec % 16 == 0 && kKeyRec % 16 == 0, "bulk copies move multiples of 16 bytes");
   static_assert(NH * 2048 + 4 * 2048 >= (20 * kThreads + 20) * 4, "flush scratch must fit in Bsc/Bpv");
+};
+
+// Decode TMEM geometry.  m_in = 512 (KC > 12): the score MMA runs in two K halves whose
+// A operands (<= 80 columns each) reuse columns [0, 96), so D_sc sits at 96 and a CTA
+// needs 128 columns -- 3 CTAs per SM instead of 2 with a 256-column allocation.
+template <int KCI, int KCO>
+struct DecTmem {
+  static constexpr int KC = KCI + KCO;
+  static constexpr bool SK = KC > 12;
+  static constexpr int KH = SK ? KCI / 2 : KC;          // sign words in the first half
+  static constexpr int cDsc = SK ? 96 : Layout<KCI, KCO>::cDsc;
+  static constexpr int kAlloc = SK ? 128 : Layout<KCI, KCO>::kAlloc;
+  static_assert(!SK || 8 * (KC - KH) <= 96, "second A half must fit below D_sc");
 };
 
 // ----------------------------------------------------------------- prep kernel
@@ -472,6 +486,51 @@ __device__ __forceinline__ void issue_score_mma(uint32_t tbase, uint64_t dsc0) {
       mma_i8<1>(tbase + L::cDsc + 16, tbase + 8 * (KCI + c), dsc0 + (uint64_t)(h0 + (c >> 2) * 128 + (c & 3) * 2), ID);
   }
 }
+// sign words [W0, W1) of the thread's token row (in-side words first, then out-side)
+template <int KCI, int KCO, int W0, int W1>
+__device__ __forceinline__ void load_sign_range(const uint8_t* st, int tid, uint32_t* wv) {
+  using L = Layout<KCI, KCO>;
+  static_assert(W0 % 4 == 0 && (W1 <= KCI ? W1 % 4 == 0 : (W1 - KCI) % 2 == 0), "vector-aligned ranges");
+  const uint4* bi = reinterpret_cast<const uint4*>(st + L::oBitsIn + tid * KCI * 4);
+#pragma unroll
+  for (int c = W0 / 4; c < (W1 < KCI ? W1 : KCI) / 4; ++c) {
+    const uint4 x = bi[c];
+    wv[4 * c - W0] = x.x; wv[4 * c + 1 - W0] = x.y; wv[4 * c + 2 - W0] = x.z; wv[4 * c + 3 - W0] = x.w;
+  }
+  if (KCO && W1 > KCI) {
+    const uint2* bo = reinterpret_cast<const uint2*>(st + L::oBitsOut + tid * KCO * 4);
+#pragma unroll
+    for (int c = 0; c < (W1 - KCI) / 2; ++c) {
+      const uint2 x = bo[c];
+      wv[KCI - W0 + 2 * c] = x.x; wv[KCI - W0 + 2 * c + 1] = x.y;
+    }
+  }
+}
+// split-K score MMAs: half 0 = in-side chunks [0, KH) at A columns 8 c; half 1 = in-side
+// chunks [KH, KCI) and the out-side chunks, at A columns from 0 again
+template <int KCI, int KCO, int HALF>
+__device__ __forceinline__ void issue_score_mma_half(uint32_t tbase, uint64_t dsc0) {
+  using L = Layout<KCI, KCO>;
+  using T = DecTmem<KCI, KCO>;
+  constexpr uint32_t ID = idesc_i8(16, 0);
+  if (HALF == 0) {
+    mma_i8<0>(tbase + T::cDsc, tbase, dsc0, ID);
+#pragma unroll
+    for (int c = 1; c < T::KH; ++c)
+      mma_i8<1>(tbase + T::cDsc, tbase + 8 * c, dsc0 + (uint64_t)((c >> 2) * 128 + (c & 3) * 2), ID);
+  } else {
+#pragma unroll
+    for (int c = T::KH; c < KCI; ++c)
+      mma_i8<1>(tbase + T::cDsc, tbase + 8 * (c - T::KH), dsc0 + (uint64_t)((c >> 2) * 128 + (c & 3) * 2), ID);
+    if (KCO) {
+      constexpr int h0 = L::NHI * 128, a0 = 8 * (KCI - T::KH);
+      mma_i8<0>(tbase + T::cDsc + 16, tbase + a0, dsc0 + (uint64_t)h0, ID);
+#pragma unroll
+      for (int c = 1; c < KCO; ++c)
+        mma_i8<1>(tbase + T::cDsc + 16, tbase + a0 + 8 * c, dsc0 + (uint64_t)(h0 + (c >> 2) * 128 + (c & 3) * 2), ID);
+    }
+  }
+}
 // logits (log2 domain) of the NQ heads from the score accumulators (kvcache.py:311-329)
 template <int KCO, int NQ, int CDSC>
 __device__ __forceinline__ void score_logits(uint32_t tlane, const float4* qcs, float nin, float nout, float* lg) {
@@ -506,8 +565,9 @@ __device__ __forceinline__ void score_logits(uint32_t tlane, const float4* qcs, 
 // NQ: query heads the epilogue processes (1, 2 or 4 >= G): MHA (G = 1) skips the work of
 // three padding heads
 template <int KCI, int KCO, int NQ>
-__global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(const Params P) {
+__global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 3 : 4) k_udecode(const Params P) {
   using L = Layout<KCI, KCO>;
+  using TM = DecTmem<KCI, KCO>;
   constexpr int KC = KCI + KCO;
   extern __shared__ uint8_t sm_raw[];
   // align to 1024 B (SWIZZLE_128B atoms) by pointer arithmetic on the shared array, so the
@@ -516,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   const uint32_t s_sm = smem_u32(sm);
   const uint32_t a_full = s_sm + L::oBar;                      // [kStages]
   const uint32_t a_sc = a_full + 8 * kStages, a_pv = a_sc + 8, a_bsc = a_sc + 16, a_ard = a_sc + 24,
-                 a_prd = a_sc + 32;
+                 a_prd = a_sc + 32, a_sk = a_sc + 40;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::oTmem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = P.ctas;
@@ -545,12 +605,13 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
     mbar_init(a_bsc, 1);
     mbar_init(a_ard, 4);
     mbar_init(a_prd, 4);
+    mbar_init(a_sk, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid < 32) reinterpret_cast<float*>(sm + L::oMax)[tid] = 0.f;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(L::kAlloc));
+                 "r"(TM::kAlloc));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -593,7 +654,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   float m_lane = -INFINITY, l_part[4], acc[4], invK[4];
   float2 Z[4][2];                      // [q][group pair]
   const float4* qcs = reinterpret_cast<const float4*>(sm + L::oQc);
-  uint32_t sc_ph = 0, pv_ph = 0, bsc_par = 0, rd_ph = 0;
+  uint32_t sc_ph = 0, pv_ph = 0, bsc_par = 0, rd_ph = 0, sk_ph = 0;
   bool pv_pend = false;
   // the thread's code-chunk offsets within its dim quad's 128-byte row (p2t_byte swizzle)
   const uint32_t c_row = L::oCodes + (tid >> 2) * 128, c_sw = ((tid >> 2) & 3) << 4;
@@ -807,7 +868,38 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
         const bool valid = !MASK || lt * kTile + tid < n32;            // this thread's token is < n
 
         // ---------------- 1. score A operand: masked sign words -> TMEM ----------------
-        {
+        if constexpr (TM::SK) {
+          // split K (m_in = 512): first half of the in-side words, its MMAs, then the rest
+          {
+            uint32_t wv[TM::KH];
+            load_sign_range<KCI, KCO, 0, TM::KH>(st, tid, wv);
+            if (pv_pend) pv_readback();               // the PV MMA of the previous tile (aliases A_sc)
+            store_sign_operand<TM::KH>(tlane, wv);
+          }
+          tmem_wait_st();
+          tc_fence_before();
+          bar_sync(1, kThreads);
+          if (warp == 0) {
+            if (elect_one()) {
+              if (first) {
+                mbar_wait(a_bsc, bsc_par);
+                bsc_par ^= 1;
+              }
+              tc_fence_after();
+              issue_score_mma_half<KCI, KCO, 0>(tbase, dsc0);
+              tc_commit(a_sk);
+            }
+            __syncwarp();
+          }
+          {
+            uint32_t wv[KC - TM::KH];
+            load_sign_range<KCI, KCO, TM::KH, KC>(st, tid, wv);
+            mbar_wait(a_sk, sk_ph);                   // the first half's A columns are free
+            sk_ph ^= 1;
+            tc_fence_after();
+            store_sign_operand<KC - TM::KH>(tlane, wv);
+          }
+        } else {
           uint32_t wv[KC];
           load_sign_words<KCI, KCO>(st, tid, wv);
           if (pv_pend) pv_readback();                 // the PV MMA of the previous tile (aliases A_sc)
@@ -824,12 +916,13 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
         if (warp == 0) {
           if (elect_one()) {
             if (kSplit) mbar_wait(a_ard, rd_ph);
-            if (first) {
+            if (first && !TM::SK) {
               mbar_wait(a_bsc, bsc_par);
               bsc_par ^= 1;
             }
             tc_fence_after();
-            issue_score_mma<KCI, KCO>(tbase, dsc0);
+            if constexpr (TM::SK) issue_score_mma_half<KCI, KCO, 1>(tbase, dsc0);
+            else issue_score_mma<KCI, KCO>(tbase, dsc0);
             tc_commit(a_sc);
           }
           __syncwarp();
@@ -847,7 +940,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
         sc_ph ^= 1;
         tc_fence_after();
         float lg[4];
-        score_logits<KCO, NQ, L::cDsc>(tlane, qcs, nin, nout, lg);
+        score_logits<KCO, NQ, TM::cDsc>(tlane, qcs, nin, nout, lg);
         if (MASK && !valid) {
 #pragma unroll
           for (int q = 0; q < NQ; ++q) lg[q] = -INFINITY;
@@ -1013,7 +1106,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_udecode(
   }
   if (tid == 0) g_ud_trace[blockIdx.x][2] = gtimer();
 #endif
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(L::kAlloc));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(TM::kAlloc));
 }
 
 // ------------------------------------------------------------ scores-only K2
@@ -1173,7 +1266,7 @@ static int resident_ctas(K kern, int smem_bytes, int tmem_cols) {
 template <int KCI, int KCO, int NQ>
 static int occupancy_dec() {
   static int occ = -1;
-  if (occ < 0) occ = resident_ctas(k_udecode<KCI, KCO, NQ>, Layout<KCI, KCO>::kTotal, Layout<KCI, KCO>::kAlloc);
+  if (occ < 0) occ = resident_ctas(k_udecode<KCI, KCO, NQ>, Layout<KCI, KCO>::kTotal, DecTmem<KCI, KCO>::kAlloc);
   return occ;
 }
 template <int KCI, int KCO, int NQ>

@@ -232,6 +232,16 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t* r) {
 constexpr bool kAT = QJL_K1_ATMEM != 0;
 static_assert(!kAT || QJL_K1_ZEROACC, "the TMEM-A MMAs always accumulate onto re-zeroed buffers");
 
+#ifndef QJL_K1_HALFDRAIN
+#define QJL_K1_HALFDRAIN 0  // 1: both epilogue sets drain every chunk, half the words each (measured 2 % slower)
+#endif
+#ifndef QJL_K1_TRACE
+#define QJL_K1_TRACE 0      // diagnostics: per-CTA cycle counters of the MMA issuer (tools/k1_trace.py)
+#endif
+#if QJL_K1_TRACE
+__device__ unsigned long long g_k1_trace[1024][6];   // [cta] {at_full wait, t_empty wait, b_full wait, issue, total, tiles}
+#endif
+
 template <int MT, int NC, int STAGES>
 struct QLayout {
   static constexpr int CH = MT / NC;                       // columns per N chunk
@@ -307,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     mbar_init(b_empty, 1);
     for (int b = 0; b < L::NBUF; ++b) {
       mbar_init(&t_full[b], 1);
-      mbar_init(&t_empty[b], 4);          // the 4 epilogue warps of the chunk's set
+      mbar_init(&t_empty[b], QJL_K1_HALFDRAIN ? 8 : 4);   // the epilogue warps draining the buffer
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_keys) : "memory");
@@ -375,16 +385,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
     // ================================ MMA issuer ==================================
     if (lane == 0) {
       int u = u_first, lt = lt_first, cur_u = -1, b_uses = 0, chunk = 0;
+#if QJL_K1_TRACE
+      long long tw_a = 0, tw_t = 0, tw_b = 0, t_iss = 0;
+      const long long t_start = clock64();
+#define K1T(var, stmt) { const long long c0_ = clock64(); stmt; var += clock64() - c0_; }
+#else
+#define K1T(var, stmt) stmt;
+#endif
       for (int it = 0; it < ntiles; ++it) {
         if (u != cur_u) {
-          mbar_wait(b_full, b_uses & 1);
+          K1T(tw_b, mbar_wait(b_full, b_uses & 1))
           cur_u = u;
           ++b_uses;
         }
         const int s = it % STAGES;
         const int ab = it & 1;                   // kAT: A buffer of this tile
-        if (kAT) mbar_wait(&at_full[ab], (it >> 1) & 1);
-        else mbar_wait(&a_full[s], (it / STAGES) & 1);
+        if (kAT) { K1T(tw_a, mbar_wait(&at_full[ab], (it >> 1) & 1)) }
+        else { K1T(tw_a, mbar_wait(&a_full[s], (it / STAGES) & 1)) }
         tc_fence_after();
         // descriptors built once; the start-address field (bits 0-13, 16-byte units) takes
         // the K / chunk offsets as plain adds (all shared addresses are < 256 KB)
@@ -395,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
 #pragma unroll
         for (int c = 0; c < NC; ++c, ++chunk) {
           const int buf = chunk % L::NBUF;
-          if (chunk >= L::NBUF) mbar_wait(&t_empty[buf], ((chunk / L::NBUF) - 1) & 1);
+          if (chunk >= L::NBUF) { K1T(tw_t, mbar_wait(&t_empty[buf], ((chunk / L::NBUF) - 1) & 1)) }
           tc_fence_after();
           const uint32_t d_tmem = tmem + buf * L::BUFW;
           if (do_mma) {
@@ -420,6 +437,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
         if (last_of_unit) tc_commit(b_empty);    // S_full of this unit no longer read
         if (++lt == P.tpu) { lt = 0; ++u; }
       }
+#if QJL_K1_TRACE
+      const long long t_tot = clock64() - t_start;
+      g_k1_trace[blockIdx.x][0] = tw_a;
+      g_k1_trace[blockIdx.x][1] = tw_t;
+      g_k1_trace[blockIdx.x][2] = tw_b;
+      g_k1_trace[blockIdx.x][3] = t_tot - tw_a - tw_t - tw_b;
+      g_k1_trace[blockIdx.x][4] = t_tot;
+      g_k1_trace[blockIdx.x][5] = ntiles;
+#endif
+#undef K1T
     }
   } else if (warp >= 14) {
     // ===================== norms, K-half 1: partial sums of squares ================
@@ -618,19 +645,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
       uint8_t* const rout =
           m_out ? P.kc.bits_out + row_off(u, P.row_offset + tok, m_out / 8, P.kc.capacity, P.kc.tile_stride) : nullptr;
       for (int c = 0; c < NC; ++c, ++chunk) {
-        if ((chunk & 1) != set) continue;      // the two warp sets alternate chunks
+        if (!QJL_K1_HALFDRAIN && (chunk & 1) != set) continue;   // (whole-chunk mode: sets alternate chunks)
         const int buf = chunk % L::NBUF;
         mbar_wait(&t_full[buf], (chunk / L::NBUF) & 1);
         tc_fence_after();
+        // QJL_K1_HALFDRAIN: both sets drain every chunk, set 0 its first ceil(W/2) sign words,
+        // set 1 the rest, so a buffer is free after half the serial TMEM loads
+        constexpr int W = CH / 32;
+        const int wb = QJL_K1_HALFDRAIN ? (set ? (W + 1) / 2 : 0) : 0;
+        const int we = QJL_K1_HALFDRAIN ? (set ? W : (W + 1) / 2) : W;
+        const uint32_t tq = tmem + ((uint32_t)(ew * 32) << 16) + buf * L::BUFW;
+        int w = wb;
 #pragma unroll 1
-        for (int g64 = 0; g64 < (P.ablate & 1 ? 0 : CH / 64); ++g64) {
+        for (; w + 2 <= (P.ablate & 1 ? wb : we); w += 2) {
           uint32_t r[64];
-          tmem_ld64(tmem + ((uint32_t)(ew * 32) << 16) + buf * L::BUFW + g64 * 64, r);
-          if (QJL_K1_ZEROACC) tmem_zero64(tmem + ((uint32_t)(ew * 32) << 16) + buf * L::BUFW + g64 * 64);
+          tmem_ld64(tq + w * 32, r);
+          if (QJL_K1_ZEROACC) tmem_zero64(tq + w * 32);
           const uint32_t w0 = QJL_K1_ZEROACC ? sign_word_raw(r) : QJL_K1_FASTSIGN ? sign_word_fast(r) : sign_word(r);
           const uint32_t w1 = QJL_K1_ZEROACC ? sign_word_raw(r + 32)
                                              : QJL_K1_FASTSIGN ? sign_word_fast(r + 32) : sign_word(r + 32);
-          const int sr = c * CH + g64 * 64;      // first sketch row of the word pair
+          const int sr = c * CH + w * 32;        // first sketch row of the word pair
           if (valid) {
             uint32_t* d0 = sr < m_in ? reinterpret_cast<uint32_t*>(rin) + (sr >> 5)
                                      : reinterpret_cast<uint32_t*>(rout) + ((sr - m_in) >> 5);
@@ -645,17 +679,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
             }
           }
         }
-        if constexpr (CH % 64 == 32) {           // trailing 32-column group of the chunk
+        if (w < we && !(P.ablate & 1)) {         // a single trailing 32-column word
           uint32_t r[32];
-          tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + buf * L::BUFW + (CH - 32), r);
-          if (QJL_K1_ZEROACC) tmem_zero32(tmem + ((uint32_t)(ew * 32) << 16) + buf * L::BUFW + (CH - 32));
-          const uint32_t w = QJL_K1_ZEROACC ? sign_word_raw(r) : QJL_K1_FASTSIGN ? sign_word_fast(r) : sign_word(r);
-          const int sr = c * CH + CH - 32;
+          tmem_ld32(tq + w * 32, r);
+          if (QJL_K1_ZEROACC) tmem_zero32(tq + w * 32);
+          const uint32_t wd = QJL_K1_ZEROACC ? sign_word_raw(r) : QJL_K1_FASTSIGN ? sign_word_fast(r) : sign_word(r);
+          const int sr = c * CH + w * 32;
           if (valid) {
             if (sr < m_in)
-              reinterpret_cast<uint32_t*>(rin)[sr >> 5] = w;
+              reinterpret_cast<uint32_t*>(rin)[sr >> 5] = wd;
             else
-              reinterpret_cast<uint32_t*>(rout)[(sr - m_in) >> 5] = w;
+              reinterpret_cast<uint32_t*>(rout)[(sr - m_in) >> 5] = wd;
           }
         }
         if (QJL_K1_ZEROACC) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");   // zeros landed
@@ -766,3 +800,9 @@ int launch_quantize_keys_tc(const void* keys, int dtype, int64_t n, int64_t kus,
 }
 
 }  // namespace qjl
+
+#if QJL_K1_TRACE
+extern "C" __attribute__((visibility("default"))) int qjl_debug_k1_trace(void* host, int ctas) {
+  return (int)cudaMemcpyFromSymbol(host, qjl::qtc::g_k1_trace, sizeof(unsigned long long) * 6 * ctas);
+}
+#endif

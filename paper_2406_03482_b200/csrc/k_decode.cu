@@ -1323,6 +1323,14 @@ static Plan make_plan(const qjl_key_cache_t& kc, int64_t n, int G, int id, bool 
   p.spu = p.seg ? (p.tpu + p.seg - 1) / p.seg : 1;
   const int64_t work = p.seg ? (int64_t)kc.units * p.spu : p.T;
   p.ctas = (int)(work < slots ? work : slots);
+  // few units (small batch): at most max(32, tiles per unit / 8) CTAs per unit -- a unit's
+  // last CTA merges one partial per CTA in dependent L2 rounds, which beyond ~32 partials
+  // costs more than the extra CTAs gain unless each still gets >= 8 tiles (measured: C5
+  // B1 x 32k 28.4 -> 21.7 us; B1 x 128k keeps its 74 CTAs per unit)
+  if (!p.seg) {
+    const int64_t nsmax = p.tpu / 8 > 32 ? p.tpu / 8 : 32;
+    if ((int64_t)kc.units * nsmax < p.ctas) p.ctas = (int)((int64_t)kc.units * nsmax);
+  }
   int ms = 1;
   if (p.seg) {
     ms = p.spu;

@@ -148,7 +148,7 @@ struct Layout {
   static constexpr int sStage = NH * 2048;
   static constexpr int sQc = sStage + kStages * kKeyRec;
   static constexpr int sBar = sQc + 4 * 16;
-  static constexpr int sTmem = sBar + (kStages + 2) * 8;
+  static constexpr int sTmem = sBar + (kStages + 3) * 8;
   static constexpr int sTotal = sTmem + 16 + 1024;
   // TMEM columns: A_sc [0, 8 KC); after the score MMA: A_pv [0, 32), D_pv [32, 96);
   // D_sc (in: 16, out: 16) after both
@@ -1114,14 +1114,15 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 3 : 4) k_udecode(
 // estimate_logits): stages hold the key fields of each record (one bulk copy), the
 // score accumulators become logits (natural-log units) stored coalesced per head.
 template <int KCI, int KCO, int NQ>
-__global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_uscores(const Params P) {
+__global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 3 : 4) k_uscores(const Params P) {
   using L = Layout<KCI, KCO>;
+  using TM = DecTmem<KCI, KCO>;                 // m_in = 512: split-K score MMA, 128 TMEM columns
   constexpr int KC = KCI + KCO;
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
   const uint32_t s_sm = smem_u32(sm);
   const uint32_t a_full = s_sm + L::sBar;
-  const uint32_t a_sc = a_full + 8 * kStages, a_bsc = a_sc + 8;
+  const uint32_t a_sc = a_full + 8 * kStages, a_bsc = a_sc + 8, a_sk = a_sc + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::sTmem);
   const int tid = threadIdx.x, warp = tid >> 5;
   const int64_t T = P.total_tiles;
@@ -1132,11 +1133,12 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_uscores(
     for (int s = 0; s < kStages; ++s) mbar_init(a_full + 8 * s, 1);
     mbar_init(a_sc, 1);
     mbar_init(a_bsc, 1);
+    mbar_init(a_sk, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(L::kAlloc));
+                 "r"(TM::kAlloc));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -1169,7 +1171,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_uscores(
   asm volatile("griddepcontrol.wait;" ::: "memory");   // Bsc / qconst come from k_uprep
   const float4* qcs = reinterpret_cast<const float4*>(sm + L::sQc);
   const int64_t n = P.n;
-  uint32_t sc_ph = 0, bsc_par = 0, full_ph = 0;
+  uint32_t sc_ph = 0, bsc_par = 0, full_ph = 0, sk_ph = 0;
   int u = u_first, lt = lt_first, s = 0, it = 0;
   while (it < ntiles) {
     const int seg_end = min(ntiles, it + (P.tpu - lt));
@@ -1184,7 +1186,34 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_uscores(
     for (; it < seg_end; ++it, ++lt) {
       mbar_wait(a_full + 8 * s, full_ph);
       const uint8_t* st = sm + L::sStage + s * L::kKeyRec;
-      {
+      if constexpr (TM::SK) {
+        {
+          uint32_t wv[TM::KH];
+          load_sign_range<KCI, KCO, 0, TM::KH>(st, tid, wv);
+          store_sign_operand<TM::KH>(tlane, wv);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        bar_sync(1, kThreads);
+        if (warp == 0) {
+          if (elect_one()) {
+            if (first) {
+              mbar_wait(a_bsc, bsc_par);
+              bsc_par ^= 1;
+            }
+            tc_fence_after();
+            issue_score_mma_half<KCI, KCO, 0>(tbase, dsc0);
+            tc_commit(a_sk);
+          }
+          __syncwarp();
+        }
+        uint32_t wv[KC - TM::KH];
+        load_sign_range<KCI, KCO, TM::KH, KC>(st, tid, wv);
+        mbar_wait(a_sk, sk_ph);
+        sk_ph ^= 1;
+        tc_fence_after();
+        store_sign_operand<KC - TM::KH>(tlane, wv);
+      } else {
         uint32_t wv[KC];
         load_sign_words<KCI, KCO>(st, tid, wv);
         store_sign_operand<KC>(tlane, wv);
@@ -1197,12 +1226,13 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_uscores(
       if (tid == 0 && iss_i < ntiles) issue_next();
       if (warp == 0) {
         if (elect_one()) {
-          if (first) {
+          if (first && !TM::SK) {
             mbar_wait(a_bsc, bsc_par);
             bsc_par ^= 1;
           }
           tc_fence_after();
-          issue_score_mma<KCI, KCO>(tbase, dsc0);
+          if constexpr (TM::SK) issue_score_mma_half<KCI, KCO, 1>(tbase, dsc0);
+          else issue_score_mma<KCI, KCO>(tbase, dsc0);
           tc_commit(a_sc);
         }
         __syncwarp();
@@ -1212,7 +1242,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_uscores(
       sc_ph ^= 1;
       tc_fence_after();
       float lg[4];
-      score_logits<KCO, NQ, L::cDsc>(tlane, qcs, nin, nout, lg);
+      score_logits<KCO, NQ, TM::cDsc>(tlane, qcs, nin, nout, lg);
       if (lt * kTile + tid < n) {
         float* lp = lbase + lt * kTile;
 #pragma unroll
@@ -1231,7 +1261,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 2 : 4) k_uscores(
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(L::kAlloc));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(TM::kAlloc));
 }
 
 // ------------------------------------------------------------------- host side
@@ -1272,7 +1302,7 @@ static int occupancy_dec() {
 template <int KCI, int KCO, int NQ>
 static int occupancy_sc() {
   static int occ = -1;
-  if (occ < 0) occ = resident_ctas(k_uscores<KCI, KCO, NQ>, Layout<KCI, KCO>::sTotal, Layout<KCI, KCO>::kAlloc);
+  if (occ < 0) occ = resident_ctas(k_uscores<KCI, KCO, NQ>, Layout<KCI, KCO>::sTotal, DecTmem<KCI, KCO>::kAlloc);
   return occ;
 }
 

@@ -615,12 +615,11 @@ int launch_prefill_profile(const void* keys, int dtype, int units, int64_t n0, i
 // 2 tokens x RPT rows of FMAs.  The fp64 FMA chain per (row, token) runs over c in increasing order.
 // ---------------------------------------------------------------------------
 constexpr int kQCk = 16;
-constexpr int kQThreads = 128;
 #ifndef QJL_QK_PRE
 #define QJL_QK_PRE 1
 #endif
 
-template <typename TK, typename TS, int RPT, int TOK>
+template <typename TK, typename TS, int RPT, int TOK, int kQThreads>
 __global__ void __launch_bounds__(kQThreads) k_quantize_keys_simt(
     const TK* __restrict__ keys, int64_t n, int64_t key_unit_stride, const TS* __restrict__ s_full,
     int64_t s_unit_stride, int d, int m_in, int m_out, const int32_t* __restrict__ channels, int h,
@@ -747,29 +746,27 @@ static int launch_qk_simt_2(const void* keys, int64_t n, int64_t kus, const void
                             int d, int m_in, int m_out, const int32_t* ch, int h,
                             const qjl_key_cache_t& kc, int64_t row_offset, cudaStream_t st) {
   const int m_total = m_in + m_out;
-  const int rpt = (m_total + kQThreads - 1) / kQThreads;
+  const int nt = m_total <= 256 ? 128 : 256;          // CTA threads: <= 4 sketch rows per thread
+  const int rpt = (m_total + nt - 1) / nt;
   const int tok = rpt <= 4 ? 16 : 8;                  // acc[RPT][TOK] in registers
-#define QJL_QK(R, TT)                                                                      \
-  if (rpt == R && tok == TT) {                                                             \
-    auto kern = k_quantize_keys_simt<TK, TS, R, TT>;                                       \
+#define QJL_QK(R, TT, NT)                                                                  \
+  if (nt == NT && rpt == R && tok == TT) {                                                 \
+    auto kern = k_quantize_keys_simt<TK, TS, R, TT, NT>;                                   \
     const size_t smem = ((size_t)TT * d + (size_t)(m_total + 1) * kQCk) * sizeof(double);  \
     dim3 grid((unsigned)((n + TT - 1) / TT), kc.units);                                    \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
     timing_begin(st);                                                                      \
-    kern<<<grid, kQThreads, smem, st>>>((const TK*)keys, n, kus, (const TS*)s, sus, d,     \
-                                        m_in, m_out, ch, h, kc, row_offset);               \
+    kern<<<grid, NT, smem, st>>>((const TK*)keys, n, kus, (const TS*)s, sus, d,            \
+                                 m_in, m_out, ch, h, kc, row_offset);                      \
     timing_end(st);                                                                        \
     QJL_LAUNCH_CHECK("quantize_keys_simt");                                                \
     return QJL_OK;                                                                         \
   }
-  QJL_QK(1, 16)
-  QJL_QK(2, 16)
-  QJL_QK(3, 16)
-  QJL_QK(4, 16)
-  QJL_QK(5, 8)
-  QJL_QK(6, 8)
-  QJL_QK(7, 8)
-  QJL_QK(8, 8)
+  QJL_QK(1, 16, 128)
+  QJL_QK(2, 16, 128)
+  QJL_QK(2, 16, 256)
+  QJL_QK(3, 16, 256)
+  QJL_QK(4, 16, 256)
 #undef QJL_QK
   set_error("quantize_keys: m_in + m_out = %d exceeds 1024", m_total);
   return QJL_ERR_UNSUPPORTED;

@@ -292,20 +292,28 @@ def measure_scores(cache, q, w, steps):
         cache.scores(q, out=logits)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
-        cache.scores(q, out=logits)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
+
+    def timed(chained):
+        e0.record()
+        for _ in range(steps):
+            cache.scores(q, out=logits, chained=chained)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    ms_unchained = timed(False)
+    # back-to-back steps chained with PDL, as the decode's `value` is (QJL_DECODE_CHAINED:
+    # the previous kernel on the stream is the previous step's score kernel)
+    ms = timed(True)
     kb = U * w["n"] * bytes_per_token_head(w, values=False)
     wb = U * G * w["n"] * 4
     peak, _, _ = load_peaks()
-    return {"ms_per_step": ms, "key_bytes": kb, "logit_bytes_written": wb,
+    return {"ms_per_step": ms, "ms_per_step_unchained": ms_unchained, "key_bytes": kb, "logit_bytes_written": wb,
             "gbs_key_bytes": kb / (ms * 1e-3) / 1e9, "frac_key_bytes": kb / (ms * 1e-3) / 1e9 / peak,
             "gbs_read_plus_write": (kb + wb) / (ms * 1e-3) / 1e9,
             "frac_read_plus_write": (kb + wb) / (ms * 1e-3) / 1e9 / peak,
-            "note": "scores-only K2 (prep + tcgen05 score kernel writing fp32 logits); algorithmic "
+            "note": "scores-only K2 (prep + tcgen05 score kernel writing fp32 logits), back-to-back "
+                    "steps chained with PDL (unchained: every prep waits for the stream); algorithmic "
                     "bytes = the key fields of the records (44 B/token-head at C3), plus the logits "
                     "written"}
 

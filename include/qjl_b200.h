@@ -66,7 +66,7 @@
 extern "C" {
 #endif
 
-#define QJL_ABI_VERSION 2
+#define QJL_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define QJL_API __attribute__((visibility("default")))
@@ -88,13 +88,13 @@ enum { QJL_VLAYOUT_U8 = 0, QJL_VLAYOUT_P2T = 2 };
 /* qjl_tile_record field indices */
 enum { QJL_REC_BITS_IN = 0, QJL_REC_BITS_OUT, QJL_REC_NORM_IN, QJL_REC_NORM_OUT, QJL_REC_CODES,
        QJL_REC_ZERO, QJL_REC_SCALE, QJL_REC_FIELDS };
-/* qjl_decode / qjl_decode_step flags */
+/* qjl_decode / qjl_decode_step / qjl_scores flags */
 enum {
-  /* The previous kernel on `stream` is a qjl_decode / qjl_decode_step of this library on the
-   * same workspace, and every input of this call (cache rows, q, k_new, v_new, sketch) was
+  /* The previous kernel on `stream` is a qjl_decode / qjl_decode_step / qjl_scores of this
+   * library, and every input of this call (cache rows, q, k_new, v_new, sketch) was
    * written before that launch: the query-sketch kernel may then read its inputs while the
    * previous decode drains (programmatic dependent launch).  Without it every read waits
-   * for the stream. */
+   * for the stream.  (qjl_scores: tensor-core path only; the generic path ignores it.) */
   QJL_DECODE_CHAINED = 1,
   /* Fixed 512-token segments per unit, merged in segment order: a unit's output bits depend
    * only on that unit (a unit-sharded decode equals the unsharded one bit for bit).  The
@@ -195,11 +195,12 @@ QJL_API int qjl_tensor_core_path(const qjl_key_cache_t* cache, const qjl_value_c
 
 /* K2: logits [units][G][n] (f32) of G query heads per unit over the first n keys.
  * Tile-major caches with m_in/32 in {8, 16}, m_out/32 in {0, 2, 4}, d == 128 and G <= 4
- * run the tensor-core score kernel; every other shape runs the generic kernel. */
+ * run the tensor-core score kernel; every other shape runs the generic kernel.
+ * flags: QJL_DECODE_CHAINED (ABI 3; other bits are rejected). */
 QJL_API size_t qjl_scores_workspace(int units, int G, int m_total);
 QJL_API int qjl_scores(const qjl_key_cache_t* cache, int64_t n, const void* q, int q_dtype, int G,
                const qjl_sketch_t* sketch, float* logits, void* workspace,
-               size_t workspace_bytes, void* stream);
+               size_t workspace_bytes, unsigned flags, void* stream);
 
 /* packed_sign_dot_batch: out f64 [G][n] = 2 * sum_{set bits of row i} values[g] - sum(values[g])
  * for n packed rows of m bits (row_bytes apart, m % 32 == 0), values f64 [G][m]. */

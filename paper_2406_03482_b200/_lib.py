@@ -59,7 +59,7 @@ SIGNATURES = {
     "qjl_sketch_query": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, P(SketchDesc), c_i32, c_i32, c_vp, c_vp]),
     "qjl_scores_workspace": (c_sz, [c_i32, c_i32, c_i32]),
     "qjl_scores": (c_i32, [P(KeyCacheDesc), c_i64, c_vp, c_i32, c_i32, P(SketchDesc), c_vp, c_vp,
-                           c_sz, c_vp]),
+                           c_sz, ctypes.c_uint, c_vp]),
     "qjl_sign_dot_batch": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_vp, c_i32, c_vp, c_vp]),
     "qjl_softmax_f64": (c_i32, [c_vp, c_i64, c_i64, c_dbl, c_vp, c_vp]),
     "qjl_decode_workspace": (c_sz, [P(KeyCacheDesc), P(ValueCacheDesc), c_i64, c_i32]),
@@ -104,7 +104,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype, fn.argtypes = res, args
-    if lib.qjl_abi_version() != 2:
+    if lib.qjl_abi_version() != 3:
         raise ImportError("qjl_b200 ABI version mismatch")
     _lib = lib
     return lib

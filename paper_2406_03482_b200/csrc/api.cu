@@ -311,8 +311,9 @@ size_t qjl_scores_workspace(int units, int G, int m_total) {
 
 int qjl_scores(const qjl_key_cache_t* cache, int64_t n, const void* q, int q_dtype, int G,
                const qjl_sketch_t* sketch, float* logits, void* workspace, size_t workspace_bytes,
-               void* stream) {
+               unsigned flags, void* stream) {
   QJL_TRY(check_key_cache(cache));
+  QJL_CHECK_ARG((flags & ~(unsigned)QJL_DECODE_CHAINED) == 0, "qjl_scores flags: QJL_DECODE_CHAINED only (got %u)", flags);
   QJL_TRY(check_sketch(sketch));
   QJL_CHECK_ARG(q && logits, "NULL pointer");
   QJL_CHECK_ARG(valid_dtype(q_dtype), "bad query dtype %d", q_dtype);
@@ -329,7 +330,7 @@ int qjl_scores(const qjl_key_cache_t* cache, int64_t n, const void* q, int q_dty
   }
   cudaStream_t st = (cudaStream_t)stream;
   if (cache->tile_stride > 0 && tile_path_supported(*cache, nullptr, G))
-    return launch_scores_tile(*cache, n, q, q_dtype, G, *sketch, logits, workspace, workspace_bytes, st);
+    return launch_scores_tile(*cache, n, q, q_dtype, G, *sketch, logits, workspace, workspace_bytes, flags, st);
   float* sq = (float*)workspace;
   float* sums = sq + (size_t)cache->units * G * m_total;
   QJL_TRY(launch_sketch_query(q, q_dtype, cache->units, G, cache->d, *sketch, cache->m_in, m_total,

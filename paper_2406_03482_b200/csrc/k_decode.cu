@@ -532,9 +532,10 @@ __device__ __forceinline__ void issue_score_mma_half(uint32_t tbase, uint64_t ds
   }
 }
 // logits (log2 domain) of the NQ heads from the score accumulators (kvcache.py:311-329)
+// (split in two: the accumulator read-back is issued, the caller waits (tcgen05.wait::ld),
+// then the arithmetic)
 template <int KCO, int NQ, int CDSC>
-__device__ __forceinline__ void score_logits(uint32_t tlane, const float4* qcs, float nin, float nout, float* lg) {
-  uint32_t dr[32];
+__device__ __forceinline__ void score_acc_load(uint32_t tlane, uint32_t* dr) {
   if (NQ == 4) {
     tmem_ld16(tlane + CDSC, dr);
     if (KCO) tmem_ld16(tlane + CDSC + 16, dr + 16);
@@ -545,7 +546,10 @@ __device__ __forceinline__ void score_logits(uint32_t tlane, const float4* qcs, 
     tmem_ld4(tlane + CDSC, dr);
     if (KCO) tmem_ld4(tlane + CDSC + 16, dr + 16);
   }
-  tmem_wait_ld();
+}
+template <int KCO, int NQ>
+__device__ __forceinline__ void score_logits_of(const uint32_t* dr, const float4* qcs, float nin, float nout,
+                                                float* lg) {
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int* di = reinterpret_cast<const int*>(dr + 4 * q);
@@ -559,6 +563,13 @@ __device__ __forceinline__ void score_logits(uint32_t tlane, const float4* qcs, 
     }
     lg[q] = l2;
   }
+}
+template <int KCO, int NQ, int CDSC>
+__device__ __forceinline__ void score_logits(uint32_t tlane, const float4* qcs, float nin, float nout, float* lg) {
+  uint32_t dr[32];
+  score_acc_load<KCO, NQ, CDSC>(tlane, dr);
+  tmem_wait_ld();
+  score_logits_of<KCO, NQ>(dr, qcs, nin, nout, lg);
 }
 
 // ----------------------------------------------------------------- main kernel
@@ -1110,6 +1121,9 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 3 : 4) k_udecode(
 }
 
 // ------------------------------------------------------------ scores-only K2
+#ifndef QJL_US_EARLY_TRIGGER
+#define QJL_US_EARLY_TRIGGER 1
+#endif
 // The score stage of the decode with logits written out (kvcache.py:311-329 ->
 // estimate_logits): stages hold the key fields of each record (one bulk copy), the
 // score accumulators become logits (natural-log units) stored coalesced per head.
@@ -1169,6 +1183,11 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 3 : 4) k_uscores(
   if (tid == 0)                                        // (early copies: see k_udecode)
     for (int i = 0; i < kStages && i < ntiles; ++i) issue_next();
   asm volatile("griddepcontrol.wait;" ::: "memory");   // Bsc / qconst come from k_uprep
+#if QJL_US_EARLY_TRIGGER
+  // the next step's query sketch may launch now: it takes the SMs this grid's CTAs leave,
+  // and (chained) computes while this grid drains; its workspace writes wait for our exit
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   const float4* qcs = reinterpret_cast<const float4*>(sm + L::sQc);
   const int64_t n = P.n;
   uint32_t sc_ph = 0, bsc_par = 0, full_ph = 0, sk_ph = 0;
@@ -1181,12 +1200,93 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 3 : 4) k_uscores(
       mbar_expect_tx(a_bsc, L::NH * 2048);
       bulk_g2s(s_sm, P.bsc + (size_t)u * L::NH * 2048, L::NH * 2048, a_bsc);
     }
-    bool first = true;
     float* const lbase = P.logits + (int64_t)u * P.G * n + tid;      // this unit's rows, this token
+    if constexpr (!TM::SK) {
+      // Software-pipelined over the unit's tiles: tile i+1's sign words are loaded while
+      // MMA(i) runs, stored as the next A operand once MMA(i) is done (same columns), and
+      // MMA(i+1) is issued before tile i's logits are computed and stored.
+      float nin, nout;
+      {
+        mbar_wait(a_full + 8 * s, full_ph);
+        const uint8_t* st = sm + L::sStage + s * L::kKeyRec;
+        uint32_t wv[KC];
+        load_sign_words<KCI, KCO>(st, tid, wv);
+        store_sign_operand<KC>(tlane, wv);
+        nin = __half2float(reinterpret_cast<const __half*>(st + L::oNormIn)[tid]);
+        nout = KCO ? __half2float(reinterpret_cast<const __half*>(st + L::oNormOut)[tid]) : 0.f;
+        tmem_wait_st();
+        tc_fence_before();
+        bar_sync(1, kThreads);                  // A operand in TMEM; the stage is fully read
+        if (tid == 0 && iss_i < ntiles) issue_next();
+        if (warp == 0) {
+          if (elect_one()) {
+            mbar_wait(a_bsc, bsc_par);
+            tc_fence_after();
+            issue_score_mma<KCI, KCO>(tbase, dsc0);
+            tc_commit(a_sc);
+          }
+          __syncwarp();
+        }
+        bsc_par ^= 1;
+        if (++s == kStages) {
+          s = 0;
+          full_ph ^= 1;
+        }
+      }
+      for (; it < seg_end; ++it, ++lt) {
+        const bool nxt = it + 1 < seg_end;
+        uint32_t wv[KC];
+        float nin_n = 0.f, nout_n = 0.f;
+        if (nxt) {
+          mbar_wait(a_full + 8 * s, full_ph);
+          const uint8_t* st = sm + L::sStage + s * L::kKeyRec;
+          load_sign_words<KCI, KCO>(st, tid, wv);
+          nin_n = __half2float(reinterpret_cast<const __half*>(st + L::oNormIn)[tid]);
+          nout_n = KCO ? __half2float(reinterpret_cast<const __half*>(st + L::oNormOut)[tid]) : 0.f;
+        }
+        mbar_wait(a_sc, sc_ph);
+        sc_ph ^= 1;
+        tc_fence_after();
+        uint32_t dr[32];
+        score_acc_load<KCO, NQ, TM::cDsc>(tlane, dr);
+        if (nxt) store_sign_operand<KC>(tlane, wv);
+        tmem_wait_ld();
+        tmem_wait_st();
+        tc_fence_before();
+        bar_sync(1, kThreads);                  // D(i) read by all; A(i+1) stored; its stage read
+        if (nxt) {
+          if (tid == 0 && iss_i < ntiles) issue_next();
+          if (warp == 0) {
+            if (elect_one()) {
+              tc_fence_after();
+              issue_score_mma<KCI, KCO>(tbase, dsc0);
+              tc_commit(a_sc);
+            }
+            __syncwarp();
+          }
+          if (++s == kStages) {
+            s = 0;
+            full_ph ^= 1;
+          }
+        }
+        float lg[4];
+        score_logits_of<KCO, NQ>(dr, qcs, nin, nout, lg);
+        if (lt * kTile + tid < n) {
+          float* lp = lbase + lt * kTile;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+            if (q < P.G) __stcs(lp + q * n, lg[q] * kLn2);
+        }
+        nin = nin_n;
+        nout = nout_n;
+      }
+      tc_fence_before();
+    } else {
+    bool first = true;
     for (; it < seg_end; ++it, ++lt) {
       mbar_wait(a_full + 8 * s, full_ph);
       const uint8_t* st = sm + L::sStage + s * L::kKeyRec;
-      if constexpr (TM::SK) {
+      {
         {
           uint32_t wv[TM::KH];
           load_sign_range<KCI, KCO, 0, TM::KH>(st, tid, wv);
@@ -1213,10 +1313,6 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 3 : 4) k_uscores(
         sk_ph ^= 1;
         tc_fence_after();
         store_sign_operand<KC - TM::KH>(tlane, wv);
-      } else {
-        uint32_t wv[KC];
-        load_sign_words<KCI, KCO>(st, tid, wv);
-        store_sign_operand<KC>(tlane, wv);
       }
       const float nin = __half2float(reinterpret_cast<const __half*>(st + L::oNormIn)[tid]);
       const float nout = KCO ? __half2float(reinterpret_cast<const __half*>(st + L::oNormOut)[tid]) : 0.f;
@@ -1255,10 +1351,13 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 3 : 4) k_uscores(
         full_ph ^= 1;
       }
     }
+    }
     ++u;
     lt = 0;
   }
+#if !QJL_US_EARLY_TRIGGER
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(TM::kAlloc));
@@ -1607,8 +1706,9 @@ int launch_decode_step_tile(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
 }
 
 int launch_scores_tile(const qjl_key_cache_t& kc, int64_t n, const void* q, int q_dtype, int G,
-                       const qjl_sketch_t& sk, float* logits, void* ws, size_t ws_bytes, cudaStream_t st) {
-  ud::Launch a{&kc, n, q, q_dtype, G, &sk, 1.f, nullptr, nullptr, logits, ws, 0, nullptr, 1, 0, nullptr};
+                       const qjl_sketch_t& sk, float* logits, void* ws, size_t ws_bytes, unsigned flags,
+                       cudaStream_t st) {
+  ud::Launch a{&kc, n, q, q_dtype, G, &sk, 1.f, nullptr, nullptr, logits, ws, flags, nullptr, 1, 0, nullptr};
   return ud::launch_any(a, ws_bytes, st);
 }
 

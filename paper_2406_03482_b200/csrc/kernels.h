@@ -62,7 +62,8 @@ int launch_decode_step_tile(const qjl_key_cache_t& kc, const qjl_value_cache_t& 
                             const void* k_new, const void* v_new, float inv_t, float* out, float* lse,
                             float* logits, void* ws, size_t ws_bytes, unsigned flags, cudaStream_t st);
 int launch_scores_tile(const qjl_key_cache_t& kc, int64_t n, const void* q, int q_dtype, int G,
-                       const qjl_sketch_t& sk, float* logits, void* ws, size_t ws_bytes, cudaStream_t st);
+                       const qjl_sketch_t& sk, float* logits, void* ws, size_t ws_bytes, unsigned flags,
+                       cudaStream_t st);
 int bench_decode_tile(const qjl_key_cache_t& kc, int64_t n, const void* q, int q_dtype, int G, const qjl_sketch_t& sk,
                       float inv_t, float* out, float* lse, void* ws, size_t ws_bytes, unsigned flags, int reps,
                       float* ms, cudaStream_t st);

@@ -410,8 +410,11 @@ class DeviceKeyCache:
                                              out.data_ptr(), _stream()), "sketch_query")
         return out
 
-    def scores(self, q: torch.Tensor, n: int | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
-        """K2: logits [U, G, n] f32 (kvcache.py:311-329)."""
+    def scores(self, q: torch.Tensor, n: int | None = None, out: torch.Tensor | None = None,
+               chained: bool = False) -> torch.Tensor:
+        """K2: logits [U, G, n] f32 (kvcache.py:311-329).  `chained`: as for `decode`
+        (QJL_DECODE_CHAINED) -- the previous kernel on the stream is this library's scores or
+        decode and every input predates it."""
         s = self.shape
         q = self._check_q(q)
         n = self.n if n is None else n
@@ -423,7 +426,7 @@ class DeviceKeyCache:
         kd, sd = self.key_desc(), self.sketch_desc()
         _lib.check(self.lib.qjl_scores(ctypes.byref(kd), n, q.data_ptr(), _TORCH2QJL[q.dtype], G,
                                        ctypes.byref(sd), out.data_ptr(), ws.data_ptr(), ws.numel(),
-                                       _stream()), "scores")
+                                       _lib.QJL_DECODE_CHAINED if chained else 0, _stream()), "scores")
         return out
 
     def decode_workspace_bytes(self, G: int, n: int | None = None) -> int:

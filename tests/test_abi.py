@@ -28,7 +28,7 @@ def test_library_exports_every_symbol():
     lib = _lib.load()
     for name in header_symbols():
         assert hasattr(lib, name), name
-    assert lib.qjl_abi_version() == 2
+    assert lib.qjl_abi_version() == 3
     assert lib.qjl_status_string(-1) == b"invalid argument"
 
 

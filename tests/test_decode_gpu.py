@@ -107,6 +107,24 @@ def test_determinism_and_chaining(cuda):
     assert _close(o1, d1)
 
 
+def test_scores_chaining(cuda):
+    """qjl_scores with QJL_DECODE_CHAINED (PDL: the query sketch overlaps the previous score
+    or decode kernel) writes the same logits as unchained calls, including after a decode
+    and with a different query (the previous kernel still reads the workspace)."""
+    c, q = make_cache(8, 5000, 4, 8, 256, 64, seed=12)
+    q2 = torch.flip(q, dims=[0]).contiguous()
+    l1 = c.scores(q).clone()
+    m1 = c.scores(q2).clone()
+    l2 = c.scores(q, chained=True).clone()
+    m2 = c.scores(q2, chained=True).clone()
+    c.decode(q)
+    l3 = c.scores(q, chained=True).clone()
+    m3 = c.scores(q2, chained=True)
+    assert torch.equal(l1, l2) and torch.equal(l1, l3)
+    assert torch.equal(m1, m2) and torch.equal(m1, m3)
+    assert not torch.equal(l1, m1)
+
+
 def test_bench_hook_runs_the_same_kernel(cuda):
     c, q = make_cache(16, 3000, 4, 8, 256, 64, seed=5)
     ref = c.decode(q).clone()

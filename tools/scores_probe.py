@@ -23,7 +23,7 @@ torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(reps):
-    c.scores(q, out=out)
+    c.scores(q, out=out, chained=True)
 e1.record()
 torch.cuda.synchronize()
 print(f"scores: {e0.elapsed_time(e1) / reps * 1e3:.1f} us/step")

@@ -674,6 +674,36 @@ def run_gpu(args):
         torch.cuda.synchronize()
         zc_ms = e2.elapsed_time(e3)
 
+    # hybrid variant (N = 1): the query-sketch kernel reads the step's query straight from
+    # pinned host memory (H2D by the kernel's loads, overlapping the previous decode under
+    # PDL), each step decodes into its own device buffer, and the copy stream reads it back
+    # after that step's decode -- the compute stream never waits, so the PDL chain holds
+    hy_ms, hy_ok = None, None
+    if world == 1:
+        nbuf = args.steps
+        odh = [torch.empty_like(out) for _ in range(nbuf)]
+        ohh = [torch.empty(out.shape, dtype=out.dtype).pin_memory() for _ in range(nbuf)]
+        evs = [torch.cuda.Event() for _ in range(nbuf)]
+
+        def hybrid_steps(k):
+            for i in range(k):
+                cache.decode(qh, out=odh[i], chained=i > 0)
+                evs[i].record(comp)
+                with torch.cuda.stream(copy):
+                    copy.wait_event(evs[i])
+                    ohh[i].copy_(odh[i], non_blocking=True)
+            comp.wait_stream(copy)
+
+        hybrid_steps(min(args.warmup, nbuf))
+        torch.cuda.synchronize()
+        e2.record()
+        hybrid_steps(args.steps)
+        e3.record()
+        torch.cuda.synchronize()
+        hy_ms = e2.elapsed_time(e3)
+        hy_ok = bool(((ohh[-1].double() - _ref).norm() <= 1e-5 * _ref.norm()).item())
+        del odh, ohh
+
     # ---- K2 scores-only and K1 prefill (sharded like the decode)
     scores = measure_scores(cache, q, w, max(20, args.steps // 4)) if not args.no_extras else None
     prefill = None
@@ -736,6 +766,22 @@ def run_gpu(args):
     }
     if zc_ms is not None:
         res["e2e"]["zero_copy_gbs"] = alg_bytes * args.steps / (zc_ms * 1e-3) / 1e9
+    if hy_ms is not None:
+        # N = 1: the e2e value is the pipelined form (the query read from pinned host memory
+        # by the query-sketch kernel, a device output per step read back on the copy stream);
+        # the double-buffered copy form above stays beside it as `copy_gbs`
+        res["e2e"]["copy_gbs"] = e2e_val
+        res["e2e"]["copy_output_ok"] = e2e_ok
+        res["e2e"]["value"] = alg_bytes * args.steps / (hy_ms * 1e-3) / 1e9
+        res["e2e"]["output_ok"] = hy_ok
+        res["e2e"]["note"] = (
+            "per step, all in the timed region: the query (H2D bytes) read from pinned host memory "
+            "by the query-sketch kernel of DeviceKeyCache.decode (PDL-chained on the previous "
+            "step), the decode into that step's device output, and a D2H copy of the [units, G, d] "
+            "output into pinned host memory on a side stream after that step's decode; the compute "
+            "stream never waits. copy_gbs: the query uploaded by cudaMemcpyAsync on a side stream "
+            "(double-buffered, event waits on the compute stream; the N > 1 form, with the NCCL "
+            "all_gather); zero_copy_gbs: decode on the pinned host buffers themselves")
     if scores:
         scores["ms_per_step"] = sc_ms
         kb = U_all * w["n"] * bytes_per_token_head(w, values=False)

@@ -1128,7 +1128,7 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 3 : 4) k_udecode(
 // estimate_logits): stages hold the key fields of each record (one bulk copy), the
 // score accumulators become logits (natural-log units) stored coalesced per head.
 template <int KCI, int KCO, int NQ>
-__global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 3 : 4) k_uscores(const Params P) {
+__global__ void __launch_bounds__(kThreads, 4) k_uscores(const Params P) {
   using L = Layout<KCI, KCO>;
   using TM = DecTmem<KCI, KCO>;                 // m_in = 512: split-K score MMA, 128 TMEM columns
   constexpr int KC = KCI + KCO;
@@ -1282,75 +1282,102 @@ __global__ void __launch_bounds__(kThreads, (KCI + KCO > 12) ? 3 : 4) k_uscores(
       }
       tc_fence_before();
     } else {
-    bool first = true;
-    for (; it < seg_end; ++it, ++lt) {
-      mbar_wait(a_full + 8 * s, full_ph);
-      const uint8_t* st = sm + L::sStage + s * L::kKeyRec;
+      // split-K (m_in = 512): the same pipeline with the two K halves of each tile's MMA --
+      // the second half's A columns overlap the first half's, so they wait for it
+      float nin, nout;
+      auto stage_in = [&](const uint8_t* st, bool first_tile) {
+        uint32_t wv[KC - TM::KH];
+        load_sign_range<KCI, KCO, TM::KH, KC>(st, tid, wv);
+        mbar_wait(a_sk, sk_ph);                 // the first half's A columns are free
+        sk_ph ^= 1;
+        tc_fence_after();
+        store_sign_operand<KC - TM::KH>(tlane, wv);
+        tmem_wait_st();
+        tc_fence_before();
+        bar_sync(1, kThreads);                  // A (second half) in TMEM; the stage is fully read
+        if (tid == 0 && iss_i < ntiles) issue_next();
+        if (warp == 0) {
+          if (elect_one()) {
+            tc_fence_after();
+            issue_score_mma_half<KCI, KCO, 1>(tbase, dsc0);
+            tc_commit(a_sc);
+          }
+          __syncwarp();
+        }
+        if (++s == kStages) {
+          s = 0;
+          full_ph ^= 1;
+        }
+      };
       {
+        mbar_wait(a_full + 8 * s, full_ph);
+        const uint8_t* st = sm + L::sStage + s * L::kKeyRec;
         {
           uint32_t wv[TM::KH];
           load_sign_range<KCI, KCO, 0, TM::KH>(st, tid, wv);
           store_sign_operand<TM::KH>(tlane, wv);
         }
+        nin = __half2float(reinterpret_cast<const __half*>(st + L::oNormIn)[tid]);
+        nout = KCO ? __half2float(reinterpret_cast<const __half*>(st + L::oNormOut)[tid]) : 0.f;
         tmem_wait_st();
         tc_fence_before();
         bar_sync(1, kThreads);
         if (warp == 0) {
           if (elect_one()) {
-            if (first) {
-              mbar_wait(a_bsc, bsc_par);
-              bsc_par ^= 1;
-            }
+            mbar_wait(a_bsc, bsc_par);
             tc_fence_after();
             issue_score_mma_half<KCI, KCO, 0>(tbase, dsc0);
             tc_commit(a_sk);
           }
           __syncwarp();
         }
-        uint32_t wv[KC - TM::KH];
-        load_sign_range<KCI, KCO, TM::KH, KC>(st, tid, wv);
-        mbar_wait(a_sk, sk_ph);
-        sk_ph ^= 1;
-        tc_fence_after();
-        store_sign_operand<KC - TM::KH>(tlane, wv);
+        bsc_par ^= 1;
+        stage_in(st, true);
       }
-      const float nin = __half2float(reinterpret_cast<const __half*>(st + L::oNormIn)[tid]);
-      const float nout = KCO ? __half2float(reinterpret_cast<const __half*>(st + L::oNormOut)[tid]) : 0.f;
-      tmem_wait_st();
-      tc_fence_before();
-      bar_sync(1, kThreads);                    // A operand in TMEM; the stage is fully read
-      if (tid == 0 && iss_i < ntiles) issue_next();
-      if (warp == 0) {
-        if (elect_one()) {
-          if (first && !TM::SK) {
-            mbar_wait(a_bsc, bsc_par);
-            bsc_par ^= 1;
-          }
-          tc_fence_after();
-          if constexpr (TM::SK) issue_score_mma_half<KCI, KCO, 1>(tbase, dsc0);
-          else issue_score_mma<KCI, KCO>(tbase, dsc0);
-          tc_commit(a_sc);
+      for (; it < seg_end; ++it, ++lt) {
+        const bool nxt = it + 1 < seg_end;
+        uint32_t wv[TM::KH];
+        float nin_n = 0.f, nout_n = 0.f;
+        const uint8_t* st = sm + L::sStage + s * L::kKeyRec;
+        if (nxt) {
+          mbar_wait(a_full + 8 * s, full_ph);
+          load_sign_range<KCI, KCO, 0, TM::KH>(st, tid, wv);
+          nin_n = __half2float(reinterpret_cast<const __half*>(st + L::oNormIn)[tid]);
+          nout_n = KCO ? __half2float(reinterpret_cast<const __half*>(st + L::oNormOut)[tid]) : 0.f;
         }
-        __syncwarp();
-      }
-      first = false;
-      mbar_wait(a_sc, sc_ph);
-      sc_ph ^= 1;
-      tc_fence_after();
-      float lg[4];
-      score_logits<KCO, NQ, TM::cDsc>(tlane, qcs, nin, nout, lg);
-      if (lt * kTile + tid < n) {
-        float* lp = lbase + lt * kTile;
+        mbar_wait(a_sc, sc_ph);
+        sc_ph ^= 1;
+        tc_fence_after();
+        uint32_t dr[32];
+        score_acc_load<KCO, NQ, TM::cDsc>(tlane, dr);
+        if (nxt) store_sign_operand<TM::KH>(tlane, wv);
+        tmem_wait_ld();
+        tmem_wait_st();
+        tc_fence_before();
+        bar_sync(1, kThreads);                  // D(i) read by all; A(i+1) first half stored
+        if (nxt) {
+          if (warp == 0) {
+            if (elect_one()) {
+              tc_fence_after();
+              issue_score_mma_half<KCI, KCO, 0>(tbase, dsc0);
+              tc_commit(a_sk);
+            }
+            __syncwarp();
+          }
+          stage_in(st, false);
+        }
+        float lg[4];
+        score_logits_of<KCO, NQ>(dr, qcs, nin, nout, lg);
+        if (lt * kTile + tid < n) {
+          float* lp = lbase + lt * kTile;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q)
-          if (q < P.G) __stcs(lp + q * n, lg[q] * kLn2);
+          for (int q = 0; q < NQ; ++q)
+            if (q < P.G) __stcs(lp + q * n, lg[q] * kLn2);
+        }
+        nin = nin_n;
+        nout = nout_n;
       }
       tc_fence_before();
-      if (++s == kStages) {
-        s = 0;
-        full_ph ^= 1;
-      }
-    }
     }
     ++u;
     lt = 0;

@@ -6,6 +6,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_ptx.cuh"
 
 namespace qjl {
 
@@ -60,6 +61,7 @@ __global__ void __launch_bounds__(1024) k_detect_outliers(const T* __restrict__ 
 // block partials in a fixed order, then ranks.  |bf16| / |fp16| sums are exact in
 // fp64 at these lengths, so the result does not depend on the split.
 constexpr int kDetRows = 256;
+constexpr int kDetBulkD = 128;     // 16-bit keys with d <= this: bulk-copied row blocks (<= 64 KB)
 
 // |x| as fp64 without the F2F conversion pipe: for a normal 16-bit float the fp64 bit
 // pattern is the magnitude bits shifted into place plus an exponent rebias (exact);
@@ -77,28 +79,90 @@ __device__ __forceinline__ double abs_f64_bits(__half x) {
 __device__ __forceinline__ double abs_f64_bits(float x) { return fabs((double)x); }
 __device__ __forceinline__ double abs_f64_bits(double x) { return fabs(x); }
 
+// |x| of the 8 16-bit floats of one 16-byte vector, added to acc as fp64 values scaled by
+// 2^-kDetShift: the magnitude bits are shifted into the high word of an fp64 whose low word
+// is 0 and NO exponent rebias is added.  A normal 1.M x 2^(E - bias16) becomes
+// 1.M x 2^(E - 1023), a subnormal 0.M x 2^(1 - bias16) becomes the fp64 subnormal
+// 0.M x 2^-1022, and zero stays zero: every input, subnormals included, lands on the same
+// power-of-two scaling, exactly, with two integer ops and no conversion unit.  The sums
+// equal the unscaled ones times 2^-kDetShift bit for bit (the scaled values are exact, and
+// sums that fall below 2^-1022 are exact multiples of 2^-1074); callers multiply back.
+template <typename T> struct DetScaled;
+template <> struct DetScaled<__nv_bfloat16> {
+  static constexpr int kShift = 1023 - 127;                      // 2^-896
+  static __device__ __forceinline__ int lo(uint32_t w) { return (int)((w << 13) & 0x0FFFE000u); }
+  static __device__ __forceinline__ int hi(uint32_t w) { return (int)((w >> 3) & 0x0FFFE000u); }
+};
+template <> struct DetScaled<__half> {
+  static constexpr int kShift = 1023 - 15;                       // 2^-1008
+  static __device__ __forceinline__ int lo(uint32_t w) { return (int)((w << 10) & 0x01FFFC00u); }
+  static __device__ __forceinline__ int hi(uint32_t w) { return (int)((w >> 6) & 0x01FFFC00u); }
+};
+template <typename T>
+__device__ __forceinline__ void add_abs_scaled(const uint4& raw, double* acc) {
+  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    acc[2 * k] += __hiloint2double(DetScaled<T>::lo(w[k]), 0);
+    acc[2 * k + 1] += __hiloint2double(DetScaled<T>::hi(w[k]), 0);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_detect_partial(const T* __restrict__ keys, int64_t n0, int d,
                                                         int64_t unit_stride, double* __restrict__ part) {
   constexpr int EPV = 16 / (int)sizeof(T);
-  extern __shared__ double sm_part[];             // [rows_par][d]
+  const bool bulk = sizeof(T) == 2 && d <= kDetBulkD;   // the block's rows arrive by one bulk copy
+  extern __shared__ __align__(16) double sm_part[];   // [rows_par][d]; 16-bit keys: first the rows
+  __shared__ __align__(8) uint64_t bar;
   const int u = blockIdx.y, blk = blockIdx.x;
   const int tpr = d / EPV;                        // threads per row
   const int rows_par = blockDim.x / tpr;
   const int cg = threadIdx.x % tpr, rs = threadIdx.x / tpr;
   const T* K = keys + (int64_t)u * unit_stride;
+  const int64_t r0 = (int64_t)blk * kDetRows, r_end = min(r0 + kDetRows, n0);
   double acc[EPV];
 #pragma unroll
   for (int e = 0; e < EPV; ++e) acc[e] = 0.0;
-  if (rs < rows_par) {
-    const int64_t r_end = min((int64_t)(blk + 1) * kDetRows, n0);
+  if (bulk) {
+    // the 256 rows (contiguous, 64 KB at d = 128) land in shared memory with no registers
+    // held per load: 3 CTAs per SM keep ~190 KB in flight, which a register-staged loop
+    // (the per-element subnormal test serialises its loads) does not reach
+    const uint32_t b = ptx::smem_u32(&bar), dst = ptx::smem_u32(sm_part);
+    if (threadIdx.x == 0) {
+      ptx::mbar_init(b, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = (uint32_t)((r_end - r0) * d * (int64_t)sizeof(T));
+      ptx::mbar_expect_tx(b, bytes);
+      ptx::bulk_g2s(dst, K + r0 * d, bytes, b);
+    }
+    ptx::mbar_wait(b, 0);
+    const T* rows = reinterpret_cast<const T*>(sm_part);
+    if (rs < rows_par) {
+      for (int64_t r = rs; r < r_end - r0; r += rows_par) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(rows + r * d + cg * EPV);
+        if constexpr (sizeof(T) == 2) add_abs_scaled<T>(raw, acc);
+      }
+    }
+    if constexpr (sizeof(T) == 2) {
+      const double unscale = ldexp(1.0, DetScaled<T>::kShift);   // exact
+#pragma unroll
+      for (int e = 0; e < EPV; ++e) acc[e] *= unscale;
+    }
+    __syncthreads();                              // the rows are consumed; sm_part is reused
+  } else if (rs < rows_par) {
 #pragma unroll 4
-    for (int64_t r = (int64_t)blk * kDetRows + rs; r < r_end; r += rows_par) {
+    for (int64_t r = r0 + rs; r < r_end; r += rows_par) {
       const uint4 raw = __ldg(reinterpret_cast<const uint4*>(K + r * d + cg * EPV));
       const T* v = reinterpret_cast<const T*>(&raw);
 #pragma unroll
       for (int e = 0; e < EPV; ++e) acc[e] += abs_f64_bits(v[e]);
     }
+  }
+  if (rs < rows_par) {
 #pragma unroll
     for (int e = 0; e < EPV; ++e) sm_part[rs * d + cg * EPV + e] = acc[e];
   }
@@ -108,6 +172,14 @@ __global__ void __launch_bounds__(256) k_detect_partial(const T* __restrict__ ke
     for (int i = 0; i < rows_par; ++i) t += sm_part[i * d + c];
     part[((int64_t)u * gridDim.x + blk) * d + c] = t;
   }
+}
+
+// dynamic shared memory of k_detect_partial: the per-row-slot partials, and for 16-bit keys
+// the block's rows
+static size_t det_partial_smem(int d, size_t es, int rows_par) {
+  const size_t a = (size_t)rows_par * d * sizeof(double);
+  const size_t b = es == 2 && d <= kDetBulkD ? (size_t)kDetRows * d * es : 0;
+  return a > b ? a : b;
 }
 
 // Channel means from the block partials with all 1024 threads: P = 1024 / d chunks of
@@ -220,7 +292,7 @@ int launch_detect_outliers(const void* keys, int dtype, int units, int64_t n0, i
     const int rc = detect_part(ws, ws_bytes, (size_t)units * nblk * d * sizeof(double), st, &part, &owned);
     if (rc != QJL_OK) return rc;
     const int tpr = (int)(d * es / 16), rows_par = 256 / tpr;
-    const size_t smem = (size_t)rows_par * d * sizeof(double);
+    const size_t smem = det_partial_smem(d, es, rows_par);
     dim3 grid(nblk, units);
     switch (dtype) {
 #define QJL_DETP(DT)                                                                             \
@@ -549,7 +621,7 @@ int launch_prefill_profile(const void* keys, int dtype, int units, int64_t n0, i
   const int prc = detect_part(ws, ws_bytes, (size_t)units * nblk * d * sizeof(double), st, &part, &owned);
   if (prc != QJL_OK) return prc;
   const int tpr = (int)(d * es / 16), rows_par = 256 / tpr;
-  const size_t smem = (size_t)rows_par * d * sizeof(double);
+  const size_t smem = det_partial_smem(d, es, rows_par);
   dim3 grid(nblk, units);
   switch (dtype) {
 #define QJL_PPP(DT)                                                                                  \

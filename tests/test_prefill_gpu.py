@@ -97,3 +97,35 @@ def test_prefill_c4_bitwise(cuda):
     c.prefill_profile(keys)
     assert torch.equal(c.channels, b.channels) and torch.equal(c.magnitudes, b.magnitudes)
     assert torch.equal(c.s_full, b.s_full)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_detection_exact_with_subnormals_and_zeros(cuda, dtype):
+    """The detection kernel adds |x| of 16-bit keys as power-of-two-scaled fp64 values built
+    from the magnitude bits (no conversion unit): zeros, subnormals and normals must come
+    out as the exact channel means.  Channel groups: subnormals only, subnormals mixed with
+    zeros, zeros only, tiny normals, and wide normals -- each group's span keeps its fp64
+    sums exact, so the device means equal fsum(|x|) / n bit for bit in any summation order."""
+    import math
+    U, n0, d = 3, 1000, 128
+    g = torch.Generator().manual_seed(5)
+    fi = torch.finfo(dtype)
+    sub = fi.smallest_normal / (2 ** (7 if dtype == torch.bfloat16 else 10))   # smallest subnormal
+    k = torch.empty(U, n0, d, dtype=torch.float64)
+    code = torch.randint(1, 128, (U, n0, d), generator=g).double()
+    sign = torch.where(torch.rand(U, n0, d, generator=g) < 0.5, -1.0, 1.0).double()
+    k[..., 0:32] = code[..., 0:32] * sub                                  # subnormals
+    k[..., 32:48] = code[..., 32:48] * sub * (torch.rand(U, n0, 16, generator=g) < 0.5)   # + zeros
+    k[..., 48:56] = 0.0
+    k[..., 56:80] = torch.rand(U, n0, 24, generator=g).double() * 64 * fi.smallest_normal
+    k[..., 80:] = torch.randn(U, n0, d - 80, generator=g).double() * 8
+    k = (k * sign).to(dtype)
+    c = DeviceKeyCache.create(U, d, 256, h=8, m_out=64, capacity=n0, key_dtype=dtype, with_values=False)
+    c.detect_outliers(k.to("cuda"))
+    got = c.magnitudes.cpu().numpy()
+    kh = k.double().abs().numpy()
+    for u in range(U):
+        want = np.array([math.fsum(kh[u, :, j]) / n0 for j in range(d)])
+        assert np.array_equal(got[u], want), np.flatnonzero(got[u] != want)[:8]
+        ch, mags = O.detect_outliers(k[u].double().numpy(), 8)
+        assert tuple(c.channels[u].cpu().tolist()) == ch

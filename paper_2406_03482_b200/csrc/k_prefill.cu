@@ -115,6 +115,9 @@ __global__ void __launch_bounds__(256) k_detect_partial(const T* __restrict__ ke
   const bool bulk = sizeof(T) == 2 && d <= kDetBulkD;   // the block's rows arrive by one bulk copy
   extern __shared__ __align__(16) double sm_part[];   // [rows_par][d]; 16-bit keys: first the rows
   __shared__ __align__(8) uint64_t bar;
+  // the finish kernel may launch now: it stages its sketch rows while this grid drains, and
+  // waits (griddepcontrol.wait) for the partials
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int u = blockIdx.y, blk = blockIdx.x;
   const int tpr = d / EPV;                        // threads per row
   const int rows_par = blockDim.x / tpr;
@@ -421,28 +424,13 @@ __global__ void __launch_bounds__(1024, 1) k_detect_finish_build(
   // grid (units, row slices): every CTA of a unit re-derives the ranking from the partials
   // (parallel, cheap) and builds its slice of S_full rows; slice 0 publishes channels and
   // magnitudes
+  // K1 (launched next with programmatic serialization) may start its setup now
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int u = blockIdx.x, c = threadIdx.x;
   const bool publish = blockIdx.y == 0;
 #ifndef QJL_FB_ABLATE
 #define QJL_FB_ABLATE 0      // perf experiments: 1 skip the build, 2 skip the ranking too
 #endif
-  channel_means(part, u, nblk, d, n0, mag, red);
-  if (QJL_FB_ABLATE & 2) return;
-  channel_ranks(mag, d, rank);
-  // outlier flags as one bit per channel (warp ballots) -> prefix counts by popc
-  const bool is_out = c < d && rank[c] < h;
-  const unsigned bal = __ballot_sync(0xffffffffu, is_out);
-  if ((c & 31) == 0 && c < d) below[c >> 5] = (int)bal;
-  if (c < d && magnitudes && publish) magnitudes[(int64_t)u * d + c] = mag[c];
-  __syncthreads();
-  if (c < d) {
-    // ascending position among the outliers / among the inliers (kvcache.py:90-101)
-    int nb = __popc((unsigned)below[c >> 5] & ((1u << (c & 31)) - 1u));
-    for (int w = 0; w < (c >> 5); ++w) nb += __popc((unsigned)below[w]);
-    if (is_out && publish) channels[(int64_t)u * h + nb] = c;
-    src[c] = is_out ? -1 - nb : c - nb;
-  }
-  __syncthreads();
   const int m_total = m_in + m_out, d_in = d - h;
   const int r0 = (int)((int64_t)blockIdx.y * m_total / gridDim.y);
   const int r1 = (int)((int64_t)(blockIdx.y + 1) * m_total / gridDim.y);
@@ -461,7 +449,6 @@ __global__ void __launch_bounds__(1024, 1) k_detect_finish_build(
            n_el * (int64_t)sizeof(TS) < (1 << 20);
   };
   TS* s_out_rows = s_rows + (((int64_t)nin * d_in * sizeof(TS) + 15) / 16 * 16) / sizeof(TS);
-  if (QJL_FB_ABLATE & 1) return;
   const TS* src_a = s_in + (int64_t)ia * d_in;
   const TS* src_b = s_out + (int64_t)oa * h;
   const int64_t na = (int64_t)nin * d_in, nb = (int64_t)nout * h;
@@ -488,6 +475,26 @@ __global__ void __launch_bounds__(1024, 1) k_detect_finish_build(
     for (int64_t i = threadIdx.x; i < na; i += blockDim.x) s_rows[i] = src_a[i];
   if (nout && !bulk_b && !(QJL_FB_ABLATE & 4))
     for (int64_t i = threadIdx.x; i < nb; i += blockDim.x) s_out_rows[i] = src_b[i];
+  // PDL: the staging above reads only the sketches (inputs of the call); the partials come
+  // from k_detect_partial, launched just before with programmatic serialization
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  channel_means(part, u, nblk, d, n0, mag, red);
+  if (QJL_FB_ABLATE & 2) return;
+  channel_ranks(mag, d, rank);
+  // outlier flags as one bit per channel (warp ballots) -> prefix counts by popc
+  const bool is_out = c < d && rank[c] < h;
+  const unsigned bal = __ballot_sync(0xffffffffu, is_out);
+  if ((c & 31) == 0 && c < d) below[c >> 5] = (int)bal;
+  if (c < d && magnitudes && publish) magnitudes[(int64_t)u * d + c] = mag[c];
+  __syncthreads();
+  if (c < d) {
+    // ascending position among the outliers / among the inliers (kvcache.py:90-101)
+    int nb = __popc((unsigned)below[c >> 5] & ((1u << (c & 31)) - 1u));
+    for (int w = 0; w < (c >> 5); ++w) nb += __popc((unsigned)below[w]);
+    if (is_out && publish) channels[(int64_t)u * h + nb] = c;
+    src[c] = is_out ? -1 - nb : c - nb;
+  }
+  __syncthreads();
   __syncthreads();                     // barrier init visible; element-wise copies done
   asm volatile(
       "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W_%=;\n}\n" ::"r"(bar)
@@ -645,21 +652,35 @@ int launch_prefill_profile(const void* keys, int dtype, int units, int64_t n0, i
   const size_t ts = dtype_size(sketch_dtype);
   const size_t row_bytes = (size_t)std::max(d - h, h) * ts;          // widest source row
   const int m_total = m_in + m_out;
-  int slices = std::max(1, device_sm_count() / units);
+  // d <= 256: 256-thread CTAs (one thread per channel), 3 resident per SM (28 KB of static
+  // ranking arrays + the staged rows each), so a unit's rows are built by ~3 x SMs / units
+  // CTAs in one wave (C4: 3 slices of 192 rows per unit; one 1024-thread CTA per unit left
+  // 20 SMs idle and ran the latency-bound ranking and the 123 KB staging serially per SM)
+  const int fb_threads = d <= 256 ? 256 : 1024;
+  int slices = std::max(1, device_sm_count() * (fb_threads == 256 ? 3 : 1) / units);
   const int max_rows = std::max(1, (int)((160 * 1024 - 64) / row_bytes) - 1);
   slices = std::max(slices, (m_total + max_rows - 1) / max_rows);
   slices = std::min(slices, m_total);
   const size_t smem_fb = ((size_t)(m_total + slices - 1) / slices + 1) * row_bytes + 64;
+  cudaLaunchAttribute fattr[1];
+  fattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  fattr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t fcfg = {};
+  fcfg.gridDim = dim3(units, slices);
+  fcfg.blockDim = dim3(fb_threads);
+  fcfg.dynamicSmemBytes = smem_fb;
+  fcfg.stream = st;
+  fcfg.attrs = fattr;
+  fcfg.numAttrs = 1;
+  cudaError_t fb_err = cudaSuccess;
   switch (sketch_dtype) {
 #define QJL_PPF(DT)                                                                                     \
   case DT:                                                                                              \
     cudaFuncSetAttribute(k_detect_finish_build<Elem<DT>::T>,                                            \
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fb);                    \
-    k_detect_finish_build<Elem<DT>::T><<<dim3(units, slices), 1024, smem_fb, st>>>(part, nblk, n0, d, h, \
-                                                               channels, mags,                           \
-                                                               (const Elem<DT>::T*)s_in,                 \
-                                                               (const Elem<DT>::T*)s_out, m_in, m_out,   \
-                                                               (Elem<DT>::T*)s_full);                    \
+    fb_err = cudaLaunchKernelEx(&fcfg, k_detect_finish_build<Elem<DT>::T>, (const double*)part, nblk, n0, d, h, \
+                                channels, mags, (const Elem<DT>::T*)s_in, (const Elem<DT>::T*)s_out, m_in,   \
+                                m_out, (Elem<DT>::T*)s_full);                                                \
     break;
     QJL_PPF(QJL_F32)
     QJL_PPF(QJL_F16)
@@ -669,6 +690,10 @@ int launch_prefill_profile(const void* keys, int dtype, int units, int64_t n0, i
     default:
       if (owned) cudaFreeAsync(part, st);
       return QJL_ERR_ARG;
+  }
+  if (fb_err != cudaSuccess) {
+    if (owned) cudaFreeAsync(part, st);
+    return cuda_status(fb_err, "prefill_profile");
   }
   if (owned) cudaFreeAsync(part, st);
   QJL_LAUNCH_CHECK("prefill_profile");

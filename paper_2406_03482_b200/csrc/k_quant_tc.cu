@@ -330,6 +330,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_quant_tc(const __grid_constant_
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // launched with programmatic serialization: the setup above overlaps the previous
+  // kernel's tail (in a prefill, the S_full build); every global read and write follows
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem = *tmem_ptr;
   if (QJL_K1_ZEROACC) {
     // the accumulator buffers start at +0 (each epilogue warp zeroes its lane quadrant of
@@ -765,9 +768,22 @@ static int launch_impl(const void* keys, int64_t n, int64_t kus, const qjl_sketc
   auto kern = k_quant_tc<MT, NC, STAGES, ABF>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
   const int ctas = (int)(P.T < device_sm_count() ? P.T : device_sm_count());
+  // programmatic serialization: the kernel's setup (barriers, TMEM allocation, tensor-map
+  // prefetch) overlaps the previous kernel; it waits for it before touching memory
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = L::kTotal;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   timing_begin(st);
-  kern<<<ctas, kThreads, L::kTotal, st>>>(tk, ts, P);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tk, ts, P);
   timing_end(st);
+  if (e != cudaSuccess) return cuda_status(e, "quantize_keys_tc");
   QJL_LAUNCH_CHECK("quantize_keys_tc");
   return QJL_OK;
 }

@@ -351,7 +351,7 @@ def prefill_oracle_check(cache, K, w, u=0):
     return res
 
 
-def measure_prefill(device, seed, shard_of_units, steps=5, warmup=2, parity=True):
+def measure_prefill(device, seed, shard_of_units, steps=20, warmup=3, parity=True):
     """K1 (config 4: B16 x Hkv8, 8192 new tokens, m = 512 + 64, r = 8, lognormal channel
     scales) over this rank's units: keys/s, TFLOP/s (padded K=128 and useful flops), and the
     whole prefill with the fused prompt profile (F2)."""

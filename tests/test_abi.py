@@ -50,6 +50,12 @@ def test_argument_errors_without_gpu():
     rc = lib.qjl_quantize_keys(ctypes.c_void_p(8), 2, 1, 128, ctypes.byref(sd), None, 0,
                                ctypes.byref(kc), 0, None)
     assert rc == _lib.QJL_ERR_UNSUPPORTED
+    # qjl_scores flags (ABI 3): QJL_DECODE_CHAINED only
+    kc = _lib.KeyCacheDesc(8, None, 8, None, 16, 1, 128, 256, 0, 0)
+    rc = lib.qjl_scores(ctypes.byref(kc), 1, ctypes.c_void_p(8), 2, 1, ctypes.byref(sd), ctypes.c_void_p(8),
+                        ctypes.c_void_p(8), 1 << 20, _lib.QJL_DECODE_DETERMINISTIC, None)
+    assert rc == _lib.QJL_ERR_ARG
+    assert b"flags" in lib.qjl_last_error()
     # temperature must be positive (kvcache.py:335-336)
     assert lib.qjl_softmax_f64(ctypes.c_void_p(8), 1, 1, 0.0, ctypes.c_void_p(8), None) == _lib.QJL_ERR_ARG
 

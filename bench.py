@@ -52,6 +52,7 @@ WORKLOADS = {
 }
 PREFILL = dict(workload="c4_prefill_quantize", batch=16, kv_heads=8, n=8192, d=128, m_in=512,
                m_out=64, h=8, dtype="bf16")
+L2_BYTES = 126_000_000   # B200 L2 (both dies)
 REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x40: "sw_thermal_slowdown",
            0x80: "hw_thermal_slowdown", 0x100: "hw_power_brake_slowdown", 0x2: "applications_clocks",
            0x1: "gpu_idle", 0x20: "sync_boost", 0x200: "display_clock"}
@@ -578,11 +579,17 @@ def run_gpu(args):
     cache = build_cache(w, shard, args.seed, device)
     q = make_queries(w, shard, args.seed, device)
     out = torch.empty(U, w["G"], w["d"], dtype=torch.float32, device=device)
+    # timing rule: a step's inputs must come from HBM.  A shard whose packed cache fits the
+    # 126 MB L2 is rotated over enough replicas (own record buffers, same contents) that a
+    # replica's records are evicted before it is read again (combined footprint >= 1.5 x L2)
+    shard_bytes = U * w["n"] * bytes_per_token_head(w)
+    n_rep = 1 if shard_bytes > L2_BYTES else min(96, -(-int(1.5 * L2_BYTES) // max(shard_bytes, 1)))
+    caches = [cache] + [cache.replica() for _ in range(n_rep - 1)]
     torch.cuda.synchronize()
 
     # ---- value: back-to-back decode steps, device-resident inputs (chained launches)
     for i in range(args.warmup):
-        cache.decode(q, out=out, chained=i > 0)
+        caches[i % n_rep].decode(q, out=out, chained=i > 0)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -591,12 +598,52 @@ def run_gpu(args):
     with ClockSampler(local) as clk:
         e0.record()
         for i in range(args.steps):
-            cache.decode(q, out=out, chained=True)
+            caches[i % n_rep].decode(q, out=out, chained=True)
         e1.record()
         torch.cuda.synchronize()
     t_ms = e0.elapsed_time(e1)
     if world > 1:
         dist.barrier()
+
+    # ---- the same K steps replayed from one CUDA graph (secondary figure): short steps
+    # (< ~30 us) are bound by the host's launch rate through Python + ctypes, which the graph
+    # removes; the PDL edges between the kernels are captured with them
+    graph_info = None
+    if world == 1 and not args.no_extras:
+        try:
+            gq, gout = q.clone(), torch.empty_like(out)
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):               # allocations of the launch path, warm
+                for i in range(min(3, args.steps)):
+                    caches[i % n_rep].decode(gq, out=gout, chained=i > 0)
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for i in range(args.steps):
+                    caches[i % n_rep].decode(gq, out=gout, chained=i > 0)
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 5
+            g0.record()
+            for _ in range(reps):
+                g.replay()
+            g1.record()
+            torch.cuda.synchronize()
+            g_ms = g0.elapsed_time(g1) / (reps * args.steps)
+            ref_out = cache.decode(q)
+            graph_info = {"ms_per_step": g_ms,
+                          "gbs": U * w["n"] * bytes_per_token_head(w) / (g_ms * 1e-3) / 1e9,
+                          "output_ok": bool(torch.equal(gout, ref_out)),
+                          "note": f"{args.steps} chained steps captured in one CUDA graph (PDL edges kept), "
+                                  f"replayed {reps} times; eager `value` launches every step from Python"}
+            del g
+        except Exception as e:                          # report, never hide: `value` stays eager
+            graph_info = {"error": f"{type(e).__name__}: {e}"[:300]}
+            torch.cuda.synchronize()
 
     # ---- roofline: the decode kernel alone, in a chain of back-to-back decodes
     kern_ms = cache.bench_decode_kernel(q, reps=max(args.steps, 20))
@@ -635,7 +682,7 @@ def run_gpu(args):
                 comp.wait_event(d2h_done[b])            # od[b] / oh[b] were read back two steps ago
             # chained (N = 1): the previous kernel on this stream is the previous step's
             # decode, and this step's query upload is complete (event wait above)
-            cache.decode(qd[b], out=od[b], chained=(i > 0 and world == 1))
+            caches[i % n_rep].decode(qd[b], out=od[b], chained=(i > 0 and world == 1))
             full = gather_units(od[b], shard) if world > 1 else od[b]
             dec_done[b].record(comp)
             with torch.cuda.stream(copy):               # read this step's (gathered) output back
@@ -665,11 +712,11 @@ def run_gpu(args):
     if world == 1:
         ohz = torch.empty(out.shape, dtype=out.dtype).pin_memory()
         for i in range(args.warmup):
-            cache.decode(qh, out=ohz, chained=i > 0)
+            caches[i % n_rep].decode(qh, out=ohz, chained=i > 0)
         torch.cuda.synchronize()
         e2.record()
-        for _ in range(args.steps):
-            cache.decode(qh, out=ohz, chained=True)
+        for i in range(args.steps):
+            caches[i % n_rep].decode(qh, out=ohz, chained=True)
         e3.record()
         torch.cuda.synchronize()
         zc_ms = e2.elapsed_time(e3)
@@ -687,7 +734,7 @@ def run_gpu(args):
 
         def hybrid_steps(k):
             for i in range(k):
-                cache.decode(qh, out=odh[i], chained=i > 0)
+                caches[i % n_rep].decode(qh, out=odh[i], chained=i > 0)
                 evs[i].record(comp)
                 with torch.cuda.stream(copy):
                     copy.wait_event(evs[i])
@@ -741,9 +788,12 @@ def run_gpu(args):
                    "parallelism": f"KV heads sharded over {world} rank(s) ({U} units each), no data-path "
                                   f"collective",
                    "l2": f"inputs larger than L2 ({alg_bytes_rank / 1e6:.0f} MB/step/rank vs 126 MB)"
-                         if alg_bytes_rank > 126e6 else
-                         f"{alg_bytes_rank / 1e6:.0f} MB/step/rank fits the 126 MB L2 (strong-scaled "
-                         f"shard; not flushed)"},
+                         if n_rep == 1 else
+                         f"{alg_bytes_rank / 1e6:.0f} MB/step/rank fits the 126 MB L2: value and e2e rotate "
+                         f"the steps over {n_rep} replicas of the packed cache ({n_rep * alg_bytes_rank / 1e6:.0f} "
+                         f"MB > L2), so every step reads HBM; roofline.kernel_ms and scores_only time one "
+                         f"replica (L2-resident)",
+                   "cache_replicas": n_rep},
         "e2e": {"value": e2e_val, "unit": "GB/s",
                 "h2d_bytes_per_step": int(q.numel() * q.element_size()),
                 "d2h_bytes_per_step": int(oh.numel() * oh.element_size()),
@@ -762,6 +812,7 @@ def run_gpu(args):
                      "deterministic_schedule_kernel_ms": det_ms,
                      "traffic": load_traffic(w["workload"])},
         "gpu_launches": 2 * args.steps,
+        "graph_replay": graph_info,
         "clocks": clk.summary(),
     }
     if zc_ms is not None:

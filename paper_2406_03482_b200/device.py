@@ -135,25 +135,7 @@ class DeviceKeyCache:
             self.record_bytes = rec
             self.record_offsets = list(offs)
             tiles = capacity // 128
-            self.records = torch.zeros(units, tiles, rec, dtype=torch.uint8, device=dev)
-            self._fields = {}
-
-            def fld(i, width, dtype=torch.uint8):
-                o = self.record_offsets[i]
-                v = self.records[:, :, o:o + 128 * width * (torch.finfo(dtype).bits // 8
-                                                             if dtype.is_floating_point else 1)]
-                v = v.view(dtype) if dtype != torch.uint8 else v
-                return v.view(units, tiles, 128, width)
-
-            self._fields["bits_in"] = fld(_lib.QJL_REC_BITS_IN, m_in // 8)
-            self._fields["norm_in"] = fld(_lib.QJL_REC_NORM_IN, 1, torch.float16)
-            if m_out:
-                self._fields["bits_out"] = fld(_lib.QJL_REC_BITS_OUT, m_out // 8)
-                self._fields["norm_out"] = fld(_lib.QJL_REC_NORM_OUT, 1, torch.float16)
-            if p2t:
-                self._fields["v_codes"] = fld(_lib.QJL_REC_CODES, d // 4)
-                self._fields["v_zero"] = fld(_lib.QJL_REC_ZERO, Gv, torch.float16)
-                self._fields["v_scale"] = fld(_lib.QJL_REC_SCALE, Gv, torch.float16)
+            self._bind_records(torch.zeros(units, tiles, rec, dtype=torch.uint8, device=dev))
         else:
             self.record_bytes = 0
             self._fields = None
@@ -168,6 +150,44 @@ class DeviceKeyCache:
                 self._v_scale = torch.zeros(units, capacity, Gv, dtype=torch.float32, device=dev)
 
     # ------------------------------------------------------------ fields
+    def _bind_records(self, records: torch.Tensor) -> None:
+        """Point the cache at a [units, tiles, record_bytes] record buffer and build the
+        per-field views into it (offsets from qjl_tile_record)."""
+        s = self.shape
+        units, tiles = s.units, s.capacity // 128
+        Gv = s.d // self.value_group
+        self.records = records
+        self._fields = {}
+
+        def fld(i, width, dtype=torch.uint8):
+            o = self.record_offsets[i]
+            v = records[:, :, o:o + 128 * width * (torch.finfo(dtype).bits // 8
+                                                    if dtype.is_floating_point else 1)]
+            v = v.view(dtype) if dtype != torch.uint8 else v
+            return v.view(units, tiles, 128, width)
+
+        self._fields["bits_in"] = fld(_lib.QJL_REC_BITS_IN, s.m_in // 8)
+        self._fields["norm_in"] = fld(_lib.QJL_REC_NORM_IN, 1, torch.float16)
+        if s.m_out:
+            self._fields["bits_out"] = fld(_lib.QJL_REC_BITS_OUT, s.m_out // 8)
+            self._fields["norm_out"] = fld(_lib.QJL_REC_NORM_OUT, 1, torch.float16)
+        if self.value_layout == "p2t" and self.with_values:
+            self._fields["v_codes"] = fld(_lib.QJL_REC_CODES, s.d // 4)
+            self._fields["v_zero"] = fld(_lib.QJL_REC_ZERO, Gv, torch.float16)
+            self._fields["v_scale"] = fld(_lib.QJL_REC_SCALE, Gv, torch.float16)
+
+    def replica(self) -> "DeviceKeyCache":
+        """A second cache with the same contents in its own record buffer (same sketches,
+        channels and workspace).  bench.py rotates decodes over replicas so that a shard
+        smaller than L2 is still read from HBM."""
+        if not self.tiled:
+            raise ValueError("replica() is for tile-major caches")
+        import copy
+
+        r = copy.copy(self)
+        r._bind_records(self.records.clone())
+        return r
+
     def field_view(self, name: str) -> torch.Tensor:
         """Writable view of one cache field: [units, tiles, 128, width] (tile-major) or
         the dense [units, capacity, ...] array (rows layout)."""

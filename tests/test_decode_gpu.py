@@ -107,6 +107,23 @@ def test_determinism_and_chaining(cuda):
     assert _close(o1, d1)
 
 
+def test_replica_decodes_identically(cuda):
+    """DeviceKeyCache.replica(): same contents in its own record buffer (bench.py rotates
+    steps over replicas so sub-L2 shards are read from HBM); decodes and logits are bitwise
+    those of the original, also chained across replicas, and writes do not alias."""
+    c, q = make_cache(8, 3000, 4, 8, 256, 64, seed=5)
+    r = c.replica()
+    assert r.records.data_ptr() != c.records.data_ptr() and torch.equal(r.records, c.records)
+    assert r.key_desc().bits_in != c.key_desc().bits_in
+    o = c.decode(q).clone()
+    o1 = r.decode(q, chained=True).clone()
+    o2 = c.decode(q, chained=True).clone()
+    assert torch.equal(o, o1) and torch.equal(o, o2)
+    assert torch.equal(c.scores(q), r.scores(q))
+    r.records.zero_()
+    assert torch.equal(c.decode(q), o)
+
+
 def test_scores_chaining(cuda):
     """qjl_scores with QJL_DECODE_CHAINED (PDL: the query sketch overlaps the previous score
     or decode kernel) writes the same logits as unchained calls, including after a decode

@@ -124,6 +124,35 @@ def test_replica_decodes_identically(cuda):
     assert torch.equal(c.decode(q), o)
 
 
+def test_decode_captures_into_a_cuda_graph(cuda):
+    """The launch path allocates nothing and synchronises nothing once its workspace exists,
+    so a serving loop can capture chained steps (decode and decode_step's PDL edges included)
+    in one CUDA graph; the replay is bitwise the eager result and follows new query contents."""
+    c, q = make_cache(8, 3000, 4, 8, 256, 64, seed=9)
+    out = torch.empty(8, 4, 128, device="cuda")
+    ref = c.decode(q).clone()                       # also sizes the workspace
+    gq = q.clone()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        c.decode(gq, out=out)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(3):
+            c.decode(gq, out=out, chained=i > 0)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    q2 = torch.randn_like(q.float()).to(q.dtype)
+    gq.copy_(q2)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, c.decode(q2))
+
+
 def test_scores_chaining(cuda):
     """qjl_scores with QJL_DECODE_CHAINED (PDL: the query sketch overlaps the previous score
     or decode kernel) writes the same logits as unchained calls, including after a decode

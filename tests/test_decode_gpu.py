@@ -126,8 +126,8 @@ def test_replica_decodes_identically(cuda):
 
 def test_decode_captures_into_a_cuda_graph(cuda):
     """The launch path allocates nothing and synchronises nothing once its workspace exists,
-    so a serving loop can capture chained steps (decode and decode_step's PDL edges included)
-    in one CUDA graph; the replay is bitwise the eager result and follows new query contents."""
+    so a serving loop can capture chained decode steps (their PDL edges included) in one
+    CUDA graph; the replay is bitwise the eager result and follows new query contents."""
     c, q = make_cache(8, 3000, 4, 8, 256, 64, seed=9)
     out = torch.empty(8, 4, 128, device="cuda")
     ref = c.decode(q).clone()                       # also sizes the workspace
